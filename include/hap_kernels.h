@@ -1,0 +1,160 @@
+/*
+ * hap_kernels.h — C-ABI of the B200 (sm_100a) HAP MoE-block executor.
+ *
+ * The reference (moeplan, /root/reference/pkg/src/moeplan) has NO forward
+ * implementation: it only *models* these ops through its FLOP and
+ * collective-volume formulas.  Each entry point below is the executable
+ * counterpart of one modelled term, cited per function:
+ *   - attention_flops  arch.py:145-162  -> hap_gemm_bf16 (QKV/O projections),
+ *                                          hap_attn_prefill / hap_attn_decode
+ *   - expert_flops     arch.py:165-178  -> hap_router_topk (router term),
+ *                                          hap_grouped_gemm_bf16 (gate/up/down)
+ *   - comm_volume EP rows strategies.py:334-340 -> hap_moe_permute /
+ *                                          hap_moe_combine (dispatch/combine
+ *                                          token re-layout around the a2a)
+ *
+ * Conventions (all functions):
+ *   - every pointer is a DEVICE pointer owned by the caller; the library never
+ *     allocates, frees, or synchronises; calls are stream-ordered on `stream`
+ *     (a cudaStream_t passed as void*) and CUDA-graph capturable;
+ *   - bf16 tensors are row-major with the given leading dimension (elements);
+ *   - return 0 (HAP_OK) or a negative hap_status.  Argument errors are
+ *     detected before any launch.
+ */
+#ifndef HAP_KERNELS_H_
+#define HAP_KERNELS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HAP_OK = 0,
+  HAP_ERR_INVALID_ARG = -1, /* bad shape / null pointer / out-of-range value */
+  HAP_ERR_UNSUPPORTED = -2, /* shape legal but not supported by this build   */
+  HAP_ERR_MISALIGNED = -3,  /* pointer / leading dimension alignment          */
+  HAP_ERR_LAUNCH = -4,      /* CUDA launch failure                            */
+  HAP_ERR_WORKSPACE = -5,   /* workspace too small                            */
+  HAP_ERR_DRIVER = -6       /* driver entry point (cuTensorMapEncodeTiled)    */
+} hap_status;
+
+/* GEMM epilogues */
+#define HAP_EPI_STORE 0  /* C = acc (+bias) (+residual)                        */
+#define HAP_EPI_SWIGLU 1 /* C = silu(acc[:, gate]) * acc[:, up] per tile        */
+
+const char* hap_status_string(int status);
+int hap_abi_version(void);
+
+/* Largest SwiGLU tile half-width (multiple of 8, <= 128) dividing `inter_dim`;
+ * the gate/up weight interleave (see hap_grouped_gemm_bf16) must use it. */
+int64_t hap_swiglu_half_width(int64_t inter_dim);
+
+/*
+ * Grouped GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA), bf16 in,
+ * fp32 accumulate, bf16 out.
+ *
+ *   for g in [0, n_groups): rows r in [seg[g], seg[g+1]) of A:
+ *       C[r, :] = epilogue( A[r, :K] . B[g*N:(g+1)*N, :K]^T )
+ *
+ * A: [a_rows, K] (lda), B: [n_groups*N, K] contiguous (nn.Linear weight
+ * layout, one block of N rows per group), C: [a_rows, out_cols] (ldc).
+ * seg: device int32[n_groups+1] (NULL => one group spanning all a_rows).
+ * Segments need not be aligned; rows outside every segment are untouched.
+ *
+ * HAP_EPI_SWIGLU: B rows are interleaved in blocks of 2*swiglu_half:
+ * block j = [gate rows j*hw..j*hw+hw-1 ; up rows j*hw..j*hw+hw-1] with
+ * hw = swiglu_half; out_cols = N/2 and C[r, j*hw+i] = silu(g)*u.
+ * HAP_EPI_STORE: optional bias (bf16[N]) and residual (bf16, ldr) are added in
+ * fp32 before the single bf16 rounding.
+ *
+ * Replaces: the per-expert gated-MLP FLOP term of expert_flops (arch.py:174-176)
+ * and the projection term of attention_flops (arch.py:157-160).
+ */
+int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                          int64_t n_groups, int64_t N, const int32_t* seg, void* C, int64_t ldc,
+                          int32_t epilogue, int64_t swiglu_half, const void* bias, const void* residual,
+                          int64_t ldr, void* stream);
+
+/*
+ * Router: logits[t,e] = x[t,:] . w[e,:] (fp32, fixed reduction order: lane l
+ * of a warp accumulates 8-element chunks l, l+32, ... sequentially, then a
+ * xor-butterfly 16,8,4,2,1), softmax in fp32, top-k selected on logits with
+ * ties to the lower expert index, weights = softmax probabilities of the
+ * selected experts, renormalised to sum 1 when `renormalize`.
+ * If has_shared_gate, w has n_experts+1 rows and row n_experts is the
+ * shared-expert gate: shared_gate[t] = sigmoid(x[t] . w[E]) (fp32).
+ * logits_out (fp32 [T, n_experts]) is optional.
+ * Requires h % 256 == 0, n_experts <= 256, top_k <= 32.
+ * Replaces: the router term 2*T*h*E of expert_flops (arch.py:177).
+ */
+int hap_router_topk(const void* x, int64_t T, int64_t h, const void* w, int64_t n_experts, int64_t top_k,
+                    int32_t renormalize, int32_t has_shared_gate, int32_t* topk_idx, float* topk_w,
+                    float* shared_gate, float* logits_out, void* stream);
+
+/*
+ * Stable counting-sort permute (scan + scatter).  Row r of the logical input
+ * (r in [0, R)) carries expert id e_r = expert_of_row[r] and payload
+ * x[r / src_row_div, :h].  Rows are placed at
+ *     dst_of_row[r] = seg[e_r] + #{r' < r : e_r' == e_r}
+ * i.e. sorted by (expert, r) — with R = T*k and src_row_div = k this is the
+ * canonical (expert, token, slot) order.  seg (int32[n_experts+1]) receives
+ * the exclusive prefix of per-expert counts.  Rows with e_r outside
+ * [0, n_experts) are dropped (dst_of_row = -1).  x_out may be NULL (index
+ * only).  Bit-exact by construction (no atomics on the ordering path).
+ * Workspace: hap_moe_permute_workspace_bytes(R, n_experts).
+ */
+size_t hap_moe_permute_workspace_bytes(int64_t R, int64_t n_experts);
+int hap_moe_permute(const int32_t* expert_of_row, int64_t R, int64_t n_experts, const void* x,
+                    int64_t src_row_div, int64_t h, void* x_out, int32_t* dst_of_row, int32_t* seg,
+                    void* workspace, size_t ws_bytes, void* stream);
+
+/*
+ * Weighted combine (unpermute):
+ *   out[t] = sum_j w[t,j] * y[dst[t*k+j]]  (+ residual[t]) (+ sg[t] * shared_y[t])
+ * fp32 accumulation in slot order, one bf16 rounding.  dst < 0 => slot skipped.
+ * residual / shared_y / shared_gate may be NULL.
+ */
+int hap_moe_combine(const void* y, const int32_t* dst_of_row, const float* topk_w, int64_t T, int64_t k,
+                    int64_t h, const void* residual, const void* shared_y, const float* shared_gate, void* out,
+                    void* stream);
+
+/* RMSNorm (fp32 statistics): out = w * (x * rsqrt(mean(x^2) + eps)). */
+int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, const void* w, float eps, void* out,
+                int64_t ldo, void* stream);
+
+/*
+ * In-place rotary embedding (rotate-half convention) on the q and k heads of
+ * a fused qkv row buffer: row t = [q (n_q*d) | k (n_kv*d) | v (n_kv*d)],
+ * leading dimension ld.  positions: int32[T].  inv_freq[i] = theta^(-2i/d).
+ */
+int hap_rope_qk(void* qkv, int64_t T, int64_t ld, int64_t n_q_heads, int64_t n_kv_heads, int64_t head_dim,
+                const int32_t* positions, float theta, void* stream);
+
+/*
+ * Causal (or full) GQA prefill attention, bf16 in/out, fp32 softmax.
+ * Token (s, i) = row s*seq_len + i.  q/k/v/out addressed by leading dims;
+ * head h of a row starts at column h*head_dim.  head_dim == 128.
+ * Replaces: score+value term 4*n*kv_len*h of attention_flops (arch.py:161).
+ */
+int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                     void* out, int64_t ldo, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
+                     int64_t n_kv_heads, int64_t head_dim, float scale, int32_t causal, void* stream);
+
+/*
+ * Append one token's k/v (from a fused qkv row buffer) into a [B, max_len,
+ * n_kv, d] cache at position pos[b], then split-KV GQA decode attention of
+ * q over cache rows [0, pos[b]] for each sequence b.
+ * Workspace: hap_attn_decode_workspace_bytes(B, n_q_heads, head_dim, max_len).
+ */
+size_t hap_attn_decode_workspace_bytes(int64_t B, int64_t n_q_heads, int64_t head_dim, int64_t max_len);
+int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, void* v_cache, int64_t max_len,
+                    const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads, int64_t head_dim,
+                    float scale, void* out, int64_t ldo, void* workspace, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HAP_KERNELS_H_ */

@@ -1,0 +1,355 @@
+// Grouped / dense bf16 GEMM on sm_100a tensor cores.
+//
+// Persistent, warp-specialised kernel (one CTA per SM):
+//   warp 0      TMA producer   (A 128x64 and B BNx64 boxes, 128B swizzle)
+//   warp 1      MMA issuer     (one thread, tcgen05.mma kind::f16, M=128, N=BN, K=16)
+//   warp 2      TMEM allocator (2 x 256 fp32 accumulator columns)
+//   warps 4..7  epilogue       (tcgen05.ld -> fp32 math -> bf16 stores)
+// Pipelines: smem ring full/empty (TMA <-> MMA) and a double-buffered TMEM
+// accumulator tfull/tempty (MMA <-> epilogue), so the epilogue of tile i
+// overlaps the main loop of tile i+1.
+//
+// The tile list is derived ON DEVICE from the per-group row offsets `seg`
+// (expert segments produced by hap_moe_permute), so no host synchronisation is
+// needed between the router and the expert GEMMs.  Tiles are ordered m-fastest
+// inside each (group, n-block) so concurrently resident CTAs share the weight
+// tile through L2.
+//
+// Models: expert_flops (reference arch.py:165-178) gated-MLP term and the
+// projection term of attention_flops (arch.py:157-160).
+#include "common.cuh"
+
+namespace hap {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
+constexpr int kMaxBN = 256;
+constexpr int kStages = 4;
+constexpr int kMaxGroups = 256;
+constexpr int kAccCols = 256;  // TMEM columns per accumulator buffer
+constexpr int kThreads = 256;
+constexpr int kABytes = BM * BK * 2;       // 16 KB
+constexpr int kBBytes = kMaxBN * BK * 2;   // 32 KB
+constexpr int kSmemBytes = kStages * (kABytes + kBBytes) + 1024;
+
+struct Params {
+  int32_t a_rows;
+  int32_t K;
+  int32_t N;         // B rows per group
+  int32_t n_groups;
+  int32_t BN;        // n tile (multiple of 16, <= 256)
+  int32_t epi;
+  int32_t hw;        // swiglu half width (== BN/2 for swiglu)
+  int32_t out_cols;  // valid output columns
+  const int32_t* seg;
+  __nv_bfloat16* C;
+  int64_t ldc;
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* resid;
+  int64_t ldr;
+};
+
+struct TileCoord {
+  int32_t g, m0, m_end, n_blk;
+};
+
+// Map a linear tile index to (group, row range, n block).  tile_start has
+// n_groups+1 prefix entries; m-blocks vary fastest.
+__device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, const int32_t* seg, int n_groups,
+                                              int n_blocks) {
+  int lo = 0, hi = n_groups - 1;
+  while (lo < hi) {  // last g with tile_start[g] <= t
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_start[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  const int g = lo;
+  const int local = t - tile_start[g];
+  const int rows = seg[g + 1] - seg[g];
+  const int m_blocks = (rows + BM - 1) / BM;
+  TileCoord c;
+  c.g = g;
+  c.m0 = seg[g] + (local % m_blocks) * BM;
+  c.m_end = seg[g + 1];
+  c.n_blk = local / m_blocks;
+  return c;
+}
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + kStages * kABytes;
+
+  __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar[2];
+  __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ int32_t seg_s[kMaxGroups + 1];
+  __shared__ int32_t tile_start_s[kMaxGroups + 1];
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_groups = p.n_groups;
+  const int n_blocks = (p.N + p.BN - 1) / p.BN;
+
+  // ---- setup: segment table, tile prefix, barriers, TMEM
+  for (int i = threadIdx.x; i <= n_groups; i += blockDim.x) {
+    seg_s[i] = p.seg ? p.seg[i] : (i == 0 ? 0 : p.a_rows);
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(&tmem_base_s, 2 * kAccCols);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int g = 0; g < n_groups; ++g) {
+      tile_start_s[g] = acc;
+      const int rows = seg_s[g + 1] - seg_s[g];
+      acc += ((rows + BM - 1) / BM) * n_blocks;
+    }
+    tile_start_s[n_groups] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+  const int total_tiles = tile_start_s[n_groups];
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const uint32_t tx_bytes = kABytes + p.BN * BK * 2;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const TileCoord c = map_tile(t, tile_start_s, seg_s, n_groups, n_blocks);
+        const int b_row = c.g * p.N + c.n_blk * p.BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
+          tma_load_2d(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, c.m0, kEvictNormal);
+          tma_load_2d(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(BM, p.BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint64_t da = make_sdesc_sw128(smem_u32(smA + stage * kABytes));
+          const uint64_t db = make_sdesc_sw128(smem_u32(smB + stage * kBBytes));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // +32 bytes per K=16 step inside the 128B swizzle atom (>>4 => +2)
+            umma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull_bar[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue =================
+    const int q = warp & 3;  // TMEM lane quadrant accessible by this warp
+    int it = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+      const TileCoord c = map_tile(t, tile_start_s, seg_s, n_groups, n_blocks);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = c.m0 + q * 32 + lane;
+      const bool row_ok = row < c.m_end;
+      const uint32_t t_row = tmem_base + acc * kAccCols + ((uint32_t)(q * 32) << 16);
+      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+      if (p.epi == HAP_EPI_SWIGLU) {
+        const int hw = p.hw;
+        const int col0 = c.n_blk * hw;
+        for (int j = 0; j < hw; j += 8) {
+          uint32_t g[8], u[8];
+          tmem_ld_x8(t_row + j, g);
+          tmem_ld_x8(t_row + hw + j, u);
+          tmem_ld_wait();
+          if (row_ok && col0 + j < p.out_cols) {
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+              const float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+              o[i] = pack_bf16x2(a0, a1);
+            }
+            *reinterpret_cast<uint4*>(crow + col0 + j) = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        }
+      } else {
+        const int col0 = c.n_blk * p.BN;
+        for (int j = 0; j < p.BN; j += 32) {
+          uint32_t v[32];
+          tmem_ld_x32(t_row + j, v);
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              const int col = col0 + j + s * 8;
+              if (col < p.out_cols) {
+                float f[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[s * 8 + i]);
+                if (p.bias) {
+                  const uint4 b = *reinterpret_cast<const uint4*>(p.bias + col);
+                  const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    const float2 bb = unpack_bf16x2(bw[i]);
+                    f[2 * i] += bb.x;
+                    f[2 * i + 1] += bb.y;
+                  }
+                }
+                if (p.resid) {
+                  const uint4 r = *reinterpret_cast<const uint4*>(p.resid + (int64_t)row * p.ldr + col);
+                  const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    const float2 rr = unpack_bf16x2(rw[i]);
+                    f[2 * i] += rr.x;
+                    f[2 * i + 1] += rr.y;
+                  }
+                }
+                uint32_t o[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) o[i] = pack_bf16x2(f[2 * i], f[2 * i + 1]);
+                *reinterpret_cast<uint4*>(crow + col) = make_uint4(o[0], o[1], o[2], o[3]);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * kAccCols);
+  }
+}
+
+// Pick the n tile: the largest multiple of 16 <= 256 that divides N (so no
+// weight tile straddles two groups' rows wastefully); fall back to 256 with
+// column masking.
+static int pick_bn(int64_t N) {
+  for (int bn = 256; bn >= 64; bn -= 16)
+    if (N % bn == 0) return bn;
+  return N < 256 ? (int)((N + 15) / 16 * 16) : 256;
+}
+
+}  // namespace gemm
+}  // namespace hap
+
+using namespace hap;
+
+extern "C" int64_t hap_swiglu_half_width(int64_t inter_dim) {
+  if (inter_dim <= 0 || inter_dim % 8) return -1;
+  for (int64_t hw = 128; hw >= 8; hw -= 8)
+    if (inter_dim % hw == 0) return hw;
+  return -1;
+}
+
+extern "C" int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                                     int64_t n_groups, int64_t N, const int32_t* seg, void* C, int64_t ldc,
+                                     int32_t epilogue, int64_t swiglu_half, const void* bias, const void* residual,
+                                     int64_t ldr, void* stream) {
+  using namespace hap::gemm;
+  if (!A || !B || !C || a_rows < 0 || K <= 0 || N <= 0 || n_groups <= 0) return HAP_ERR_INVALID_ARG;
+  if (n_groups > kMaxGroups || (n_groups > 1 && !seg)) return HAP_ERR_INVALID_ARG;
+  if (a_rows > INT32_MAX || N * n_groups > INT32_MAX || K > INT32_MAX) return HAP_ERR_UNSUPPORTED;
+  if (K % 8 || lda % 8 || ldc % 8 || N % 8 || lda < K) return HAP_ERR_MISALIGNED;
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+    return HAP_ERR_MISALIGNED;
+  if (a_rows == 0) return HAP_OK;
+  Params p{};
+  p.a_rows = (int32_t)a_rows;
+  p.K = (int32_t)K;
+  p.N = (int32_t)N;
+  p.n_groups = (int32_t)n_groups;
+  p.epi = epilogue;
+  p.seg = seg;
+  p.C = reinterpret_cast<__nv_bfloat16*>(C);
+  p.ldc = ldc;
+  if (epilogue == HAP_EPI_SWIGLU) {
+    if (bias || residual) return HAP_ERR_UNSUPPORTED;
+    if (swiglu_half <= 0 || swiglu_half > 128 || swiglu_half % 8 || N % (2 * swiglu_half))
+      return HAP_ERR_INVALID_ARG;
+    p.hw = (int32_t)swiglu_half;
+    p.BN = (int32_t)(2 * swiglu_half);
+    if (p.BN % 16) return HAP_ERR_UNSUPPORTED;
+    p.out_cols = (int32_t)(N / 2);
+    if (ldc < p.out_cols) return HAP_ERR_INVALID_ARG;
+  } else if (epilogue == HAP_EPI_STORE) {
+    p.BN = pick_bn(N);
+    p.out_cols = (int32_t)N;
+    if (ldc < N) return HAP_ERR_INVALID_ARG;
+    if (residual && (ldr % 8 || ldr < N || (reinterpret_cast<uintptr_t>(residual) & 15))) return HAP_ERR_MISALIGNED;
+    if (bias && (reinterpret_cast<uintptr_t>(bias) & 15)) return HAP_ERR_MISALIGNED;
+    p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+    p.resid = reinterpret_cast<const __nv_bfloat16*>(residual);
+    p.ldr = ldr;
+  } else {
+    return HAP_ERR_INVALID_ARG;
+  }
+
+  CUtensorMap tmA, tmB;
+  if (!encode_tmap_2d_bf16(&tmA, A, (uint64_t)K, (uint64_t)a_rows, (uint64_t)lda * 2, BK, BM, true))
+    return HAP_ERR_DRIVER;
+  if (!encode_tmap_2d_bf16(&tmB, B, (uint64_t)K, (uint64_t)(n_groups * N), (uint64_t)K * 2, BK, p.BN, true))
+    return HAP_ERR_DRIVER;
+
+  static int configured = 0;
+  if (!configured) {
+    if (configure_smem((const void*)grouped_gemm_kernel, kSmemBytes) != 0) return HAP_ERR_LAUNCH;
+    configured = 1;
+  }
+  // Upper bound on tiles without reading seg on the host.
+  const int64_t n_blocks = (N + p.BN - 1) / p.BN;
+  const int64_t max_tiles = ((a_rows + BM - 1) / BM + (n_groups - 1)) * n_blocks;
+  const int grid = (int)(max_tiles < kNumSMs ? max_tiles : kNumSMs);
+  grouped_gemm_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tmA, tmB, p);
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
+}

@@ -1,0 +1,60 @@
+// Host-side helpers shared by all kernels: TMA descriptor encoding through the
+// driver entry point, dynamic shared-memory opt-in, status strings.
+#include <mutex>
+
+#include "common.cuh"
+
+namespace hap {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                         uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer > 0 ? outer : 1};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int configure_smem(const void* kernel, int bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace hap
+
+extern "C" const char* hap_status_string(int status) {
+  switch (status) {
+    case HAP_OK: return "ok";
+    case HAP_ERR_INVALID_ARG: return "invalid argument";
+    case HAP_ERR_UNSUPPORTED: return "unsupported shape";
+    case HAP_ERR_MISALIGNED: return "misaligned pointer or leading dimension";
+    case HAP_ERR_LAUNCH: return "CUDA launch failure";
+    case HAP_ERR_WORKSPACE: return "workspace too small";
+    case HAP_ERR_DRIVER: return "driver entry point unavailable (cuTensorMapEncodeTiled)";
+    default: return "unknown status";
+  }
+}
+
+extern "C" int hap_abi_version(void) { return 1; }
