@@ -56,12 +56,16 @@ int64_t hap_swiglu_half_width(int64_t inter_dim);
  * Grouped GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA), bf16 in,
  * fp32 accumulate, bf16 out.
  *
- *   for g in [0, n_groups): rows r in [seg[g], seg[g+1]) of A:
+ *   for s in [0, n_segs): g = seg_group ? seg_group[s] : s;
+ *       rows r in [seg[s], seg[s+1]) of A:
  *       C[r, :] = epilogue( A[r, :K] . B[g*N:(g+1)*N, :K]^T )
  *
  * A: [a_rows, K] (lda), B: [n_groups*N, K] contiguous (nn.Linear weight
  * layout, one block of N rows per group), C: [a_rows, out_cols] (ldc).
- * seg: device int32[n_groups+1] (NULL => one group spanning all a_rows).
+ * seg: device int32[n_segs+1] row offsets (NULL => one segment spanning all
+ * a_rows); seg_group: device int32[n_segs] weight group per segment (NULL =>
+ * identity, n_segs == n_groups).  Several segments may share a group (EP:
+ * rows received from different source ranks for the same local expert).
  * Segments need not be aligned; rows outside every segment are untouched.
  *
  * HAP_EPI_SWIGLU: B rows are interleaved in blocks of 2*swiglu_half:
@@ -74,20 +78,22 @@ int64_t hap_swiglu_half_width(int64_t inter_dim);
  * and the projection term of attention_flops (arch.py:157-160).
  */
 int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
-                          int64_t n_groups, int64_t N, const int32_t* seg, void* C, int64_t ldc,
-                          int32_t epilogue, int64_t swiglu_half, const void* bias, const void* residual,
-                          int64_t ldr, void* stream);
+                          int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
+                          const int32_t* seg_group, void* C, int64_t ldc, int32_t epilogue,
+                          int64_t swiglu_half, const void* bias, const void* residual, int64_t ldr,
+                          void* stream);
 
 /*
- * Router: logits[t,e] = x[t,:] . w[e,:] (fp32, fixed reduction order: lane l
- * of a warp accumulates 8-element chunks l, l+32, ... sequentially, then a
- * xor-butterfly 16,8,4,2,1), softmax in fp32, top-k selected on logits with
- * ties to the lower expert index, weights = softmax probabilities of the
- * selected experts, renormalised to sum 1 when `renormalize`.
+ * Router: logits[t,e] = x[t,:] . w[e,:] in fp32 with a FIXED reduction
+ * order — acc = fma(x[t,j], w[e,j], acc) for j = 0..h-1 sequentially (the
+ * bf16*bf16 products are exact in fp32, so this equals the sequential fp32 sum
+ * of products the oracle computes) — softmax in fp32, top-k selected on
+ * logits with ties to the lower expert index, weights = softmax probabilities
+ * of the selected experts, renormalised to sum 1 when `renormalize`.
  * If has_shared_gate, w has n_experts+1 rows and row n_experts is the
  * shared-expert gate: shared_gate[t] = sigmoid(x[t] . w[E]) (fp32).
  * logits_out (fp32 [T, n_experts]) is optional.
- * Requires h % 256 == 0, n_experts <= 256, top_k <= 32.
+ * Requires h % 256 == 0, n_experts + has_shared_gate <= 72, top_k <= 32.
  * Replaces: the router term 2*T*h*E of expert_flops (arch.py:177).
  */
 int hap_router_topk(const void* x, int64_t T, int64_t h, const void* w, int64_t n_experts, int64_t top_k,
@@ -113,13 +119,16 @@ int hap_moe_permute(const int32_t* expert_of_row, int64_t R, int64_t n_experts, 
 
 /*
  * Weighted combine (unpermute):
- *   out[t] = sum_j w[t,j] * y[dst[t*k+j]]  (+ residual[t]) (+ sg[t] * shared_y[t])
+ *   out[t] = sum_j w[t,j] * y[dst[t*k+j]]  (+ sg[t] * shared_y[t])
+ *            (+ residual[t - res_row0]  if res_row0 <= t < res_row0 + res_rows)
  * fp32 accumulation in slot order, one bf16 rounding.  dst < 0 => slot skipped.
- * residual / shared_y / shared_gate may be NULL.
+ * residual / shared_y / shared_gate may be NULL.  The residual row window lets
+ * a rank add the residual only to the rows a following reduce-scatter hands
+ * back to it (so the sum over ranks counts it once).
  */
 int hap_moe_combine(const void* y, const int32_t* dst_of_row, const float* topk_w, int64_t T, int64_t k,
-                    int64_t h, const void* residual, const void* shared_y, const float* shared_gate, void* out,
-                    void* stream);
+                    int64_t h, const void* residual, int64_t res_row0, int64_t res_rows, const void* shared_y,
+                    const float* shared_gate, void* out, void* stream);
 
 /* RMSNorm (fp32 statistics): out = w * (x * rsqrt(mean(x^2) + eps)). */
 int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, const void* w, float eps, void* out,

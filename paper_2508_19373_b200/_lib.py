@@ -39,8 +39,8 @@ SIGNATURES = {
     "hap_swiglu_half_width": (c_int64, [c_int64]),
     "hap_grouped_gemm_bf16": (
         ctypes.c_int,
-        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64,
-         c_int32, c_int64, c_void_p, c_void_p, c_int64, c_void_p],
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+         c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_int64, c_void_p],
     ),
     "hap_router_topk": (
         ctypes.c_int,
@@ -55,8 +55,8 @@ SIGNATURES = {
     ),
     "hap_moe_combine": (
         ctypes.c_int,
-        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
-         c_void_p],
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p,
+         c_void_p, c_void_p, c_void_p],
     ),
     "hap_rmsnorm": (
         ctypes.c_int,

@@ -26,7 +26,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kMaxBN = 256;
 constexpr int kStages = 4;
-constexpr int kMaxGroups = 256;
+constexpr int kMaxSegs = 512;
 constexpr int kAccCols = 256;  // TMEM columns per accumulator buffer
 constexpr int kThreads = 256;
 constexpr int kABytes = BM * BK * 2;       // 16 KB
@@ -37,12 +37,13 @@ struct Params {
   int32_t a_rows;
   int32_t K;
   int32_t N;         // B rows per group
-  int32_t n_groups;
+  int32_t n_segs;
   int32_t BN;        // n tile (multiple of 16, <= 256)
   int32_t epi;
   int32_t hw;        // swiglu half width (== BN/2 for swiglu)
   int32_t out_cols;  // valid output columns
   const int32_t* seg;
+  const int32_t* seg_group;
   __nv_bfloat16* C;
   int64_t ldc;
   const __nv_bfloat16* bias;
@@ -54,11 +55,11 @@ struct TileCoord {
   int32_t g, m0, m_end, n_blk;
 };
 
-// Map a linear tile index to (group, row range, n block).  tile_start has
-// n_groups+1 prefix entries; m-blocks vary fastest.
-__device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, const int32_t* seg, int n_groups,
-                                              int n_blocks) {
-  int lo = 0, hi = n_groups - 1;
+// Map a linear tile index to (segment's weight group, row range, n block).
+// tile_start has n_segs+1 prefix entries; m-blocks vary fastest.
+__device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, const int32_t* seg,
+                                              const int32_t* seg_group, int n_segs, int n_blocks) {
+  int lo = 0, hi = n_segs - 1;
   while (lo < hi) {  // last g with tile_start[g] <= t
     int mid = (lo + hi + 1) >> 1;
     if (tile_start[mid] <= t) lo = mid; else hi = mid - 1;
@@ -68,7 +69,7 @@ __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, 
   const int rows = seg[g + 1] - seg[g];
   const int m_blocks = (rows + BM - 1) / BM;
   TileCoord c;
-  c.g = g;
+  c.g = seg_group[g];
   c.m0 = seg[g] + (local % m_blocks) * BM;
   c.m_end = seg[g + 1];
   c.n_blk = local / m_blocks;
@@ -89,17 +90,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
   __shared__ uint32_t tmem_base_s;
-  __shared__ int32_t seg_s[kMaxGroups + 1];
-  __shared__ int32_t tile_start_s[kMaxGroups + 1];
+  __shared__ int32_t seg_s[kMaxSegs + 1];
+  __shared__ int32_t group_s[kMaxSegs];
+  __shared__ int32_t tile_start_s[kMaxSegs + 1];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n_groups = p.n_groups;
+  const int n_segs = p.n_segs;
   const int n_blocks = (p.N + p.BN - 1) / p.BN;
 
   // ---- setup: segment table, tile prefix, barriers, TMEM
-  for (int i = threadIdx.x; i <= n_groups; i += blockDim.x) {
+  for (int i = threadIdx.x; i <= n_segs; i += blockDim.x) {
     seg_s[i] = p.seg ? p.seg[i] : (i == 0 ? 0 : p.a_rows);
+    if (i < n_segs) group_s[i] = p.seg_group ? p.seg_group[i] : i;
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -120,18 +123,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
-    for (int g = 0; g < n_groups; ++g) {
+    for (int g = 0; g < n_segs; ++g) {
       tile_start_s[g] = acc;
       const int rows = seg_s[g + 1] - seg_s[g];
       acc += ((rows + BM - 1) / BM) * n_blocks;
     }
-    tile_start_s[n_groups] = acc;
+    tile_start_s[n_segs] = acc;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
-  const int total_tiles = tile_start_s[n_groups];
+  const int total_tiles = tile_start_s[n_segs];
   const int num_kb = (p.K + BK - 1) / BK;
 
   if (warp == 0) {
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileCoord c = map_tile(t, tile_start_s, seg_s, n_groups, n_blocks);
+        const TileCoord c = map_tile(t, tile_start_s, seg_s, group_s, n_segs, n_blocks);
         const int b_row = c.g * p.N + c.n_blk * p.BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quadrant accessible by this warp
     int it = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
-      const TileCoord c = map_tile(t, tile_start_s, seg_s, n_groups, n_blocks);
+      const TileCoord c = map_tile(t, tile_start_s, seg_s, group_s, n_segs, n_blocks);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -292,12 +295,16 @@ extern "C" int64_t hap_swiglu_half_width(int64_t inter_dim) {
 }
 
 extern "C" int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
-                                     int64_t n_groups, int64_t N, const int32_t* seg, void* C, int64_t ldc,
-                                     int32_t epilogue, int64_t swiglu_half, const void* bias, const void* residual,
-                                     int64_t ldr, void* stream) {
+                                     int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
+                                     const int32_t* seg_group, void* C, int64_t ldc, int32_t epilogue,
+                                     int64_t swiglu_half, const void* bias, const void* residual, int64_t ldr,
+                                     void* stream) {
   using namespace hap::gemm;
   if (!A || !B || !C || a_rows < 0 || K <= 0 || N <= 0 || n_groups <= 0) return HAP_ERR_INVALID_ARG;
-  if (n_groups > kMaxGroups || (n_groups > 1 && !seg)) return HAP_ERR_INVALID_ARG;
+  if (!seg) n_segs = 1;
+  if (n_segs <= 0 || n_segs > kMaxSegs) return HAP_ERR_INVALID_ARG;
+  if (!seg_group && n_segs != n_groups && seg) return HAP_ERR_INVALID_ARG;
+  if (!seg && n_groups != 1) return HAP_ERR_INVALID_ARG;
   if (a_rows > INT32_MAX || N * n_groups > INT32_MAX || K > INT32_MAX) return HAP_ERR_UNSUPPORTED;
   if (K % 8 || lda % 8 || ldc % 8 || N % 8 || lda < K) return HAP_ERR_MISALIGNED;
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
@@ -307,7 +314,8 @@ extern "C" int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda,
   p.a_rows = (int32_t)a_rows;
   p.K = (int32_t)K;
   p.N = (int32_t)N;
-  p.n_groups = (int32_t)n_groups;
+  p.n_segs = (int32_t)n_segs;
+  p.seg_group = seg_group;
   p.epi = epilogue;
   p.seg = seg;
   p.C = reinterpret_cast<__nv_bfloat16*>(C);
@@ -347,7 +355,7 @@ extern "C" int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda,
   }
   // Upper bound on tiles without reading seg on the host.
   const int64_t n_blocks = (N + p.BN - 1) / p.BN;
-  const int64_t max_tiles = ((a_rows + BM - 1) / BM + (n_groups - 1)) * n_blocks;
+  const int64_t max_tiles = ((a_rows + BM - 1) / BM + (n_segs - 1)) * n_blocks;
   const int grid = (int)(max_tiles < kNumSMs ? max_tiles : kNumSMs);
   grouped_gemm_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tmA, tmB, p);
   HAP_CHECK_LAUNCH();

@@ -1,0 +1,127 @@
+// Block glue: RMSNorm and rotary position embedding.
+//
+// Not modelled by the reference FLOP formulas (arch.py:145-178 has no
+// norm/rope term); semantics follow the HF decoder layer the planner's
+// ModelSpec presets describe (Mixtral / Qwen2-MoE RMSNorm with fp32
+// statistics; rotate-half RoPE with inv_freq = theta^(-2i/d)).
+#include "common.cuh"
+
+namespace hap {
+namespace norm {
+
+constexpr int kThreads = 256;
+
+// One warp per row; the row is held in registers (h/256 16-byte vectors per lane).
+template <int VPL>  // 16-byte vectors per lane
+__global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const uint4* __restrict__ x, int T, int hv, int ldxv,
+                                                           const uint4* __restrict__ w, float eps,
+                                                           uint4* __restrict__ out, int ldov) {
+  const int row = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  uint4 v[VPL];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = c < hv ? __ldg(x + (int64_t)row * ldxv + c) : make_uint4(0, 0, 0, 0);
+    const uint32_t u[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16x2(u[j]);
+      ss = fmaf(f.x, f.x, ss);
+      ss = fmaf(f.y, f.y, ss);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = rsqrtf(ss / (float)(hv * 8) + eps);
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c >= hv) break;
+    const uint4 wv = __ldg(w + c);
+    const uint32_t u[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+    const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16x2(u[j]);
+      const float2 g = unpack_bf16x2(ww[j]);
+      o[j] = pack_bf16x2(f.x * inv * g.x, f.y * inv * g.y);
+    }
+    out[(int64_t)row * ldov + c] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// One warp per (token, head) for the q and k heads; lane owns rotation pairs
+// (i, i + d/2) for i = lane, lane + 32 (d = 128) or i = lane (d = 64).
+__global__ void __launch_bounds__(kThreads) rope_kernel(__nv_bfloat16* __restrict__ qkv, int T, int64_t ld,
+                                                        int n_heads_rot, int d, const int32_t* __restrict__ pos,
+                                                        float theta) {
+  const int item = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (item >= T * n_heads_rot) return;
+  const int t = item / n_heads_rot;
+  const int hh = item % n_heads_rot;
+  __nv_bfloat16* base = qkv + (int64_t)t * ld + (int64_t)hh * d;
+  const int half = d / 2;
+  const float p = (float)pos[t];
+  for (int i = lane; i < half; i += 32) {
+    // inv_freq computed exactly as HF: 1 / theta^((2i)/d) in fp32
+    const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / (float)d);
+    const float ang = p * inv_freq;
+    float s, c;
+    sincosf(ang, &s, &c);
+    const float x1 = __bfloat162float(base[i]);
+    const float x2 = __bfloat162float(base[i + half]);
+    base[i] = __float2bfloat16_rn(x1 * c - x2 * s);
+    base[i + half] = __float2bfloat16_rn(x2 * c + x1 * s);
+  }
+}
+
+}  // namespace norm
+}  // namespace hap
+
+using namespace hap::norm;
+
+extern "C" int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, const void* w, float eps, void* out,
+                           int64_t ldo, void* stream) {
+  if (!x || !w || !out || T < 0 || h <= 0 || ldx < h || ldo < h) return HAP_ERR_INVALID_ARG;
+  if (h % 8 || ldx % 8 || ldo % 8) return HAP_ERR_MISALIGNED;
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return HAP_ERR_MISALIGNED;
+  if (T == 0) return HAP_OK;
+  const int hv = (int)(h / 8);
+  const int vpl = (hv + 31) / 32;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = (int)((T * 32 + kThreads - 1) / kThreads);
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+  uint4* ov = reinterpret_cast<uint4*>(out);
+#define HAP_NORM_CASE(V) \
+  if (vpl <= V) { rmsnorm_kernel<V><<<grid, kThreads, 0, st>>>(xv, (int)T, hv, (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8)); HAP_CHECK_LAUNCH(); return HAP_OK; }
+  HAP_NORM_CASE(2)
+  HAP_NORM_CASE(4)
+  HAP_NORM_CASE(8)
+  HAP_NORM_CASE(16)
+  HAP_NORM_CASE(24)
+  HAP_NORM_CASE(32)
+#undef HAP_NORM_CASE
+  return HAP_ERR_UNSUPPORTED;
+}
+
+extern "C" int hap_rope_qk(void* qkv, int64_t T, int64_t ld, int64_t n_q_heads, int64_t n_kv_heads,
+                           int64_t head_dim, const int32_t* positions, float theta, void* stream) {
+  if (!qkv || !positions || T < 0 || n_q_heads < 1 || n_kv_heads < 0 || head_dim < 2 || head_dim % 2)
+    return HAP_ERR_INVALID_ARG;
+  if (ld < (n_q_heads + n_kv_heads) * head_dim) return HAP_ERR_INVALID_ARG;
+  if (T == 0) return HAP_OK;
+  const int heads = (int)(n_q_heads + n_kv_heads);
+  const int64_t items = T * heads;
+  const int grid = (int)((items * 32 + kThreads - 1) / kThreads);
+  rope_kernel<<<grid, kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<__nv_bfloat16*>(qkv), (int)T, ld, heads, (int)head_dim, positions, theta);
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
+}

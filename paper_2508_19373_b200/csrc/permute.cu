@@ -1,0 +1,272 @@
+// Token permute (dispatch re-layout) and weighted combine (unpermute).
+//
+// Permute is a stable counting sort keyed on the expert id, in three passes:
+//   1. rank:    each block takes a contiguous range of rows; per 256-row pass
+//               a warp computes stable in-warp ranks with __match_any_sync and
+//               per-warp expert counts, combined across warps in row order.
+//               Output: local_rank[r] (rank among equal experts inside the
+//               block) and block_counts[b][e].
+//   2. scan:    per-expert totals -> seg (exclusive prefix), and per-block
+//               bases base[b][e] = seg[e] + sum_{b'<b} block_counts[b'][e].
+//   3. scatter: dst = base[b(r)][e_r] + local_rank[r]; one warp copies the
+//               h-wide bf16 row with 16-byte vector loads/stores.
+// Every step is deterministic (no atomics on the ordering path), so the
+// permutation is bit-exact against the oracle's stable sort by (expert, row).
+//
+// Combine reads the k expert outputs of a token (gather), accumulates
+// w * y in fp32 in slot order, adds the optional shared-expert output scaled
+// by its sigmoid gate and the residual, and rounds once to bf16.
+//
+// Models: the EP dispatch/combine token re-layout implicit in the all-to-all
+// rows of comm_volume (reference strategies.py:334-340).
+#include "common.cuh"
+
+namespace hap {
+namespace permute {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kRowsPerBlock = 4096;
+constexpr int kMaxExperts = 512;
+
+struct Workspace {
+  int32_t* local_rank;    // [R]
+  int32_t* block_counts;  // [NB][E]
+  int32_t* block_base;    // [NB][E]
+};
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+static size_t ws_bytes(int64_t R, int64_t E, int64_t* nb_out) {
+  const int64_t nb = (R + kRowsPerBlock - 1) / kRowsPerBlock;
+  if (nb_out) *nb_out = nb;
+  return align_up((size_t)R * 4, 256) + 2 * align_up((size_t)(nb > 0 ? nb : 1) * E * 4, 256);
+}
+
+__global__ void __launch_bounds__(kThreads) rank_kernel(const int32_t* __restrict__ eid, int R, int E,
+                                                        int32_t* __restrict__ local_rank,
+                                                        int32_t* __restrict__ block_counts) {
+  extern __shared__ int32_t sm[];
+  int32_t* running = sm;             // [E]
+  int32_t* warp_cnt = sm + E;        // [kWarps][E]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < E; i += kThreads) running[i] = 0;
+  const int r_begin = blockIdx.x * kRowsPerBlock;
+  const int r_end = min(R, r_begin + kRowsPerBlock);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int base = r_begin; base < r_end; base += kThreads) {
+    for (int i = threadIdx.x; i < kWarps * E; i += kThreads) warp_cnt[i] = 0;
+    __syncthreads();
+    const int r = base + threadIdx.x;
+    int e = -1;
+    if (r < r_end) {
+      e = eid[r];
+      if (e < 0 || e >= E) e = -1;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank_in_warp = __popc(peers & lt_mask);
+    if (e >= 0 && rank_in_warp == 0) warp_cnt[warp * E + e] = __popc(peers);
+    __syncthreads();
+    if (e >= 0) {
+      int off = running[e];
+      for (int w2 = 0; w2 < warp; ++w2) off += warp_cnt[w2 * E + e];
+      local_rank[r] = off + rank_in_warp;
+    } else if (r < r_end) {
+      local_rank[r] = -1;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < E; i += kThreads) {
+      int s = 0;
+      for (int w2 = 0; w2 < kWarps; ++w2) s += warp_cnt[w2 * E + i];
+      running[i] += s;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < E; i += kThreads) block_counts[(int64_t)blockIdx.x * E + i] = running[i];
+}
+
+__global__ void scan_kernel(const int32_t* __restrict__ block_counts, int NB, int E, int32_t* __restrict__ block_base,
+                            int32_t* __restrict__ seg) {
+  __shared__ int32_t totals[kMaxExperts];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int s = 0;
+    for (int b = 0; b < NB; ++b) s += block_counts[(int64_t)b * E + e];
+    totals[e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      const int c = totals[e];
+      totals[e] = acc;
+      seg[e] = acc;
+      acc += c;
+    }
+    seg[E] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int acc = totals[e];
+    for (int b = 0; b < NB; ++b) {
+      block_base[(int64_t)b * E + e] = acc;
+      acc += block_counts[(int64_t)b * E + e];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) scatter_kernel(const int32_t* __restrict__ eid, int R, int E,
+                                                           const int32_t* __restrict__ local_rank,
+                                                           const int32_t* __restrict__ block_base,
+                                                           const uint4* __restrict__ x, int src_div, int hv,
+                                                           uint4* __restrict__ x_out, int32_t* __restrict__ dst_of_row) {
+  const int warp_global = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_warps = (gridDim.x * kThreads) >> 5;
+  for (int r = warp_global; r < R; r += n_warps) {
+    int e = eid[r];
+    int dst = -1;
+    if (e >= 0 && e < E) dst = block_base[(int64_t)(r / kRowsPerBlock) * E + e] + local_rank[r];
+    if (lane == 0) dst_of_row[r] = dst;
+    if (dst >= 0 && x_out) {
+      const uint4* src = x + (int64_t)(r / src_div) * hv;
+      uint4* out = x_out + (int64_t)dst * hv;
+      int i = lane;
+      for (; i + 96 < hv; i += 128) {
+        const uint4 a = __ldg(src + i), b = __ldg(src + i + 32), c = __ldg(src + i + 64), d = __ldg(src + i + 96);
+        out[i] = a;
+        out[i + 32] = b;
+        out[i + 64] = c;
+        out[i + 96] = d;
+      }
+      for (; i < hv; i += 32) out[i] = __ldg(src + i);
+    }
+  }
+}
+
+// One warp per token; each lane owns 8-element column slices lane*8 + 256*c.
+__global__ void __launch_bounds__(kThreads) combine_kernel(const uint4* __restrict__ y, const int32_t* __restrict__ dst,
+                                                           const float* __restrict__ tw, int T, int k, int hv,
+                                                           const uint4* __restrict__ resid, int res_row0,
+                                                           int res_rows, const uint4* __restrict__ shared_y,
+                                                           const float* __restrict__ shared_gate,
+                                                           uint4* __restrict__ out) {
+  const int warp_global = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_warps = (gridDim.x * kThreads) >> 5;
+  for (int t = warp_global; t < T; t += n_warps) {
+    int rows[32];
+    float ws[32];
+    for (int j = 0; j < k; ++j) {
+      rows[j] = dst[(int64_t)t * k + j];
+      ws[j] = tw[(int64_t)t * k + j];
+    }
+    const float sg = shared_gate ? shared_gate[t] : 0.f;
+    for (int c = lane; c < hv; c += 32) {
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        if (rows[j] < 0) continue;
+        const uint4 v = __ldg(y + (int64_t)rows[j] * hv + c);
+        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = unpack_bf16x2(vw[i]);
+          acc[2 * i] = fmaf(ws[j], f.x, acc[2 * i]);
+          acc[2 * i + 1] = fmaf(ws[j], f.y, acc[2 * i + 1]);
+        }
+      }
+      if (shared_y) {
+        const uint4 v = __ldg(shared_y + (int64_t)t * hv + c);
+        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = unpack_bf16x2(vw[i]);
+          acc[2 * i] = fmaf(sg, f.x, acc[2 * i]);
+          acc[2 * i + 1] = fmaf(sg, f.y, acc[2 * i + 1]);
+        }
+      }
+      if (resid && t >= res_row0 && t < res_row0 + res_rows) {
+        const uint4 v = __ldg(resid + (int64_t)(t - res_row0) * hv + c);
+        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = unpack_bf16x2(vw[i]);
+          acc[2 * i] += f.x;
+          acc[2 * i + 1] += f.y;
+        }
+      }
+      out[(int64_t)t * hv + c] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                                            pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+    }
+  }
+}
+
+}  // namespace permute
+}  // namespace hap
+
+using namespace hap::permute;
+
+extern "C" size_t hap_moe_permute_workspace_bytes(int64_t R, int64_t n_experts) {
+  if (R < 0 || n_experts <= 0) return 0;
+  return ws_bytes(R, n_experts, nullptr);
+}
+
+extern "C" int hap_moe_permute(const int32_t* expert_of_row, int64_t R, int64_t n_experts, const void* x,
+                               int64_t src_row_div, int64_t h, void* x_out, int32_t* dst_of_row, int32_t* seg,
+                               void* workspace, size_t ws_size, void* stream) {
+  if (!seg || R < 0 || n_experts <= 0) return HAP_ERR_INVALID_ARG;
+  if (R > 0 && (!expert_of_row || !dst_of_row)) return HAP_ERR_INVALID_ARG;
+  if (n_experts > kMaxExperts || R > INT32_MAX) return HAP_ERR_UNSUPPORTED;
+  if (x_out && (!x || src_row_div <= 0 || h <= 0)) return HAP_ERR_INVALID_ARG;
+  if (x_out && (h % 8 || ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(x_out)) & 15)))
+    return HAP_ERR_MISALIGNED;
+  int64_t nb = 0;
+  const size_t need = ws_bytes(R, n_experts, &nb);
+  if (!workspace || ws_size < need) return HAP_ERR_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int E = (int)n_experts;
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(workspace);
+  int32_t* local_rank = reinterpret_cast<int32_t*>(w8);
+  int32_t* block_counts = reinterpret_cast<int32_t*>(w8 + align_up((size_t)R * 4, 256));
+  int32_t* block_base =
+      reinterpret_cast<int32_t*>(w8 + align_up((size_t)R * 4, 256) + align_up((size_t)(nb > 0 ? nb : 1) * E * 4, 256));
+  if (R == 0) {
+    cudaMemsetAsync(seg, 0, sizeof(int32_t) * (E + 1), st);
+    HAP_CHECK_LAUNCH();
+    return HAP_OK;
+  }
+  const int smem = (int)((1 + kWarps) * E * sizeof(int32_t));
+  rank_kernel<<<(int)nb, kThreads, smem, st>>>(expert_of_row, (int)R, E, local_rank, block_counts);
+  scan_kernel<<<1, 256, 0, st>>>(block_counts, (int)nb, E, block_base, seg);
+  const int64_t warps_needed = R;
+  int grid = (int)((warps_needed * 32 + kThreads - 1) / kThreads);
+  if (grid > 148 * 16) grid = 148 * 16;
+  scatter_kernel<<<grid, kThreads, 0, st>>>(expert_of_row, (int)R, E, local_rank, block_base,
+                                            reinterpret_cast<const uint4*>(x), (int)(src_row_div > 0 ? src_row_div : 1),
+                                            (int)(h / 8), reinterpret_cast<uint4*>(x_out), dst_of_row);
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
+}
+
+extern "C" int hap_moe_combine(const void* y, const int32_t* dst_of_row, const float* topk_w, int64_t T, int64_t k,
+                               int64_t h, const void* residual, int64_t res_row0, int64_t res_rows,
+                               const void* shared_y, const float* shared_gate, void* out, void* stream) {
+  if (!y || !dst_of_row || !topk_w || !out || T < 0 || k < 1 || k > 32 || h <= 0) return HAP_ERR_INVALID_ARG;
+  if (h % 8) return HAP_ERR_MISALIGNED;
+  if ((shared_y == nullptr) != (shared_gate == nullptr)) return HAP_ERR_INVALID_ARG;
+  if (residual && (res_row0 < 0 || res_rows < 0)) return HAP_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(residual) |
+       reinterpret_cast<uintptr_t>(shared_y)) & 15)
+    return HAP_ERR_MISALIGNED;
+  if (T == 0) return HAP_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int grid = (int)((T * 32 + kThreads - 1) / kThreads);
+  if (grid > 148 * 16) grid = 148 * 16;
+  combine_kernel<<<grid, kThreads, 0, st>>>(reinterpret_cast<const uint4*>(y), dst_of_row, topk_w, (int)T, (int)k,
+                                            (int)(h / 8), reinterpret_cast<const uint4*>(residual), (int)res_row0,
+                                            (int)res_rows, reinterpret_cast<const uint4*>(shared_y), shared_gate,
+                                            reinterpret_cast<uint4*>(out));
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
+}

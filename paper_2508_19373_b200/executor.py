@@ -1,0 +1,276 @@
+"""HAP MoE-block executor: runs one (AttentionStrategy, ExpertStrategy) plan
+emitted by the reference planner (moeplan planner.py:527-549) on B200s.
+
+Per rank and per call (prefill or decode) the block is
+
+  attention module (heads sharded by attention tp, sequences by attention dp)
+    rmsnorm -> QKV GEMM (+bias) -> RoPE -> attention core -> O GEMM (+residual)
+    -> AllReduce over the attention-TP group                (strategies.py:314-322)
+  boundary: all-gather of normalised tokens when the expert shard spans
+    several attention replicas (DP -> TP, strategies.py:324-332)
+  expert module (experts sharded by ep, intermediate dim by expert tp)
+    router/top-k -> permute -> [EP: count exchange + dispatch All-to-All]
+    -> grouped GEMM gate/up (+SwiGLU) -> grouped GEMM down
+    -> [EP: combine All-to-All] -> weighted combine (+shared expert, +residual)
+  reduce-scatter over the expert-TP group (TP -> DP, strategies.py:324-342),
+  then all-gather over the attention-TP group back to the input layout.
+
+Every compute op is a libhap_kernels launch (``CudaOps``); the executor never
+computes on the host and has no fallback.  A different ``ops`` object can be
+injected only by the test-suite's CPU multi-process tests, which exercise the
+collective schedule on gloo (see tests/test_executor_dist.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from math import ceil
+from typing import Optional
+
+import torch
+
+from . import ops as K
+from .comm import Comm
+from .config import BlockConfig
+from .layout import PlanDegrees, RankLayout, replica_sequences, tokens_per_replica
+from .weights import RankWeights, pack_rank_weights, synthetic_weights
+
+BF16 = torch.bfloat16
+
+
+class CudaOps:
+    """The product compute backend: every method launches a kernel of
+    libhap_kernels.so through the C-ABI (ops.py).  Construction fails loudly
+    if CUDA or the library is unavailable."""
+
+    def __init__(self):
+        from . import _lib
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("HAP executor requires a CUDA device (sm_100a); there is no CPU path")
+        _lib.load()
+
+    rmsnorm = staticmethod(K.rmsnorm)
+    gemm = staticmethod(K.gemm)
+    grouped_gemm = staticmethod(K.grouped_gemm)
+    rope_qk = staticmethod(K.rope_qk)
+    attn_prefill = staticmethod(K.attn_prefill)
+    attn_decode = staticmethod(K.attn_decode)
+    router_topk = staticmethod(K.router_topk)
+    moe_permute = staticmethod(K.moe_permute)
+    moe_combine = staticmethod(K.moe_combine)
+    permute_workspace_bytes = staticmethod(K.permute_workspace_bytes)
+    attn_decode_workspace_bytes = staticmethod(K.attn_decode_workspace_bytes)
+
+
+@dataclass
+class KVCache:
+    """Head-major cache of this rank's local kv heads: [bpr, Hkv_l, max_len, d]."""
+
+    k: torch.Tensor
+    v: torch.Tensor
+
+    @classmethod
+    def empty(cls, bpr: int, n_kv_local: int, max_len: int, head_dim: int, device, random: bool = False):
+        shape = (bpr, n_kv_local, max_len, head_dim)
+        if random:
+            k = torch.randn(shape, device=device, dtype=torch.float32).to(BF16)
+            v = torch.randn(shape, device=device, dtype=torch.float32).to(BF16)
+        else:
+            k = torch.zeros(shape, device=device, dtype=BF16)
+            v = torch.zeros(shape, device=device, dtype=BF16)
+        return cls(k, v)
+
+
+class HapMoEBlock:
+    """One MoE decoder block laid out for one plan on one rank."""
+
+    def __init__(self, cfg: BlockConfig, attention, expert, *, rank: int = 0, device=None, seed: int = 0,
+                 weights: Optional[dict] = None, ops=None, comm: Optional[Comm] = None):
+        self.cfg = cfg
+        self.deg = attention if isinstance(attention, PlanDegrees) and expert is None else \
+            PlanDegrees.from_strategies(attention, expert)
+        self.lay = RankLayout(self.deg, rank, cfg.n_q_heads, cfg.n_kv_heads, cfg.n_experts, cfg.inter,
+                              cfg.n_shared)
+        self.ops = ops if ops is not None else CudaOps()
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        full = weights if weights is not None else synthetic_weights(cfg, self.device, seed)
+        self.w: RankWeights = pack_rank_weights(cfg, full, self.lay)
+        del full
+        self.comm = comm if comm is not None else (Comm(self.lay) if self.lay.n > 1 else None)
+        self.last_routing = None  # (topk_idx, dst_of_row, seg) of the last expert call, for parity tests
+
+    @classmethod
+    def from_plan(cls, cfg: BlockConfig, plan, stage: str = "prefill", **kw) -> "HapMoEBlock":
+        """Build from a moeplan Plan (planner.py:142-166) for one stage."""
+        exp = plan.expert_prefill if stage == "prefill" else plan.expert_decode
+        return cls(cfg, plan.attention, exp, **kw)
+
+    # ------------------------------------------------------------ helpers --
+    def _coll(self, name, *args):
+        if self.comm is None:
+            return None
+        return getattr(self.comm, name)(*args)
+
+    def _attn_rows(self, batch: int, seq: int):
+        bpr, rows = tokens_per_replica(batch, self.deg.a_dp, seq, self.lay.n)
+        s0, s1 = replica_sequences(batch, self.deg.a_dp, self.lay.a_rep)
+        return bpr, rows, s1 - s0
+
+    # ------------------------------------------------------------ forward --
+    def forward(self, x_local: torch.Tensor, stage: str, batch: int, seq_len: int = 1,
+                kv_cache: Optional[KVCache] = None, positions: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """x_local: this attention replica's tokens [n_seqs_local * seq_len, h]
+        (prefill) or [n_seqs_local, h] (decode); returns the block output in
+        the same layout.  positions (decode): int32 [n_seqs_local] current
+        lengths (the new token's position)."""
+        if stage == "prefill":
+            return self._forward(x_local, batch, seq_len, decode=False, kv_cache=kv_cache)
+        if stage == "decode":
+            if kv_cache is None or positions is None:
+                raise ValueError("decode needs a kv_cache and positions")
+            return self._forward(x_local, batch, 1, decode=True, kv_cache=kv_cache, positions=positions)
+        raise ValueError(f"unknown stage {stage!r}")
+
+    def _forward(self, x_local, batch, S, decode, kv_cache=None, positions=None):
+        cfg, w, lay, ops = self.cfg, self.w, self.lay, self.ops
+        dev = self.device
+        h, d = cfg.hidden, cfg.head_dim
+        bpr, rows, n_seq = self._attn_rows(batch, S)
+        T_real = n_seq * S
+        if x_local.shape != (T_real, h):
+            raise ValueError(f"x_local must be [{T_real}, {h}] for this rank, got {tuple(x_local.shape)}")
+        if rows != T_real:
+            x = torch.zeros(rows, h, device=dev, dtype=BF16)
+            x[:T_real].copy_(x_local)
+        else:
+            x = x_local.contiguous()
+
+        # ---------------- attention module
+        xn = ops.rmsnorm(x, w.ln1, cfg.rms_eps)
+        qkv = ops.gemm(xn, w.wqkv, bias=w.bqkv)
+        nq, nkv = w.n_q_local, w.n_kv_local
+        if decode:
+            pos = torch.zeros(rows, device=dev, dtype=torch.int32)
+            pos[:n_seq].copy_(positions)
+        else:
+            pos = torch.arange(S, device=dev, dtype=torch.int32).repeat(bpr)
+            pos = torch.cat([pos, pos.new_zeros(rows - pos.numel())]) if pos.numel() < rows else pos[:rows]
+        ops.rope_qk(qkv, nq, nkv, d, pos, cfg.rope_theta)
+        attn = torch.zeros(rows, nq * d, device=dev, dtype=BF16) if rows != T_real else \
+            torch.empty(rows, nq * d, device=dev, dtype=BF16)
+        if decode:
+            ws = torch.empty(ops.attn_decode_workspace_bytes(max(n_seq, 1), nq, d, kv_cache.k.shape[2]),
+                             device=dev, dtype=torch.uint8)
+            if n_seq:
+                ops.attn_decode(qkv[:n_seq], kv_cache.k[:n_seq], kv_cache.v[:n_seq], pos[:n_seq], nq, nkv, d,
+                                attn[:n_seq], ws)
+        elif n_seq:
+            ops.attn_prefill(qkv, nq, nkv, d, n_seq, S, attn)
+        h1 = ops.gemm(attn, w.wo, residual=x if lay.a_tp_rank == 0 else None)
+        self._coll("all_reduce", h1, "attn_tp_group")
+        hn = ops.rmsnorm(h1, w.ln2, cfg.rms_eps)
+
+        # ---------------- boundary: attention layout -> expert shard
+        S_e, a_dp = lay.n_shards, self.deg.a_dp
+        if S_e < a_dp:
+            R = a_dp // S_e
+            hn_s = torch.empty(R * rows, h, device=dev, dtype=BF16)
+            self.comm.all_gather(hn_s, hn, "gather_group")
+        elif S_e > a_dp:
+            P = S_e // a_dp
+            p = lay.shard % P
+            rs = rows // P
+            hn_s = hn[p * rs:(p + 1) * rs]
+        else:
+            hn_s = hn
+        rows_s = hn_s.shape[0]
+
+        # ---------------- expert module (partial over expert tp)
+        c = rows // self.deg.a_tp  # rows this rank owns after the reduce-scatter
+        residual = h1[lay.a_tp_rank * c:(lay.a_tp_rank + 1) * c]
+        y = self._experts(hn_s, residual, res_row0=lay.e_tp_rank * c, res_rows=c)
+
+        # ---------------- back to the attention layout
+        if self.deg.e_tp > 1:
+            chunk = torch.empty(c, h, device=dev, dtype=BF16)
+            self.comm.reduce_scatter(chunk, y, "exp_tp_group")
+        else:
+            chunk = y
+        if self.deg.a_tp > 1:
+            out = torch.empty(rows, h, device=dev, dtype=BF16)
+            self.comm.all_gather(out, chunk, "attn_tp_group")
+        else:
+            out = chunk
+        return out[:T_real]
+
+    def _experts(self, hn_s, residual, res_row0, res_rows):
+        cfg, w, lay, ops = self.cfg, self.w, self.lay, self.ops
+        dev = self.device
+        T, h = hn_s.shape
+        E, k = cfg.n_experts, cfg.top_k
+        idx = torch.empty(T, k, device=dev, dtype=torch.int32)
+        tw = torch.empty(T, k, device=dev, dtype=torch.float32)
+        sg = torch.empty(T, device=dev, dtype=torch.float32) if cfg.n_shared else None
+        ops.router_topk(hn_s, w.router, E, k, cfg.norm_topk_prob, bool(cfg.n_shared), idx, tw, sg)
+        R = T * k
+        x_perm = torch.empty(R, h, device=dev, dtype=BF16)
+        dst = torch.empty(R, device=dev, dtype=torch.int32)
+        seg = torch.empty(E + 1, device=dev, dtype=torch.int32)
+        ws = torch.empty(max(ops.permute_workspace_bytes(R, E), 16), device=dev, dtype=torch.uint8)
+        ops.moe_permute(idx.view(-1), E, hn_s, k, x_perm, dst, seg, ws)
+        self.last_routing = (idx, dst, seg)
+        il = w.inter_local
+        if self.deg.e_ep == 1:
+            H = torch.empty(R, il, device=dev, dtype=BF16)
+            ops.grouped_gemm(x_perm, w.w13, E, seg, H, swiglu_half=w.hw)
+            Y = torch.empty(R, h, device=dev, dtype=BF16)
+            ops.grouped_gemm(H, w.w2, E, seg, Y)
+        else:
+            Y = self._ep_experts(x_perm, seg)
+        ys = None
+        if cfg.n_shared:
+            hs = ops.gemm(hn_s, w.ws13, swiglu_half=w.hw_s)
+            ys = ops.gemm(hs, w.ws2)
+        out = torch.empty(T, h, device=dev, dtype=BF16)
+        ops.moe_combine(Y, dst, tw, T, k, out, residual=residual, shared_y=ys, shared_gate=sg,
+                        res_row0=res_row0, res_rows=res_rows)
+        return out
+
+    def _ep_experts(self, x_perm, seg):
+        """EP dispatch -> local grouped GEMMs -> combine (strategies.py:334-340)."""
+        w, ops, comm = self.w, self.ops, self.comm
+        dev = self.device
+        ep, El, h = self.deg.e_ep, w.n_experts_local, self.cfg.hidden
+        counts = (seg[1:] - seg[:-1]).contiguous()           # [E] rows per global expert, dest-group major
+        recv_counts = torch.empty_like(counts)                # [ep * El]: from src s, local expert j
+        comm.all_to_all(recv_counts, counts, [El] * ep, [El] * ep, "a2a_group")
+        both = torch.cat([counts, recv_counts]).cpu()         # the one host sync of the EP path
+        send = both[:ep * El].view(ep, El).sum(1).tolist()
+        rc = both[ep * El:].view(ep, El)
+        recv = rc.sum(1).tolist()
+        n_recv = int(sum(recv))
+        x_recv = torch.empty(n_recv, h, device=dev, dtype=BF16)
+        comm.all_to_all(x_recv, x_perm, recv, send, "a2a_group")
+        # received rows are grouped (src rank, local expert): one GEMM segment each
+        seg_r = torch.zeros(ep * El + 1, dtype=torch.int32)
+        seg_r[1:] = torch.cumsum(rc.reshape(-1), 0)
+        grp = torch.arange(El, dtype=torch.int32).repeat(ep)
+        seg_r, grp = seg_r.to(dev, non_blocking=True), grp.to(dev, non_blocking=True)
+        il = w.inter_local
+        H = torch.empty(n_recv, il, device=dev, dtype=BF16)
+        Y_r = torch.empty(n_recv, h, device=dev, dtype=BF16)
+        if n_recv:
+            ops.grouped_gemm(x_recv, w.w13, El, seg_r, H, swiglu_half=w.hw, seg_group=grp)
+            ops.grouped_gemm(H, w.w2, El, seg_r, Y_r, seg_group=grp)
+        Y = torch.empty(x_perm.shape[0], h, device=dev, dtype=BF16)
+        comm.all_to_all(Y, Y_r, send, recv, "a2a_group")
+        return Y
+
+
+def forward(block: HapMoEBlock, hidden: torch.Tensor, stage: str, batch: int, seq_len: int = 1,
+            kv_cache: Optional[KVCache] = None, positions: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """hap.forward: the block's plan applied to this rank's tokens."""
+    return block.forward(hidden, stage, batch, seq_len, kv_cache=kv_cache, positions=positions)

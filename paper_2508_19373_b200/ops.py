@@ -1,0 +1,210 @@
+"""Torch-facing wrappers of the C-ABI kernels (include/hap_kernels.h).
+
+Each wrapper validates dtypes / devices / contiguity, passes raw device
+pointers plus ``torch.cuda.current_stream()`` to the library and maps status
+codes to exceptions.  Nothing here computes on the host and nothing falls
+back to PyTorch math: if the library is missing, ``_lib.load`` raises.
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import HAP_EPI_STORE, HAP_EPI_SWIGLU, check
+
+BF16 = torch.bfloat16
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need(t: torch.Tensor, name: str, dtype=None, cuda=True):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if cuda and not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def _rowmajor(t: torch.Tensor, name: str):
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{name} must be a 2-D row-major view")
+
+
+def swiglu_half_width(inter: int) -> int:
+    hw = _lib.load().hap_swiglu_half_width(int(inter))
+    if hw <= 0:
+        raise ValueError(f"no SwiGLU tile width divides inter={inter}")
+    return int(hw)
+
+
+def grouped_gemm(a: torch.Tensor, b: torch.Tensor, n_groups: int, seg: Optional[torch.Tensor],
+                 out: torch.Tensor, *, swiglu_half: int = 0, bias: Optional[torch.Tensor] = None,
+                 residual: Optional[torch.Tensor] = None,
+                 seg_group: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """out[r] = epi(a[r] @ b[g*N:(g+1)*N]^T) for rows r of segment s, g = seg_group[s] (tcgen05 kernel)."""
+    lib = _lib.load()
+    _need(a, "a", BF16); _need(b, "b", BF16); _need(out, "out", BF16)
+    _rowmajor(a, "a"); _rowmajor(out, "out")
+    if not b.is_contiguous():
+        raise ValueError("b must be contiguous [n_groups*N, K]")
+    K = a.shape[1]
+    b2 = b.reshape(-1, b.shape[-1])
+    if b2.shape[1] != K or b2.shape[0] % n_groups:
+        raise ValueError(f"b shape {tuple(b.shape)} incompatible with K={K}, n_groups={n_groups}")
+    N = b2.shape[0] // n_groups
+    n_segs = 1
+    if seg is not None:
+        _need(seg, "seg", torch.int32)
+        n_segs = seg.numel() - 1
+        if seg_group is not None:
+            _need(seg_group, "seg_group", torch.int32)
+            if seg_group.numel() != n_segs:
+                raise ValueError("seg_group must have one entry per segment")
+        elif n_segs != n_groups:
+            raise ValueError("seg must have n_groups+1 entries (or pass seg_group)")
+    elif n_groups != 1:
+        raise ValueError("seg is required when n_groups > 1")
+    epi = HAP_EPI_SWIGLU if swiglu_half else HAP_EPI_STORE
+    if residual is not None:
+        _need(residual, "residual", BF16); _rowmajor(residual, "residual")
+    if bias is not None:
+        _need(bias, "bias", BF16)
+    st = lib.hap_grouped_gemm_bf16(a.data_ptr(), a.shape[0], a.stride(0), K, b2.data_ptr(), n_groups, N,
+                                   _ptr(seg), n_segs, _ptr(seg_group), out.data_ptr(), out.stride(0), epi,
+                                   int(swiglu_half),
+                                   _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0,
+                                   _stream())
+    check(st, "hap_grouped_gemm_bf16")
+    return out
+
+
+def gemm(a: torch.Tensor, w: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None, residual=None,
+         swiglu_half: int = 0) -> torch.Tensor:
+    """Dense a @ w^T (nn.Linear layout) on the tcgen05 kernel."""
+    n_out = w.shape[0] // 2 if swiglu_half else w.shape[0]
+    if out is None:
+        out = torch.empty(a.shape[0], n_out, device=a.device, dtype=BF16)
+    return grouped_gemm(a, w, 1, None, out, swiglu_half=swiglu_half, bias=bias, residual=residual)
+
+
+def router_topk(x: torch.Tensor, w: torch.Tensor, n_experts: int, top_k: int, renormalize: bool,
+                has_shared_gate: bool, topk_idx: torch.Tensor, topk_w: torch.Tensor,
+                shared_gate: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None):
+    lib = _lib.load()
+    _need(x, "x", BF16); _need(w, "w", BF16)
+    if not x.is_contiguous() or not w.is_contiguous():
+        raise ValueError("router inputs must be contiguous")
+    _need(topk_idx, "topk_idx", torch.int32); _need(topk_w, "topk_w", torch.float32)
+    st = lib.hap_router_topk(x.data_ptr(), x.shape[0], x.shape[1], w.data_ptr(), n_experts, top_k,
+                             int(renormalize), int(has_shared_gate), topk_idx.data_ptr(), topk_w.data_ptr(),
+                             _ptr(shared_gate), _ptr(logits), _stream())
+    check(st, "hap_router_topk")
+
+
+def permute_workspace_bytes(rows: int, n_experts: int) -> int:
+    return int(_lib.load().hap_moe_permute_workspace_bytes(rows, n_experts))
+
+
+def moe_permute(expert_of_row: torch.Tensor, n_experts: int, x: Optional[torch.Tensor], src_row_div: int,
+                x_out: Optional[torch.Tensor], dst_of_row: torch.Tensor, seg: torch.Tensor,
+                workspace: torch.Tensor) -> None:
+    lib = _lib.load()
+    _need(expert_of_row, "expert_of_row", torch.int32)
+    _need(dst_of_row, "dst_of_row", torch.int32); _need(seg, "seg", torch.int32)
+    R = expert_of_row.numel()
+    h = 0
+    if x_out is not None:
+        _need(x, "x", BF16); _need(x_out, "x_out", BF16)
+        if not x.is_contiguous() or not x_out.is_contiguous():
+            raise ValueError("permute payloads must be contiguous")
+        h = x.shape[1]
+    st = lib.hap_moe_permute(expert_of_row.data_ptr(), R, n_experts, _ptr(x), src_row_div, h, _ptr(x_out),
+                             dst_of_row.data_ptr(), seg.data_ptr(), workspace.data_ptr(),
+                             workspace.numel() * workspace.element_size(), _stream())
+    check(st, "hap_moe_permute")
+
+
+def moe_combine(y: torch.Tensor, dst_of_row: torch.Tensor, topk_w: torch.Tensor, T: int, k: int,
+                out: torch.Tensor, residual: Optional[torch.Tensor] = None,
+                shared_y: Optional[torch.Tensor] = None, shared_gate: Optional[torch.Tensor] = None,
+                res_row0: int = 0, res_rows: Optional[int] = None) -> None:
+    """out[t] = sum_j w * y[dst] (+ sg * shared_y) (+ residual[t - res_row0] inside the row window)."""
+    lib = _lib.load()
+    _need(y, "y", BF16); _need(out, "out", BF16)
+    for t, n in ((y, "y"), (out, "out"), (residual, "residual"), (shared_y, "shared_y")):
+        if t is not None and not t.is_contiguous():
+            raise ValueError(f"{n} must be contiguous")
+    h = out.shape[1]
+    if residual is not None and res_rows is None:
+        res_rows = residual.shape[0]
+    st = lib.hap_moe_combine(y.data_ptr(), dst_of_row.data_ptr(), topk_w.data_ptr(), T, k, h, _ptr(residual),
+                             int(res_row0), int(res_rows or 0), _ptr(shared_y), _ptr(shared_gate), out.data_ptr(),
+                             _stream())
+    check(st, "hap_moe_combine")
+
+
+def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    lib = _lib.load()
+    _need(x, "x", BF16); _need(w, "w", BF16)
+    _rowmajor(x, "x")
+    if out is None:
+        out = torch.empty(x.shape, device=x.device, dtype=BF16)
+    st = lib.hap_rmsnorm(x.data_ptr(), x.shape[0], x.shape[1], x.stride(0), w.data_ptr(), float(eps),
+                         out.data_ptr(), out.stride(0), _stream())
+    check(st, "hap_rmsnorm")
+    return out
+
+
+def rope_qk(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, positions: torch.Tensor, theta: float):
+    lib = _lib.load()
+    _need(qkv, "qkv", BF16); _need(positions, "positions", torch.int32)
+    _rowmajor(qkv, "qkv")
+    st = lib.hap_rope_qk(qkv.data_ptr(), qkv.shape[0], qkv.stride(0), n_q, n_kv, head_dim, positions.data_ptr(),
+                         float(theta), _stream())
+    check(st, "hap_rope_qk")
+
+
+def attn_prefill(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, n_seqs: int, seq_len: int,
+                 out: torch.Tensor, causal: bool = True) -> torch.Tensor:
+    """Attention over a fused [T, (n_q + 2 n_kv) * d] qkv buffer -> out [T, n_q * d]."""
+    lib = _lib.load()
+    _need(qkv, "qkv", BF16); _need(out, "out", BF16)
+    _rowmajor(qkv, "qkv"); _rowmajor(out, "out")
+    ld = qkv.stride(0)
+    base = qkv.data_ptr()
+    esz = qkv.element_size()
+    st = lib.hap_attn_prefill(base, ld, base + n_q * head_dim * esz, ld, base + (n_q + n_kv) * head_dim * esz, ld,
+                              out.data_ptr(), out.stride(0), n_seqs, seq_len, n_q, n_kv, head_dim,
+                              float(head_dim ** -0.5), int(causal), _stream())
+    check(st, "hap_attn_prefill")
+    return out
+
+
+def attn_decode_workspace_bytes(B: int, n_q: int, head_dim: int, max_len: int) -> int:
+    return int(_lib.load().hap_attn_decode_workspace_bytes(B, n_q, head_dim, max_len))
+
+
+def attn_decode(qkv: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, pos: torch.Tensor,
+                n_q: int, n_kv: int, head_dim: int, out: torch.Tensor, workspace: torch.Tensor) -> torch.Tensor:
+    lib = _lib.load()
+    _need(qkv, "qkv", BF16); _need(k_cache, "k_cache", BF16); _need(v_cache, "v_cache", BF16)
+    _need(pos, "pos", torch.int32); _need(out, "out", BF16)
+    if k_cache.dim() != 4 or not k_cache.is_contiguous() or not v_cache.is_contiguous():
+        raise ValueError("caches must be contiguous [B, n_kv, max_len, d]")
+    B, _, max_len, _ = k_cache.shape
+    st = lib.hap_attn_decode(qkv.data_ptr(), qkv.stride(0), k_cache.data_ptr(), v_cache.data_ptr(), max_len,
+                             pos.data_ptr(), B, n_q, n_kv, head_dim, float(head_dim ** -0.5), out.data_ptr(),
+                             out.stride(0), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                             _stream())
+    check(st, "hap_attn_decode")
+    return out

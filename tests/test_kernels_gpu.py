@@ -1,0 +1,273 @@
+"""Kernel-level parity on a B200: every C-ABI op against the CPU oracle.
+
+Bit-exact: router top-k indices (same bf16 input, fixed fp32 reduction
+order), permutation (dst_of_row, seg).  Toleranced (stated per test):
+GEMMs (bf16 out, fp32 accumulate), combine, norm, rope, attention.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_block as O
+
+pytestmark = pytest.mark.gpu
+
+dev = "cuda"
+
+
+def K():
+    from paper_2508_19373_b200 import ops
+
+    return ops
+
+
+def np32(t):
+    return t.detach().float().cpu().numpy()
+
+
+def rel_err(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def bf16(shape, std=1.0, seed=0):
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    return (torch.randn(shape, device=dev, generator=g) * std).to(torch.bfloat16)
+
+
+# ------------------------------------------------------------------ GEMM --
+@pytest.mark.parametrize("M,N,Kd", [(1, 64, 64), (128, 256, 64), (77, 4096, 512), (1000, 768, 4096),
+                                    (300, 6144, 4096), (64, 28672, 4096)])
+def test_dense_gemm(M, N, Kd):
+    a, b = bf16((M, Kd), seed=1), bf16((N, Kd), 0.05, seed=2)
+    c = K().gemm(a, b)
+    torch.cuda.synchronize()
+    ref = np32(a).astype(np.float64) @ np32(b).astype(np.float64).T
+    assert rel_err(np32(c), ref) < 1e-2  # bf16 output rounding
+
+
+def test_gemm_bias_residual():
+    a, b = bf16((300, 256), seed=1), bf16((768, 256), seed=2)
+    bias, res = bf16((768,), seed=3), bf16((300, 768), seed=4)
+    c = K().gemm(a, b, bias=bias, residual=res)
+    torch.cuda.synchronize()
+    ref = np32(a).astype(np.float64) @ np32(b).T + np32(bias) + np32(res)
+    assert rel_err(np32(c), ref) < 1e-2
+
+
+@pytest.mark.parametrize("inter", [1792, 1408, 704, 176, 320])
+def test_grouped_gemm_swiglu_ragged(inter):
+    from paper_2508_19373_b200.weights import interleave_gate_up, swiglu_half_width
+
+    E, h = 8, 512
+    counts = [0, 130, 1, 257, 64, 0, 300, 128]
+    seg = np.zeros(E + 1, dtype=np.int32)
+    seg[1:] = np.cumsum(counts)
+    R = int(seg[-1])
+    x = bf16((R, h), seed=5)
+    w1, w3 = bf16((E, inter, h), 0.05, seed=6), bf16((E, inter, h), 0.05, seed=7)
+    hw = swiglu_half_width(inter)
+    assert hw == K().swiglu_half_width(inter)
+    w13 = interleave_gate_up(w1, w3, hw)
+    H = torch.empty(R, inter, device=dev, dtype=torch.bfloat16)
+    K().grouped_gemm(x, w13, E, torch.from_numpy(seg).to(dev), H, swiglu_half=hw)
+    torch.cuda.synchronize()
+    xs = np32(x).astype(np.float64)
+    ref = np.zeros((R, inter))
+    for e in range(E):
+        r0, r1 = seg[e], seg[e + 1]
+        g = xs[r0:r1] @ np32(w1[e]).T
+        u = xs[r0:r1] @ np32(w3[e]).T
+        ref[r0:r1] = g / (1 + np.exp(-g)) * u
+    assert rel_err(np32(H), ref) < 2e-2
+
+
+def test_grouped_gemm_segment_groups():
+    """EP receive layout: several segments mapped to the same weight group."""
+    El, N, Kd = 4, 256, 256
+    rc = np.array([[3, 0, 129, 5], [0, 77, 1, 2]])  # (src, local expert)
+    seg = np.zeros(rc.size + 1, dtype=np.int32)
+    seg[1:] = np.cumsum(rc.reshape(-1))
+    grp = np.tile(np.arange(El, dtype=np.int32), 2)
+    R = int(seg[-1])
+    a, b = bf16((R, Kd), seed=8), bf16((El * N, Kd), 0.05, seed=9)
+    c = torch.empty(R, N, device=dev, dtype=torch.bfloat16)
+    K().grouped_gemm(a, b, El, torch.from_numpy(seg).to(dev), c, seg_group=torch.from_numpy(grp).to(dev))
+    torch.cuda.synchronize()
+    ref = np.zeros((R, N))
+    for s in range(rc.size):
+        g = grp[s]
+        ref[seg[s]:seg[s + 1]] = np32(a)[seg[s]:seg[s + 1]].astype(np.float64) @ np32(b)[g * N:(g + 1) * N].T
+    assert rel_err(np32(c), ref) < 1e-2
+
+
+# ---------------------------------------------------------------- router --
+@pytest.mark.parametrize("T,h,E,k,renorm,shared", [(1000, 512, 8, 2, True, False), (517, 2048, 60, 4, False, True),
+                                                   (300, 3584, 64, 8, False, True), (64, 4096, 8, 2, True, False)])
+def test_router_bit_exact(T, h, E, k, renorm, shared):
+    x = bf16((T, h), seed=10)
+    w = bf16((E + int(shared), h), 0.02, seed=11)
+    idx = torch.empty(T, k, device=dev, dtype=torch.int32)
+    tw = torch.empty(T, k, device=dev, dtype=torch.float32)
+    sg = torch.empty(T, device=dev, dtype=torch.float32) if shared else None
+    logits = torch.empty(T, E, device=dev, dtype=torch.float32)
+    K().router_topk(x, w, E, k, renorm, shared, idx, tw, sg, logits)
+    torch.cuda.synchronize()
+    ol = O.router_logits(np32(x), np32(w)[:E])
+    assert np.array_equal(np32(logits), ol), "fp32 logits must be bit-identical (fixed reduction order)"
+    oi, ow = O.router_topk(ol, k, renorm)
+    assert np.array_equal(idx.cpu().numpy(), oi), "top-k indices must be bit-exact"
+    assert np.abs(tw.cpu().numpy() - ow).max() < 1e-6
+    if shared:
+        og = O.router_logits(np32(x), np32(w)[E:])[:, 0]
+        assert np.abs(sg.cpu().numpy() - 1 / (1 + np.exp(-og.astype(np.float64)))).max() < 1e-6
+
+
+def test_router_ties_lower_index():
+    T, h, E, k = 64, 256, 8, 2
+    x = torch.ones(T, h, device=dev, dtype=torch.bfloat16)
+    w = torch.zeros(E, h, device=dev, dtype=torch.bfloat16)  # all logits equal
+    idx = torch.empty(T, k, device=dev, dtype=torch.int32)
+    tw = torch.empty(T, k, device=dev, dtype=torch.float32)
+    K().router_topk(x, w, E, k, True, False, idx, tw)
+    torch.cuda.synchronize()
+    assert (idx.cpu().numpy() == np.array([0, 1])).all()
+    assert np.allclose(tw.cpu().numpy(), 0.5)
+
+
+# --------------------------------------------------------------- permute --
+@pytest.mark.parametrize("T,k,E", [(1, 2, 8), (1000, 2, 8), (16384, 2, 8), (4096, 8, 64), (777, 4, 60)])
+def test_permute_bit_exact(T, k, E):
+    rng = np.random.default_rng(T + E)
+    eid = rng.integers(0, E, size=T * k).astype(np.int32)
+    eid[::97] = 3 % E  # skew
+    h = 256
+    x = bf16((T, h), seed=12)
+    ops = K()
+    R = T * k
+    x_out = torch.empty(R, h, device=dev, dtype=torch.bfloat16)
+    dst = torch.empty(R, device=dev, dtype=torch.int32)
+    seg = torch.empty(E + 1, device=dev, dtype=torch.int32)
+    ws = torch.empty(ops.permute_workspace_bytes(R, E), device=dev, dtype=torch.uint8)
+    ops.moe_permute(torch.from_numpy(eid).to(dev), E, x, k, x_out, dst, seg, ws)
+    torch.cuda.synchronize()
+    od, os_ = O.permute_index(eid, E)
+    assert np.array_equal(dst.cpu().numpy(), od)
+    assert np.array_equal(seg.cpu().numpy(), os_)
+    xo = x_out.cpu()
+    xs = x.cpu()
+    rows = np.arange(R)
+    assert torch.equal(xo[torch.from_numpy(od.astype(np.int64))], xs[torch.from_numpy(rows // k)])
+
+
+def test_permute_drops_invalid_and_empty():
+    ops = K()
+    eid = torch.tensor([2, -1, 9, 0, 2, 1], device=dev, dtype=torch.int32)
+    E = 4
+    dst = torch.empty(6, device=dev, dtype=torch.int32)
+    seg = torch.empty(E + 1, device=dev, dtype=torch.int32)
+    ws = torch.empty(ops.permute_workspace_bytes(6, E), device=dev, dtype=torch.uint8)
+    ops.moe_permute(eid, E, None, 1, None, dst, seg, ws)
+    torch.cuda.synchronize()
+    od, os_ = O.permute_index(eid.cpu().numpy(), E)
+    assert np.array_equal(dst.cpu().numpy(), od) and np.array_equal(seg.cpu().numpy(), os_)
+    # R = 0
+    e0 = torch.empty(0, device=dev, dtype=torch.int32)
+    ops.moe_permute(e0, E, None, 1, None, torch.empty(0, device=dev, dtype=torch.int32), seg, ws)
+    torch.cuda.synchronize()
+    assert seg.cpu().numpy().tolist() == [0] * (E + 1)
+
+
+# --------------------------------------------------------------- combine --
+def test_combine_with_shared_and_residual_window():
+    ops = K()
+    T, k, h = 300, 4, 512
+    R = T * k
+    y = bf16((R, h), seed=13)
+    perm = torch.randperm(R, device=dev).to(torch.int32)
+    tw = torch.rand(T, k, device=dev)
+    res = bf16((100, h), seed=14)
+    ys = bf16((T, h), seed=15)
+    sg = torch.rand(T, device=dev)
+    out = torch.empty(T, h, device=dev, dtype=torch.bfloat16)
+    ops.moe_combine(y, perm, tw, T, k, out, residual=res, shared_y=ys, shared_gate=sg, res_row0=50, res_rows=100)
+    torch.cuda.synchronize()
+    yy = np32(y)[perm.cpu().numpy()].reshape(T, k, h)
+    ref = (yy * tw.cpu().numpy()[..., None]).sum(1) + sg.cpu().numpy()[:, None] * np32(ys)
+    ref[50:150] += np32(res)
+    assert rel_err(np32(out), ref) < 1e-2
+
+
+# ------------------------------------------------------------ norm / rope --
+def test_rmsnorm():
+    x = bf16((333, 4096), seed=16)
+    w = (1 + 0.1 * torch.randn(4096, device=dev)).to(torch.bfloat16)
+    out = K().rmsnorm(x, w, 1e-5)
+    torch.cuda.synchronize()
+    ref = O.rmsnorm(np32(x), np32(w), 1e-5)
+    assert rel_err(np32(out), ref) < 1e-2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_rope(d):
+    T, nq, nkv = 50, 4, 2
+    qkv = bf16((T, (nq + 2 * nkv) * d), seed=17)
+    pos = torch.randint(0, 4096, (T,), device=dev, dtype=torch.int32)
+    ref_in = np32(qkv).copy()
+    K().rope_qk(qkv, nq, nkv, d, pos, 1e6)
+    torch.cuda.synchronize()
+    p = pos.cpu().numpy()
+    q = O.rope(ref_in[:, :nq * d].reshape(T, nq, d), p, 1e6).reshape(T, -1)
+    kk = O.rope(ref_in[:, nq * d:(nq + nkv) * d].reshape(T, nkv, d), p, 1e6).reshape(T, -1)
+    got = np32(qkv)
+    assert np.abs(got[:, :nq * d] - q).max() < 3e-2
+    assert np.abs(got[:, nq * d:(nq + nkv) * d] - kk).max() < 3e-2
+    assert np.array_equal(got[:, (nq + nkv) * d:], ref_in[:, (nq + nkv) * d:])  # v untouched
+
+
+# ------------------------------------------------------------- attention --
+@pytest.mark.parametrize("d,nq,nkv,S,B", [(128, 8, 2, 200, 2), (64, 8, 2, 128, 4), (128, 4, 4, 1000, 1)])
+def test_attn_prefill(d, nq, nkv, S, B):
+    T = B * S
+    qkv = bf16((T, (nq + 2 * nkv) * d), seed=18)
+    out = torch.empty(T, nq * d, device=dev, dtype=torch.bfloat16)
+    K().attn_prefill(qkv, nq, nkv, d, B, S, out)
+    torch.cuda.synchronize()
+    a = np32(qkv)
+    ref = []
+    for s in range(B):
+        blk = a[s * S:(s + 1) * S]
+        q = blk[:, :nq * d].reshape(S, nq, d)
+        k = blk[:, nq * d:(nq + nkv) * d].reshape(S, nkv, d)
+        v = blk[:, (nq + nkv) * d:].reshape(S, nkv, d)
+        ref.append(O.attention(q, k, v).reshape(S, -1))
+    assert rel_err(np32(out), np.concatenate(ref)) < 2e-2
+
+
+@pytest.mark.parametrize("d,nq,nkv", [(128, 32, 8), (64, 8, 2), (128, 28, 4), (128, 16, 16)])
+def test_attn_decode(d, nq, nkv):
+    B, Lmax = 5, 700
+    qkv = bf16((B, (nq + 2 * nkv) * d), seed=19)
+    kc = bf16((B, nkv, Lmax, d), seed=20)
+    vc = bf16((B, nkv, Lmax, d), seed=21)
+    pos = torch.tensor([0, 1, 255, 256, 699], device=dev, dtype=torch.int32)
+    kc0, vc0 = np32(kc), np32(vc)
+    ops = K()
+    out = torch.empty(B, nq * d, device=dev, dtype=torch.bfloat16)
+    ws = torch.empty(ops.attn_decode_workspace_bytes(B, nq, d, Lmax), device=dev, dtype=torch.uint8)
+    ops.attn_decode(qkv, kc, vc, pos, nq, nkv, d, out, ws)
+    torch.cuda.synchronize()
+    a = np32(qkv)
+    kcn, vcn = np32(kc), np32(vc)
+    for b in range(B):
+        p = int(pos[b])
+        knew = a[b, nq * d:(nq + nkv) * d].reshape(nkv, d)
+        vnew = a[b, (nq + nkv) * d:].reshape(nkv, d)
+        assert np.array_equal(kcn[b, :, p], knew) and np.array_equal(vcn[b, :, p], vnew)
+        kk = np.concatenate([kc0[b, :, :p], knew[:, None]], 1).transpose(1, 0, 2)
+        vv = np.concatenate([vc0[b, :, :p], vnew[:, None]], 1).transpose(1, 0, 2)
+        ref = O.attention(a[b, :nq * d].reshape(1, nq, d), kk, vv, causal=True).reshape(-1)
+        assert rel_err(np32(out[b]), ref) < 2e-2
