@@ -23,8 +23,8 @@ collective schedule on gloo (see tests/test_executor_dist.py).
 
 from __future__ import annotations
 
+from contextlib import contextmanager
 from dataclasses import dataclass
-from math import ceil
 from typing import Optional
 
 import torch
@@ -101,6 +101,8 @@ class HapMoEBlock:
         del full
         self.comm = comm if comm is not None else (Comm(self.lay) if self.lay.n > 1 else None)
         self.last_routing = None  # (topk_idx, dst_of_row, seg) of the last expert call, for parity tests
+        self.capture = None       # set to {} to keep references to intermediates (tests only)
+        self.timers = None        # set to {} to record CUDA events around the expert GEMMs (bench)
 
     @classmethod
     def from_plan(cls, cfg: BlockConfig, plan, stage: str = "prefill", **kw) -> "HapMoEBlock":
@@ -109,6 +111,18 @@ class HapMoEBlock:
         return cls(cfg, plan.attention, exp, **kw)
 
     # ------------------------------------------------------------ helpers --
+    @contextmanager
+    def _timed(self, name):
+        if self.timers is None:
+            yield
+            return
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        yield
+        e.record()
+        self.timers.setdefault(name, []).append((s, e))
+
     def _coll(self, name, *args):
         if self.comm is None:
             return None
@@ -186,7 +200,8 @@ class HapMoEBlock:
             hn_s = hn[p * rs:(p + 1) * rs]
         else:
             hn_s = hn
-        rows_s = hn_s.shape[0]
+        if self.capture is not None:
+            self.capture.update(h1=h1, hn=hn, hn_s=hn_s)
 
         # ---------------- expert module (partial over expert tp)
         c = rows // self.deg.a_tp  # rows this rank owns after the reduce-scatter
@@ -222,12 +237,16 @@ class HapMoEBlock:
         ws = torch.empty(max(ops.permute_workspace_bytes(R, E), 16), device=dev, dtype=torch.uint8)
         ops.moe_permute(idx.view(-1), E, hn_s, k, x_perm, dst, seg, ws)
         self.last_routing = (idx, dst, seg)
+        if self.capture is not None:
+            self.capture.update(topk_w=tw, shared_gate=sg)
         il = w.inter_local
         if self.deg.e_ep == 1:
             H = torch.empty(R, il, device=dev, dtype=BF16)
-            ops.grouped_gemm(x_perm, w.w13, E, seg, H, swiglu_half=w.hw)
+            with self._timed("gate_up"):
+                ops.grouped_gemm(x_perm, w.w13, E, seg, H, swiglu_half=w.hw)
             Y = torch.empty(R, h, device=dev, dtype=BF16)
-            ops.grouped_gemm(H, w.w2, E, seg, Y)
+            with self._timed("down"):
+                ops.grouped_gemm(H, w.w2, E, seg, Y)
         else:
             Y = self._ep_experts(x_perm, seg)
         ys = None
@@ -263,8 +282,10 @@ class HapMoEBlock:
         H = torch.empty(n_recv, il, device=dev, dtype=BF16)
         Y_r = torch.empty(n_recv, h, device=dev, dtype=BF16)
         if n_recv:
-            ops.grouped_gemm(x_recv, w.w13, El, seg_r, H, swiglu_half=w.hw, seg_group=grp)
-            ops.grouped_gemm(H, w.w2, El, seg_r, Y_r, seg_group=grp)
+            with self._timed("gate_up"):
+                ops.grouped_gemm(x_recv, w.w13, El, seg_r, H, swiglu_half=w.hw, seg_group=grp)
+            with self._timed("down"):
+                ops.grouped_gemm(H, w.w2, El, seg_r, Y_r, seg_group=grp)
         Y = torch.empty(x_perm.shape[0], h, device=dev, dtype=BF16)
         comm.all_to_all(Y, Y_r, send, recv, "a2a_group")
         return Y

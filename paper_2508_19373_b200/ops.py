@@ -17,6 +17,13 @@ from ._lib import HAP_EPI_STORE, HAP_EPI_SWIGLU, check
 
 BF16 = torch.bfloat16
 
+# Kernel launches issued through this module (the bench's gpu_launches claim).
+LAUNCHES = [0]
+
+
+def _count(n: int = 1) -> None:
+    LAUNCHES[0] += n
+
 
 def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else t.data_ptr()
@@ -85,6 +92,7 @@ def grouped_gemm(a: torch.Tensor, b: torch.Tensor, n_groups: int, seg: Optional[
                                    _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0,
                                    _stream())
     check(st, "hap_grouped_gemm_bf16")
+    _count(1 if a.shape[0] else 0)
     return out
 
 
@@ -109,6 +117,7 @@ def router_topk(x: torch.Tensor, w: torch.Tensor, n_experts: int, top_k: int, re
                              int(renormalize), int(has_shared_gate), topk_idx.data_ptr(), topk_w.data_ptr(),
                              _ptr(shared_gate), _ptr(logits), _stream())
     check(st, "hap_router_topk")
+    _count(1 if x.shape[0] else 0)
 
 
 def permute_workspace_bytes(rows: int, n_experts: int) -> int:
@@ -132,6 +141,7 @@ def moe_permute(expert_of_row: torch.Tensor, n_experts: int, x: Optional[torch.T
                              dst_of_row.data_ptr(), seg.data_ptr(), workspace.data_ptr(),
                              workspace.numel() * workspace.element_size(), _stream())
     check(st, "hap_moe_permute")
+    _count(3 if R else 0)
 
 
 def moe_combine(y: torch.Tensor, dst_of_row: torch.Tensor, topk_w: torch.Tensor, T: int, k: int,
@@ -151,6 +161,7 @@ def moe_combine(y: torch.Tensor, dst_of_row: torch.Tensor, topk_w: torch.Tensor,
                              int(res_row0), int(res_rows or 0), _ptr(shared_y), _ptr(shared_gate), out.data_ptr(),
                              _stream())
     check(st, "hap_moe_combine")
+    _count(1 if T else 0)
 
 
 def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -162,6 +173,7 @@ def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float, out: Optional[torch.Te
     st = lib.hap_rmsnorm(x.data_ptr(), x.shape[0], x.shape[1], x.stride(0), w.data_ptr(), float(eps),
                          out.data_ptr(), out.stride(0), _stream())
     check(st, "hap_rmsnorm")
+    _count(1 if x.shape[0] else 0)
     return out
 
 
@@ -172,6 +184,7 @@ def rope_qk(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, positions: to
     st = lib.hap_rope_qk(qkv.data_ptr(), qkv.shape[0], qkv.stride(0), n_q, n_kv, head_dim, positions.data_ptr(),
                          float(theta), _stream())
     check(st, "hap_rope_qk")
+    _count(1 if qkv.shape[0] else 0)
 
 
 def attn_prefill(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, n_seqs: int, seq_len: int,
@@ -187,6 +200,7 @@ def attn_prefill(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, n_seqs: 
                               out.data_ptr(), out.stride(0), n_seqs, seq_len, n_q, n_kv, head_dim,
                               float(head_dim ** -0.5), int(causal), _stream())
     check(st, "hap_attn_prefill")
+    _count(1 if n_seqs * seq_len else 0)
     return out
 
 
@@ -207,4 +221,5 @@ def attn_decode(qkv: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
                              out.stride(0), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
                              _stream())
     check(st, "hap_attn_decode")
+    _count(3 if B else 0)
     return out
