@@ -84,16 +84,31 @@ int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda, int64_t K,
                           void* stream);
 
 /*
+ * Fused QKV projection + rotary embedding (same tcgen05 kernel, RoPE in the
+ * epilogue): C = A . W^T (+bias), then for the first n_rope_heads heads of
+ * each row (the q and k heads of a [q | k | v] row) the rotate-half RoPE with
+ * angle positions[r] * theta^(-2i/head_dim) (fp32), one bf16 rounding.
+ * head_dim in {64, 128}; N % head_dim == 0.
+ * Replaces: the Q/K/V projection term of attention_flops (arch.py:157-160)
+ * plus the (unmodelled) rotary embedding.
+ */
+int hap_gemm_qkv_rope(const void* A, int64_t M, int64_t lda, int64_t K, const void* W, int64_t N,
+                      const void* bias, void* C, int64_t ldc, const int32_t* positions, int64_t n_rope_heads,
+                      int64_t head_dim, float theta, void* stream);
+
+/*
  * Router: logits[t,e] = x[t,:] . w[e,:] in fp32 with a FIXED reduction
- * order — acc = fma(x[t,j], w[e,j], acc) for j = 0..h-1 sequentially (the
- * bf16*bf16 products are exact in fp32, so this equals the sequential fp32 sum
- * of products the oracle computes) — softmax in fp32, top-k selected on
- * logits with ties to the lower expert index, weights = softmax probabilities
- * of the selected experts, renormalised to sum 1 when `renormalize`.
+ * order — h is cut into 8 equal contiguous ranges; in range p the partial is
+ * the sequential chain acc = fma(x[t,j], w[e,j], acc) (bf16*bf16 products are
+ * exact in fp32, so this is the sequential fp32 sum of products), and the
+ * partials are added in order ((p0 + p1) + p2) + ... — the order the oracle
+ * computes.  Softmax in fp32, top-k selected on logits with ties to the
+ * lower expert index, weights = softmax probabilities of the selected
+ * experts, renormalised to sum 1 when `renormalize`.
  * If has_shared_gate, w has n_experts+1 rows and row n_experts is the
  * shared-expert gate: shared_gate[t] = sigmoid(x[t] . w[E]) (fp32).
  * logits_out (fp32 [T, n_experts]) is optional.
- * Requires h % 256 == 0, n_experts + has_shared_gate <= 72, top_k <= 32.
+ * Requires h % 64 == 0, n_experts + has_shared_gate <= 72, top_k <= 32.
  * Replaces: the router term 2*T*h*E of expert_flops (arch.py:177).
  */
 int hap_router_topk(const void* x, int64_t T, int64_t h, const void* w, int64_t n_experts, int64_t top_k,

@@ -42,6 +42,11 @@ SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
          c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_int64, c_void_p],
     ),
+    "hap_gemm_qkv_rope": (
+        ctypes.c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
+         c_int64, c_int64, c_float, c_void_p],
+    ),
     "hap_router_topk": (
         ctypes.c_int,
         [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int32, c_int32, c_void_p, c_void_p,

@@ -270,9 +270,13 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __nv_bfloa
                                                                 const int32_t* __restrict__ pos, int n_q, int n_kv,
                                                                 float scale_log2, float* __restrict__ ws_o,
                                                                 float* __restrict__ ws_ml, int n_splits) {
+  constexpr int LPK = D / 8;              // lanes per key row (16 B each)
+  constexpr int KPP = kThreads / LPK;     // keys per CTA pass
+  constexpr int U = 4;                    // passes in flight per thread
   __shared__ float qs[G][D];
   __shared__ float sc[G][kSplit];
-  __shared__ float red[G][kThreads / (D / 2)][D];
+  __shared__ float red[KPP][G][D];
+  __shared__ float mstat[G], lstat[G];
   const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
   const int L = pos[b] + 1;
   const int k0 = split * kSplit;
@@ -293,46 +297,49 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __nv_bfloa
     qs[gg][d] = __bfloat162float(qkv[(int64_t)b * ld + (int64_t)(kvh * G + gg) * D + d]);
   }
   __syncthreads();
-  const __nv_bfloat16* kbase = kc + (((int64_t)b * n_kv + kvh) * max_len) * D;
-  const __nv_bfloat16* vbase = vc + (((int64_t)b * n_kv + kvh) * max_len) * D;
-  // scores: half-warp per key, 8 dims per lane
-  // LPK lanes per key (8 dims each): D=128 -> 16 lanes, 2 keys per warp pass
-  constexpr int LPK = D / 8;
-  constexpr int KPW = 32 / LPK;
-  const int half = lane / LPK, l16 = lane % LPK;
+  const __nv_bfloat16* kbase = kc + (((int64_t)b * n_kv + kvh) * max_len + k0) * D;
+  const __nv_bfloat16* vbase = vc + (((int64_t)b * n_kv + kvh) * max_len + k0) * D;
+  const int kr = threadIdx.x / LPK;   // key slot within a pass
+  const int l16 = threadIdx.x % LPK;  // 8-dim slice
   float qreg[G][8];
 #pragma unroll
   for (int gg = 0; gg < G; ++gg)
 #pragma unroll
     for (int i = 0; i < 8; ++i) qreg[gg][i] = qs[gg][l16 * 8 + i];
-  for (int kb = warp * KPW; kb < nk; kb += KPW * (kThreads / 32)) {  // warp-uniform trip count
-    const int kk = kb + half;
-    const bool kv_ok = kk < nk;
-    const uint4 kv4 = kv_ok ? __ldg(reinterpret_cast<const uint4*>(kbase + (int64_t)(k0 + kk) * D + l16 * 8))
-                            : make_uint4(0, 0, 0, 0);
-    const uint32_t kw[4] = {kv4.x, kv4.y, kv4.z, kv4.w};
-    float kf[8];
+
+  // ---- scores: U passes of KPP keys in flight
+  for (int kb = 0; kb < nk; kb += KPP * U) {
+    uint4 kv4[U];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 f = unpack_bf16x2(kw[i]);
-      kf[2 * i] = f.x;
-      kf[2 * i + 1] = f.y;
+    for (int u = 0; u < U; ++u) {
+      const int kk = kb + u * KPP + kr;
+      kv4[u] = kk < nk ? __ldg(reinterpret_cast<const uint4*>(kbase + (int64_t)kk * D + l16 * 8))
+                       : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int gg = 0; gg < G; ++gg) {
-      float acc = 0.f;
+    for (int u = 0; u < U; ++u) {
+      const int kk = kb + u * KPP + kr;
+      const uint32_t kw[4] = {kv4[u].x, kv4[u].y, kv4[u].z, kv4[u].w};
+      float kf[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc = fmaf(qreg[gg][i], kf[i], acc);
-      if (LPK > 8) acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      if (l16 == 0 && kv_ok) sc[gg][kk] = acc * scale_log2;
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = unpack_bf16x2(kw[i]);
+        kf[2 * i] = f.x;
+        kf[2 * i + 1] = f.y;
+      }
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc = fmaf(qreg[gg][i], kf[i], acc);
+#pragma unroll
+        for (int o2 = LPK / 2; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
+        if (l16 == 0 && kk < nk) sc[gg][kk] = acc * scale_log2;
+      }
     }
   }
   __syncthreads();
-  // softmax stats per query head (warp gg handles head gg, looping)
-  __shared__ float mstat[G], lstat[G];
+  // ---- softmax statistics per query head
   for (int gg = warp; gg < G; gg += kThreads / 32) {
     float m = -INFINITY;
     for (int i = lane; i < nk; i += 32) m = fmaxf(m, sc[gg][i]);
@@ -352,33 +359,50 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __nv_bfloa
     }
   }
   __syncthreads();
-  // O = P V : thread owns a dim pair; KH interleaved key groups
-  constexpr int KH = kThreads / (D / 2);
-  const int dp = threadIdx.x % (D / 2), kh = threadIdx.x / (D / 2);
-  float acc[G][2];
+  // ---- O = P V: thread owns an 8-dim slice of key slot kr, U rows in flight
+  float acc[G][8];
 #pragma unroll
-  for (int gg = 0; gg < G; ++gg) acc[gg][0] = acc[gg][1] = 0.f;
-  for (int kk = kh; kk < nk; kk += KH) {
-    const uint32_t vv = __ldg(reinterpret_cast<const uint32_t*>(vbase + (int64_t)(k0 + kk) * D + dp * 2));
-    const float2 f = unpack_bf16x2(vv);
+  for (int gg = 0; gg < G; ++gg)
 #pragma unroll
-    for (int gg = 0; gg < G; ++gg) {
-      const float p = sc[gg][kk];
-      acc[gg][0] = fmaf(p, f.x, acc[gg][0]);
-      acc[gg][1] = fmaf(p, f.y, acc[gg][1]);
+    for (int i = 0; i < 8; ++i) acc[gg][i] = 0.f;
+  for (int kb = 0; kb < nk; kb += KPP * U) {
+    uint4 vv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = kb + u * KPP + kr;
+      vv[u] = kk < nk ? __ldg(reinterpret_cast<const uint4*>(vbase + (int64_t)kk * D + l16 * 8))
+                      : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = kb + u * KPP + kr;
+      if (kk >= nk) continue;
+      const uint32_t vw[4] = {vv[u].x, vv[u].y, vv[u].z, vv[u].w};
+      float vf[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = unpack_bf16x2(vw[i]);
+        vf[2 * i] = f.x;
+        vf[2 * i + 1] = f.y;
+      }
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        const float p = sc[gg][kk];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[gg][i] = fmaf(p, vf[i], acc[gg][i]);
+      }
     }
   }
 #pragma unroll
-  for (int gg = 0; gg < G; ++gg) {
-    red[gg][kh][dp * 2] = acc[gg][0];
-    red[gg][kh][dp * 2 + 1] = acc[gg][1];
-  }
+  for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[kr][gg][l16 * 8 + i] = acc[gg][i];
   __syncthreads();
   for (int i = threadIdx.x; i < G * D; i += kThreads) {
     const int gg = i / D, d = i % D;
     float sacc = 0.f;
 #pragma unroll
-    for (int q2 = 0; q2 < KH; ++q2) sacc += red[gg][q2][d];
+    for (int q2 = 0; q2 < KPP; ++q2) sacc += red[q2][gg][d];
     ws_o[(out_base + (int64_t)gg * n_splits) * D + d] = sacc;
   }
   if (threadIdx.x < G) {

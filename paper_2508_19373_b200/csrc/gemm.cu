@@ -49,7 +49,15 @@ struct Params {
   const __nv_bfloat16* bias;
   const __nv_bfloat16* resid;
   int64_t ldr;
+  // rope epilogue
+  const int32_t* positions;
+  int32_t head_dim;
+  int32_t rope_cols;
+  float theta;
 };
+
+constexpr int kEpiRope = 2;     // internal epilogue id (hap_gemm_qkv_rope)
+constexpr int kGroupM = 16;     // m-blocks per raster group (L2 reuse of A rows across n-blocks)
 
 struct TileCoord {
   int32_t g, m0, m_end, n_blk;
@@ -68,11 +76,16 @@ __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, 
   const int local = t - tile_start[g];
   const int rows = seg[g + 1] - seg[g];
   const int m_blocks = (rows + BM - 1) / BM;
+  // grouped raster: kGroupM m-blocks x all n-blocks, m fastest inside a group
+  const int grp = local / (kGroupM * n_blocks);
+  const int g0 = grp * kGroupM;
+  const int gsz = min(kGroupM, m_blocks - g0);
+  const int r = local - grp * kGroupM * n_blocks;
   TileCoord c;
   c.g = seg_group[g];
-  c.m0 = seg[g] + (local % m_blocks) * BM;
+  c.m0 = seg[g] + (g0 + r % gsz) * BM;
   c.m_end = seg[g + 1];
-  c.n_blk = local / m_blocks;
+  c.n_blk = r / gsz;
   return c;
 }
 
@@ -93,6 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ int32_t seg_s[kMaxSegs + 1];
   __shared__ int32_t group_s[kMaxSegs];
   __shared__ int32_t tile_start_s[kMaxSegs + 1];
+  __shared__ float inv_freq_s[128];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -103,6 +117,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int i = threadIdx.x; i <= n_segs; i += blockDim.x) {
     seg_s[i] = p.seg ? p.seg[i] : (i == 0 ? 0 : p.a_rows);
     if (i < n_segs) group_s[i] = p.seg_group ? p.seg_group[i] : i;
+  }
+  if (p.epi == kEpiRope) {
+    // HF: inv_freq = 1 / theta^(2i/d) in fp32
+    for (int i = threadIdx.x; i < p.head_dim / 2; i += blockDim.x)
+      inv_freq_s[i] = 1.0f / powf(p.theta, (float)(2 * i) / (float)p.head_dim);
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -217,6 +236,61 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<uint4*>(crow + col0 + j) = make_uint4(o[0], o[1], o[2], o[3]);
           }
         }
+      } else if (p.epi == kEpiRope) {
+        // QKV projection with fused rotary embedding on the q/k head columns:
+        // tile = BN/d whole heads; pairs (i, i + d/2) of a head are rotated by
+        // pos*inv_freq[i] (fp32), bias added first, one bf16 rounding.
+        const int d = p.head_dim, half = d >> 1;
+        const int col0 = c.n_blk * p.BN;
+        const float pos = row_ok ? (float)p.positions[row] : 0.f;
+        for (int hb = 0; hb < p.BN; hb += d) {
+          const int hcol = col0 + hb;
+          const bool rot = hcol < p.rope_cols;
+          for (int i = 0; i < half; i += 8) {
+            uint32_t a[8], b[8];
+            tmem_ld_x8(t_row + hb + i, a);
+            tmem_ld_x8(t_row + hb + half + i, b);
+            tmem_ld_wait();
+            if (!row_ok || hcol >= p.out_cols) continue;
+            float x1[8], x2[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              x1[k] = __uint_as_float(a[k]);
+              x2[k] = __uint_as_float(b[k]);
+            }
+            if (p.bias) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                x1[k] += __bfloat162float(p.bias[hcol + i + k]);
+                x2[k] += __bfloat162float(p.bias[hcol + half + i + k]);
+              }
+            }
+            uint32_t o1[4], o2[4];
+            if (rot) {
+              float y1[8], y2[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                float sn, cs;
+                sincosf(pos * inv_freq_s[i + k], &sn, &cs);
+                y1[k] = x1[k] * cs - x2[k] * sn;
+                y2[k] = x2[k] * cs + x1[k] * sn;
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                o1[k] = pack_bf16x2(y1[2 * k], y1[2 * k + 1]);
+                o2[k] = pack_bf16x2(y2[2 * k], y2[2 * k + 1]);
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                o1[k] = pack_bf16x2(x1[2 * k], x1[2 * k + 1]);
+                o2[k] = pack_bf16x2(x2[2 * k], x2[2 * k + 1]);
+              }
+            }
+            *reinterpret_cast<uint4*>(crow + hcol + i) = make_uint4(o1[0], o1[1], o1[2], o1[3]);
+            *reinterpret_cast<uint4*>(crow + hcol + half + i) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
+          }
+        }
       } else {
         const int col0 = c.n_blk * p.BN;
         for (int j = 0; j < p.BN; j += 32) {
@@ -282,6 +356,27 @@ static int pick_bn(int64_t N) {
   return N < 256 ? (int)((N + 15) / 16 * 16) : 256;
 }
 
+static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                  int64_t n_groups, int64_t N, int64_t n_segs, void* stream) {
+  CUtensorMap tmA, tmB;
+  if (!encode_tmap_2d_bf16(&tmA, A, (uint64_t)K, (uint64_t)a_rows, (uint64_t)lda * 2, BK, BM, true))
+    return HAP_ERR_DRIVER;
+  if (!encode_tmap_2d_bf16(&tmB, B, (uint64_t)K, (uint64_t)(n_groups * N), (uint64_t)K * 2, BK, p.BN, true))
+    return HAP_ERR_DRIVER;
+  static int configured = 0;
+  if (!configured) {
+    if (configure_smem((const void*)grouped_gemm_kernel, kSmemBytes) != 0) return HAP_ERR_LAUNCH;
+    configured = 1;
+  }
+  // Upper bound on tiles without reading seg on the host.
+  const int64_t n_blocks = (N + p.BN - 1) / p.BN;
+  const int64_t max_tiles = ((a_rows + BM - 1) / BM + (n_segs - 1)) * n_blocks;
+  const int grid = (int)(max_tiles < kNumSMs ? max_tiles : kNumSMs);
+  grouped_gemm_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tmA, tmB, p);
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
+}
+
 }  // namespace gemm
 }  // namespace hap
 
@@ -342,22 +437,38 @@ extern "C" int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda,
     return HAP_ERR_INVALID_ARG;
   }
 
-  CUtensorMap tmA, tmB;
-  if (!encode_tmap_2d_bf16(&tmA, A, (uint64_t)K, (uint64_t)a_rows, (uint64_t)lda * 2, BK, BM, true))
-    return HAP_ERR_DRIVER;
-  if (!encode_tmap_2d_bf16(&tmB, B, (uint64_t)K, (uint64_t)(n_groups * N), (uint64_t)K * 2, BK, p.BN, true))
-    return HAP_ERR_DRIVER;
+  return hap::gemm::launch(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
+}
 
-  static int configured = 0;
-  if (!configured) {
-    if (configure_smem((const void*)grouped_gemm_kernel, kSmemBytes) != 0) return HAP_ERR_LAUNCH;
-    configured = 1;
-  }
-  // Upper bound on tiles without reading seg on the host.
-  const int64_t n_blocks = (N + p.BN - 1) / p.BN;
-  const int64_t max_tiles = ((a_rows + BM - 1) / BM + (n_segs - 1)) * n_blocks;
-  const int grid = (int)(max_tiles < kNumSMs ? max_tiles : kNumSMs);
-  grouped_gemm_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tmA, tmB, p);
-  HAP_CHECK_LAUNCH();
-  return HAP_OK;
+extern "C" int hap_gemm_qkv_rope(const void* A, int64_t M, int64_t lda, int64_t K, const void* W, int64_t N,
+                                 const void* bias, void* C, int64_t ldc, const int32_t* positions,
+                                 int64_t n_rope_heads, int64_t head_dim, float theta, void* stream) {
+  using namespace hap::gemm;
+  if (!A || !W || !C || !positions || M < 0 || K <= 0 || N <= 0) return HAP_ERR_INVALID_ARG;
+  if (head_dim != 64 && head_dim != 128) return HAP_ERR_UNSUPPORTED;
+  if (N % head_dim || n_rope_heads < 0 || n_rope_heads * head_dim > N) return HAP_ERR_INVALID_ARG;
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return HAP_ERR_UNSUPPORTED;
+  if (K % 8 || lda % 8 || ldc % 8 || lda < K || ldc < N) return HAP_ERR_MISALIGNED;
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(C)) & 15)
+    return HAP_ERR_MISALIGNED;
+  if (M == 0) return HAP_OK;
+  Params p{};
+  p.a_rows = (int32_t)M;
+  p.K = (int32_t)K;
+  p.N = (int32_t)N;
+  p.n_segs = 1;
+  p.epi = kEpiRope;
+  p.C = reinterpret_cast<__nv_bfloat16*>(C);
+  p.ldc = ldc;
+  p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+  p.positions = positions;
+  p.head_dim = (int32_t)head_dim;
+  p.rope_cols = (int32_t)(n_rope_heads * head_dim);
+  p.theta = theta;
+  p.out_cols = (int32_t)N;
+  // whole heads per tile: largest multiple of head_dim <= 256 dividing N
+  p.BN = (int32_t)head_dim;
+  for (int bn = 256; bn >= head_dim; bn -= (int)head_dim)
+    if (N % bn == 0) { p.BN = bn; break; }
+  return launch(p, A, M, lda, K, W, 1, N, 1, stream);
 }

@@ -143,7 +143,9 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const int32_t* __rest
   }
 }
 
-// One warp per token; each lane owns 8-element column slices lane*8 + 256*c.
+// One warp per (token, 256-column chunk): lane owns columns chunk*256 + lane*8
+// .. +8.  Slot rows/weights are loaded once per warp (lane j holds slot j) and
+// broadcast with shuffles, so small-T (decode) calls still fill the GPU.
 __global__ void __launch_bounds__(kThreads) combine_kernel(const uint4* __restrict__ y, const int32_t* __restrict__ dst,
                                                            const float* __restrict__ tw, int T, int k, int hv,
                                                            const uint4* __restrict__ resid, int res_row0,
@@ -153,52 +155,53 @@ __global__ void __launch_bounds__(kThreads) combine_kernel(const uint4* __restri
   const int warp_global = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int n_warps = (gridDim.x * kThreads) >> 5;
-  for (int t = warp_global; t < T; t += n_warps) {
-    int rows[32];
-    float ws[32];
+  const int n_chunks = (hv + 31) / 32;
+  for (int item = warp_global; item < T * n_chunks; item += n_warps) {
+    const int t = item / n_chunks;
+    const int c = (item % n_chunks) * 32 + lane;
+    const int my_row = lane < k ? dst[(int64_t)t * k + lane] : -1;
+    const float my_w = lane < k ? tw[(int64_t)t * k + lane] : 0.f;
+    const bool ok = c < hv;  // all lanes stay for the shuffles below
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
     for (int j = 0; j < k; ++j) {
-      rows[j] = dst[(int64_t)t * k + j];
-      ws[j] = tw[(int64_t)t * k + j];
+      const int row = __shfl_sync(0xffffffffu, my_row, j);
+      const float wj = __shfl_sync(0xffffffffu, my_w, j);
+      if (row < 0 || !ok) continue;
+      const uint4 v = __ldg(y + (int64_t)row * hv + c);
+      const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = unpack_bf16x2(vw[i]);
+        acc[2 * i] = fmaf(wj, f.x, acc[2 * i]);
+        acc[2 * i + 1] = fmaf(wj, f.y, acc[2 * i + 1]);
+      }
     }
-    const float sg = shared_gate ? shared_gate[t] : 0.f;
-    for (int c = lane; c < hv; c += 32) {
-      float acc[8];
+    if (!ok) continue;
+    if (shared_y) {
+      const float sg = shared_gate[t];
+      const uint4 v = __ldg(shared_y + (int64_t)t * hv + c);
+      const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-      for (int j = 0; j < k; ++j) {
-        if (rows[j] < 0) continue;
-        const uint4 v = __ldg(y + (int64_t)rows[j] * hv + c);
-        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 f = unpack_bf16x2(vw[i]);
-          acc[2 * i] = fmaf(ws[j], f.x, acc[2 * i]);
-          acc[2 * i + 1] = fmaf(ws[j], f.y, acc[2 * i + 1]);
-        }
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = unpack_bf16x2(vw[i]);
+        acc[2 * i] = fmaf(sg, f.x, acc[2 * i]);
+        acc[2 * i + 1] = fmaf(sg, f.y, acc[2 * i + 1]);
       }
-      if (shared_y) {
-        const uint4 v = __ldg(shared_y + (int64_t)t * hv + c);
-        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 f = unpack_bf16x2(vw[i]);
-          acc[2 * i] = fmaf(sg, f.x, acc[2 * i]);
-          acc[2 * i + 1] = fmaf(sg, f.y, acc[2 * i + 1]);
-        }
-      }
-      if (resid && t >= res_row0 && t < res_row0 + res_rows) {
-        const uint4 v = __ldg(resid + (int64_t)(t - res_row0) * hv + c);
-        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 f = unpack_bf16x2(vw[i]);
-          acc[2 * i] += f.x;
-          acc[2 * i + 1] += f.y;
-        }
-      }
-      out[(int64_t)t * hv + c] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
-                                            pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
     }
+    if (resid && t >= res_row0 && t < res_row0 + res_rows) {
+      const uint4 v = __ldg(resid + (int64_t)(t - res_row0) * hv + c);
+      const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = unpack_bf16x2(vw[i]);
+        acc[2 * i] += f.x;
+        acc[2 * i + 1] += f.y;
+      }
+    }
+    out[(int64_t)t * hv + c] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                                          pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
   }
 }
 
@@ -261,7 +264,8 @@ extern "C" int hap_moe_combine(const void* y, const int32_t* dst_of_row, const f
     return HAP_ERR_MISALIGNED;
   if (T == 0) return HAP_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  int grid = (int)((T * 32 + kThreads - 1) / kThreads);
+  const int64_t items = T * ((h / 8 + 31) / 32);
+  int grid = (int)((items * 32 + kThreads - 1) / kThreads);
   if (grid > 148 * 16) grid = 148 * 16;
   combine_kernel<<<grid, kThreads, 0, st>>>(reinterpret_cast<const uint4*>(y), dst_of_row, topk_w, (int)T, (int)k,
                                             (int)(h / 8), reinterpret_cast<const uint4*>(residual), (int)res_row0,

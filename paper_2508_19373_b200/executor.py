@@ -52,6 +52,7 @@ class CudaOps:
 
     rmsnorm = staticmethod(K.rmsnorm)
     gemm = staticmethod(K.gemm)
+    gemm_qkv_rope = staticmethod(K.gemm_qkv_rope)
     grouped_gemm = staticmethod(K.grouped_gemm)
     rope_qk = staticmethod(K.rope_qk)
     attn_prefill = staticmethod(K.attn_prefill)
@@ -123,6 +124,15 @@ class HapMoEBlock:
         e.record()
         self.timers.setdefault(name, []).append((s, e))
 
+    def _prefill_positions(self, bpr: int, S: int, rows: int) -> torch.Tensor:
+        key = (bpr, S, rows)
+        cache = getattr(self, "_pos_cache", None)
+        if cache is None or cache[0] != key:
+            pos = torch.zeros(rows, dtype=torch.int32)
+            pos[:bpr * S] = torch.arange(S, dtype=torch.int32).repeat(bpr)
+            self._pos_cache = (key, pos.to(self.device))
+        return self._pos_cache[1]
+
     def _coll(self, name, *args):
         if self.comm is None:
             return None
@@ -164,15 +174,14 @@ class HapMoEBlock:
 
         # ---------------- attention module
         xn = ops.rmsnorm(x, w.ln1, cfg.rms_eps)
-        qkv = ops.gemm(xn, w.wqkv, bias=w.bqkv)
         nq, nkv = w.n_q_local, w.n_kv_local
         if decode:
             pos = torch.zeros(rows, device=dev, dtype=torch.int32)
             pos[:n_seq].copy_(positions)
         else:
-            pos = torch.arange(S, device=dev, dtype=torch.int32).repeat(bpr)
-            pos = torch.cat([pos, pos.new_zeros(rows - pos.numel())]) if pos.numel() < rows else pos[:rows]
-        ops.rope_qk(qkv, nq, nkv, d, pos, cfg.rope_theta)
+            pos = self._prefill_positions(bpr, S, rows)
+        # QKV projection with RoPE fused into the GEMM epilogue
+        qkv = ops.gemm_qkv_rope(xn, w.wqkv, pos, nq + nkv, d, cfg.rope_theta, bias=w.bqkv)
         attn = torch.zeros(rows, nq * d, device=dev, dtype=BF16) if rows != T_real else \
             torch.empty(rows, nq * d, device=dev, dtype=BF16)
         if decode:

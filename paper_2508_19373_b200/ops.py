@@ -105,6 +105,29 @@ def gemm(a: torch.Tensor, w: torch.Tensor, out: Optional[torch.Tensor] = None, *
     return grouped_gemm(a, w, 1, None, out, swiglu_half=swiglu_half, bias=bias, residual=residual)
 
 
+def gemm_qkv_rope(a: torch.Tensor, w: torch.Tensor, positions: torch.Tensor, n_rope_heads: int, head_dim: int,
+                  theta: float, bias: Optional[torch.Tensor] = None,
+                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """qkv = a @ w^T (+bias) with RoPE applied to the first n_rope_heads heads (fused epilogue)."""
+    lib = _lib.load()
+    _need(a, "a", BF16); _need(w, "w", BF16); _need(positions, "positions", torch.int32)
+    _rowmajor(a, "a")
+    if not w.is_contiguous():
+        raise ValueError("w must be contiguous")
+    if bias is not None:
+        _need(bias, "bias", BF16)
+    N = w.shape[0]
+    if out is None:
+        out = torch.empty(a.shape[0], N, device=a.device, dtype=BF16)
+    _need(out, "out", BF16); _rowmajor(out, "out")
+    st = lib.hap_gemm_qkv_rope(a.data_ptr(), a.shape[0], a.stride(0), a.shape[1], w.data_ptr(), N, _ptr(bias),
+                               out.data_ptr(), out.stride(0), positions.data_ptr(), n_rope_heads, head_dim,
+                               float(theta), _stream())
+    check(st, "hap_gemm_qkv_rope")
+    _count(1 if a.shape[0] else 0)
+    return out
+
+
 def router_topk(x: torch.Tensor, w: torch.Tensor, n_experts: int, top_k: int, renormalize: bool,
                 has_shared_gate: bool, topk_idx: torch.Tensor, topk_w: torch.Tensor,
                 shared_gate: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None):

@@ -46,6 +46,22 @@ class CpuOps:
         return out
 
     @staticmethod
+    def gemm_qkv_rope(a, w, pos, n_rope_heads, d, theta, bias=None, out=None):
+        qkv = CpuOps.gemm(a, w, bias=bias)
+        T = qkv.shape[0]
+        inv = 1.0 / (theta ** (torch.arange(0, d, 2, dtype=torch.float64) / d))
+        ang = pos.double()[:, None] * inv[None, :]
+        cos, sin = torch.cos(ang).float()[:, None, :], torch.sin(ang).float()[:, None, :]
+        acc = a.float() @ w.float().t()
+        if bias is not None:
+            acc = acc + bias.float()
+        x = acc[:, :n_rope_heads * d].view(T, n_rope_heads, d)
+        x1, x2 = x[..., :d // 2], x[..., d // 2:]
+        y = torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], -1)
+        qkv[:, :n_rope_heads * d] = y.reshape(T, -1).to(BF16)
+        return qkv
+
+    @staticmethod
     def grouped_gemm(a, b, n_groups, seg, out, *, swiglu_half=0, bias=None, residual=None, seg_group=None):
         b3 = b.reshape(n_groups, -1, b.shape[-1])
         segs = seg.tolist()

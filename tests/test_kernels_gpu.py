@@ -49,6 +49,26 @@ def test_dense_gemm(M, N, Kd):
     assert rel_err(np32(c), ref) < 1e-2  # bf16 output rounding
 
 
+@pytest.mark.parametrize("d,nq,nkv,bias", [(128, 32, 8, False), (64, 8, 2, False), (128, 16, 16, True),
+                                           (128, 4, 1, True)])
+def test_gemm_qkv_rope(d, nq, nkv, bias):
+    """Fused QKV GEMM + RoPE epilogue vs oracle (GEMM in fp64, bias, then rope)."""
+    T, h = 300, 512
+    N = (nq + 2 * nkv) * d
+    a, w = bf16((T, h), seed=31), bf16((N, h), 0.05, seed=32)
+    b = bf16((N,), seed=33) if bias else None
+    pos = torch.randint(0, 4096, (T,), device=dev, dtype=torch.int32)
+    out = K().gemm_qkv_rope(a, w, pos, nq + nkv, d, 1e6, bias=b)
+    torch.cuda.synchronize()
+    acc = np32(a).astype(np.float64) @ np32(w).astype(np.float64).T
+    if bias:
+        acc += np32(b)
+    p = pos.cpu().numpy()
+    qk = O.rope(acc[:, :(nq + nkv) * d].reshape(T, nq + nkv, d), p, 1e6).reshape(T, -1)
+    ref = np.concatenate([qk, acc[:, (nq + nkv) * d:]], 1)
+    assert rel_err(np32(out), ref) < 1e-2
+
+
 def test_gemm_bias_residual():
     a, b = bf16((300, 256), seed=1), bf16((768, 256), seed=2)
     bias, res = bf16((768,), seed=3), bf16((300, 768), seed=4)
