@@ -67,7 +67,8 @@ def _events_time(fn, reps: int, warmup: int = 2) -> float:
 
 
 def _rand(shape, std=1.0):
-    return (torch.randn(shape, device="cuda") * std).to(BF16)
+    t = torch.randn(shape, device="cuda", dtype=BF16)
+    return t.mul_(std) if std != 1.0 else t
 
 
 # ------------------------------------------------------------- attention --
@@ -201,9 +202,11 @@ class Measurement:
 
 
 def measure_catalog(cfg: BlockConfig, n: int, batch: int, input_len: int, output_len: int,
-                    reps: int = 5, gamma: float = 1.3, cache: Optional[dict] = None) -> List[Measurement]:
+                    reps: int = 5, gamma: float = 1.3, cache: Optional[dict] = None,
+                    stages: Optional[Tuple[str, ...]] = None) -> List[Measurement]:
     """Measured per-device module time for every (strategy, stage) cell the
-    planner prices for this scenario (build_cost_tensors, planner.py:222-250)."""
+    planner prices for this scenario (build_cost_tensors, planner.py:222-250).
+    Cells of stages not measured keep the planner's own estimate."""
     mp = import_moeplan()
     spec = cfg.to_model_spec()
     hw = b200_hardware(n)
@@ -211,7 +214,8 @@ def measure_catalog(cfg: BlockConfig, n: int, batch: int, input_len: int, output
     cache = {} if cache is None else cache
     decode_kv = max(1, input_len + output_len // 2)
     out: List[Measurement] = []
-    stages = ["prefill"] + (["decode"] if output_len > 0 else [])
+    if stages is None:
+        stages = ("prefill",) + (("decode",) if output_len > 0 else ())
     for st in stages:
         for k_, a in enumerate(cat.attention):
             b_rep = math.ceil(batch / a.dp_degree)

@@ -30,15 +30,15 @@ from paper_2508_19373_b200.plan import plan_for  # noqa: E402
 mp = import_moeplan()
 
 SCENARIOS = [
-    # (config, batch, input_len, output_len) -- BASELINE.json configs
-    ("mixtral-8x7b", 8, 2048, 0),          # prefill 8x2048
-    ("mixtral-8x7b", 64, 1024, 2048),      # decode B=64, kv = 1024 + 2048//2 = 2048
-    ("qwen1.5-moe-a2.7b", 8, 2048, 0),
-    ("qwen2-57b-a14b", 1, 1024, 2048),     # decode sweep 1..512
-    ("qwen2-57b-a14b", 8, 1024, 2048),
-    ("qwen2-57b-a14b", 64, 1024, 2048),
-    ("qwen2-57b-a14b", 512, 1024, 2048),
-    ("mixtral-8x22b", 16, 4096, 0),
+    # (config, batch, input_len, output_len, measured stages) -- BASELINE.json configs
+    ("mixtral-8x7b", 8, 2048, 0, ("prefill",)),          # prefill 8x2048
+    ("mixtral-8x7b", 64, 1024, 2048, ("decode",)),       # decode B=64, kv = 1024 + 2048//2 = 2048
+    ("qwen1.5-moe-a2.7b", 8, 2048, 0, ("prefill",)),
+    ("qwen2-57b-a14b", 1, 1024, 2048, ("decode",)),      # decode sweep 1..512
+    ("qwen2-57b-a14b", 8, 1024, 2048, ("decode",)),
+    ("qwen2-57b-a14b", 64, 1024, 2048, ("decode",)),
+    ("qwen2-57b-a14b", 512, 1024, 2048, ("decode",)),
+    ("mixtral-8x22b", 16, 4096, 0, ("prefill",)),
 ]
 
 
@@ -58,6 +58,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--out-dir", default="gpurun_out")
     args = ap.parse_args()
     scen = SCENARIOS[:3] if args.quick else SCENARIOS
     ns = (1, 2, 4, 8)
@@ -65,11 +66,11 @@ def main():
     meas_all = []
     t0 = time.time()
     per_case = []
-    for name, B, S, O in scen:
+    for name, B, S, O, stages in scen:
         cfg = get_config(name)
         for n in ns:
             try:
-                meas = calib.measure_catalog(cfg, n, B, S, O, reps=args.reps, cache=cache)
+                meas = calib.measure_catalog(cfg, n, B, S, O, reps=args.reps, cache=cache, stages=stages)
             except mp.InfeasibleError as exc:
                 per_case.append({"model": name, "n": n, "scenario": [B, S, O], "infeasible": str(exc)})
                 continue
@@ -78,9 +79,12 @@ def main():
         print(f"measured {name} B={B} S={S} O={O} ({time.time() - t0:.0f}s)", flush=True)
 
     model, tr_err, te_err, _ = calib.fit_eta(meas_all)
-    out_dir = ROOT / "profiles"
-    mp.write_samples_csv(calib.to_samples(meas_all), str(out_dir / "r01_calibration_samples.csv"))
-    mp.save_model(model, str(out_dir / "r01_eta_model.json"))
+    out_dir = ROOT / args.out_dir  # gpurun only brings back gpurun_out/; copy to profiles/ afterwards
+    out_dir.mkdir(parents=True, exist_ok=True)
+    from moeplan.costmodel import save_model, write_samples_csv
+
+    write_samples_csv(calib.to_samples(meas_all), str(out_dir / "r01_calibration_samples.csv"))
+    save_model(model, str(out_dir / "r01_eta_model.json"))
 
     cases = []
     for c in per_case:
@@ -90,8 +94,12 @@ def main():
         cfg = get_config(c["model"])
         B, S, O = c["scenario"]
         n = c["n"]
-        res_roof = plan_for(cfg, n, B, S, O)
-        res_cal = plan_for(cfg, n, B, S, O, cost_models=mp.CostModels(eta=model))
+        try:
+            res_roof = plan_for(cfg, n, B, S, O)
+            res_cal = plan_for(cfg, n, B, S, O, cost_models=mp.CostModels(eta=model))
+        except mp.InfeasibleError as exc:  # whole-model memory (Eq.5) infeasible at this N
+            cases.append({"model": c["model"], "n": n, "scenario": c["scenario"], "infeasible": str(exc)})
+            continue
         tens = calib.measured_cost_tensors(res_roof, c["meas"])
         scen_o = mp.InferenceScenario(B, S, O)
         spec = cfg.to_model_spec()
