@@ -310,7 +310,7 @@ def main():
     from paper_2508_19373_b200 import ops as K
     from paper_2508_19373_b200.config import get_config
     from paper_2508_19373_b200.executor import HapMoEBlock
-    from paper_2508_19373_b200.plan import baseline_plan, plan_for, stage_plan
+    from paper_2508_19373_b200.plan import baseline_plan, calibrated_plan, plan_for, stage_plan
     from paper_2508_19373_b200.weights import synthetic_weights
 
     rank, world, local = dist_setup(args.gpus)
@@ -318,11 +318,17 @@ def main():
     peaks = load_peaks()
 
     t_plan = time.perf_counter()
-    res_p = plan_for(cfg, world, PREFILL_BATCH, PREFILL_SEQ, 0)
+    res_roof = plan_for(cfg, world, PREFILL_BATCH, PREFILL_SEQ, 0)
     plan_ms = (time.perf_counter() - t_plan) * 1e3
-    res_d = plan_for(cfg, world, DECODE_BATCH, DECODE_KV // 2, DECODE_KV)  # decode kv = in + out//2 = 2048
+    # HAP plan = the reference ILP on B200-measured module tables (profiles/r01_calibration.json,
+    # scripts/calibrate.py); falls back to the roofline plan when the scenario is not calibrated.
+    res_p, plan_src = calibrated_plan(cfg, world, PREFILL_BATCH, PREFILL_SEQ, 0)
+    res_d, _ = calibrated_plan(cfg, world, DECODE_BATCH, DECODE_KV // 2, DECODE_KV)  # kv = in + out//2
     hap_p, hap_d = stage_plan(res_p, "prefill"), stage_plan(res_d, "decode")
     plans = {"hap": (hap_p, hap_d)}
+    roof_p = stage_plan(res_roof, "prefill")
+    if world > 1 and roof_p.degrees != hap_p.degrees and not args.no_tp:
+        plans["hap_roofline"] = (roof_p, hap_d)
     if world > 1 and not args.no_tp:
         try:
             plans["tp"] = (baseline_plan(res_p, "tp", "prefill"), baseline_plan(res_d, "tp", "decode"))
@@ -446,7 +452,8 @@ def main():
             "config": {"workload": f"{cfg.name} MoE decoder block (attention + experts), bf16 prefill "
                                    f"{PREFILL_BATCH}x{PREFILL_SEQ}",
                        "model": cfg.name, "global_batch": PREFILL_BATCH, "seq_len": PREFILL_SEQ,
-                       "parallelism": hap["plan"], "planner": "moeplan.plan (reference ILP), B200 roofline profile",
+                       "parallelism": hap["plan"],
+                       "planner": f"moeplan solve_ilp (reference ILP) on {plan_src}",
                        "planner_ms": plan_ms,
                        "l2": "no flush: every step streams > L2 (2.8 GB expert weights + 128 MB activations)"},
             "plans": results, "decode": decode, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -10,6 +10,7 @@ objects unchanged, so any Plan from solve_ilp / solve_bruteforce drops into
 from __future__ import annotations
 
 from dataclasses import dataclass
+from pathlib import Path
 from typing import Optional
 
 from .config import BlockConfig, b200_hardware, import_moeplan
@@ -50,6 +51,44 @@ def baseline_plan(result, name: str = "tp", stage: str = "prefill") -> StagePlan
     k, i, j = mp.baseline_indices(result.catalog, name)
     cat = result.catalog
     return StagePlan(cat.attention[k], cat.expert[i if stage == "prefill" else j])
+
+
+CALIBRATION_FILE = Path(__file__).resolve().parent.parent / "profiles" / "r01_calibration.json"
+
+
+def calibrated_plan(cfg: BlockConfig, n_devices: int, batch: int, input_len: int, output_len: int = 0,
+                    path: Optional[Path] = None):
+    """The reference ILP re-solved on B200-measured module tables
+    (calib.measured_cost_tensors): returns (PlanResult-like, source) where
+    source says whether measured tables were found for this exact scenario."""
+    import json
+
+    from . import calib
+
+    mp = import_moeplan()
+    res = plan_for(cfg, n_devices, batch, input_len, output_len)
+    p = Path(path) if path else CALIBRATION_FILE
+    if not p.exists():
+        return res, "roofline (no calibration file)"
+    doc = json.loads(p.read_text())
+    case = next((c for c in doc.get("cases", []) if c.get("model") == cfg.name and c.get("n") == n_devices
+                 and c.get("scenario") == {"batch": batch, "input_len": input_len, "output_len": output_len}
+                 and "cells" in c), None)
+    if case is None:
+        return res, "roofline (scenario not calibrated)"
+    att = {a.label(): k for k, a in enumerate(res.catalog.attention)}
+    exp = {e.label(): i for i, e in enumerate(res.catalog.expert)}
+    meas = []
+    for cell in case["cells"]:
+        idx = att.get(cell["strategy"]) if cell["module"] == "attention" else exp.get(cell["strategy"])
+        if idx is None:
+            continue
+        meas.append(calib.Measurement(cfg.name, n_devices, cell["module"], cell["stage"], cell["strategy"], idx,
+                                      0, 0, 0, 0, cell["measured_us"] * 1e-6, cell["roofline_us"] * 1e-6))
+    tens = calib.measured_cost_tensors(res, meas)
+    scen = mp.InferenceScenario(batch=batch, input_len=input_len, output_len=output_len)
+    sel = mp.solve_ilp(tens, scen, cfg.to_model_spec(), res.catalog)
+    return mp.PlanResult(plan=sel, tensors=tens, catalog=res.catalog), f"measured B200 tables ({p.name})"
 
 
 def find_plan(result, attn_tp: int, exp_tp: int, exp_ep: int, exp_dp: int = 1) -> Optional[StagePlan]:
