@@ -204,8 +204,14 @@ def make_decode_state(block, cfg):
 
 
 def bench_decode(block, cfg, steps, warmup):
+    """Decode step timing; single-device non-EP plans replay a CUDA graph of the
+    block (the step is launch-bound at B=64), others run eagerly."""
     x, cache, pos = make_decode_state(block, cfg)
-    return time_loop(lambda: block.forward(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos), steps, warmup)
+    if block.lay.n == 1 and block.deg.e_ep == 1:
+        g, _ = block.capture_graph(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos)
+        return time_loop(g.replay, steps, warmup), "cuda_graph"
+    return time_loop(lambda: block.forward(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos), steps,
+                     warmup), "eager"
 
 
 def decode_bytes(cfg, block_routing_idx) -> float:
@@ -359,8 +365,8 @@ def main():
              "prefill_tokens_per_s": PREFILL_BATCH * PREFILL_SEQ / (ms_p / 1e3)}
         if not args.no_decode:
             bd = get_block(sp_d)
-            ms_d = bench_decode(bd, cfg, args.steps, args.warmup)
-            r.update({"decode_plan": sp_d.label(), "decode_ms": ms_d,
+            ms_d, mode = bench_decode(bd, cfg, args.steps, args.warmup)
+            r.update({"decode_plan": sp_d.label(), "decode_ms": ms_d, "decode_mode": mode,
                       "decode_tokens_per_s": DECODE_BATCH / (ms_d / 1e3)})
         results[name] = r
     total_launches = K.LAUNCHES[0] - launches0

@@ -54,10 +54,11 @@ struct Params {
   int32_t head_dim;
   int32_t rope_cols;
   float theta;
+  int32_t group_m;  // raster group (m-blocks)
 };
 
 constexpr int kEpiRope = 2;     // internal epilogue id (hap_gemm_qkv_rope)
-constexpr int kGroupM = 16;     // m-blocks per raster group (L2 reuse of A rows across n-blocks)
+constexpr int64_t kRasterL2Bytes = 48ll << 20;  // A rows of one raster group kept L2-resident across n-blocks
 
 struct TileCoord {
   int32_t g, m0, m_end, n_blk;
@@ -66,7 +67,7 @@ struct TileCoord {
 // Map a linear tile index to (segment's weight group, row range, n block).
 // tile_start has n_segs+1 prefix entries; m-blocks vary fastest.
 __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, const int32_t* seg,
-                                              const int32_t* seg_group, int n_segs, int n_blocks) {
+                                              const int32_t* seg_group, int n_segs, int n_blocks, int group_m) {
   int lo = 0, hi = n_segs - 1;
   while (lo < hi) {  // last g with tile_start[g] <= t
     int mid = (lo + hi + 1) >> 1;
@@ -76,11 +77,13 @@ __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, 
   const int local = t - tile_start[g];
   const int rows = seg[g + 1] - seg[g];
   const int m_blocks = (rows + BM - 1) / BM;
-  // grouped raster: kGroupM m-blocks x all n-blocks, m fastest inside a group
-  const int grp = local / (kGroupM * n_blocks);
-  const int g0 = grp * kGroupM;
-  const int gsz = min(kGroupM, m_blocks - g0);
-  const int r = local - grp * kGroupM * n_blocks;
+  // grouped raster: group_m m-blocks x all n-blocks, m fastest inside a group.
+  // group_m is sized so a group's A rows fit the L2 budget: the weight tile of
+  // an n-block is then read once per group while the group's A rows stay hot.
+  const int grp = local / (group_m * n_blocks);
+  const int g0 = grp * group_m;
+  const int gsz = min(group_m, m_blocks - g0);
+  const int r = local - grp * group_m * n_blocks;
   TileCoord c;
   c.g = seg_group[g];
   c.m0 = seg[g] + (g0 + r % gsz) * BM;
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileCoord c = map_tile(t, tile_start_s, seg_s, group_s, n_segs, n_blocks);
+        const TileCoord c = map_tile(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
         const int b_row = c.g * p.N + c.n_blk * p.BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quadrant accessible by this warp
     int it = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
-      const TileCoord c = map_tile(t, tile_start_s, seg_s, group_s, n_segs, n_blocks);
+      const TileCoord c = map_tile(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -370,6 +373,8 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
   }
   // Upper bound on tiles without reading seg on the host.
   const int64_t n_blocks = (N + p.BN - 1) / p.BN;
+  int64_t gm = kRasterL2Bytes / (K * 2 * BM);
+  p.group_m = (int32_t)(gm < 1 ? 1 : (gm > 1024 ? 1024 : gm));
   const int64_t max_tiles = ((a_rows + BM - 1) / BM + (n_segs - 1)) * n_blocks;
   const int grid = (int)(max_tiles < kNumSMs ? max_tiles : kNumSMs);
   grouped_gemm_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tmA, tmB, p);

@@ -24,6 +24,125 @@ namespace router {
 constexpr int kRanges = 8;              // == warps per CTA; fixed by the parity contract
 constexpr int kThreads = kRanges * 32;
 constexpr int kPrefetch = 4;
+constexpr int kSmallT = 1024;         // <= this many tokens: one CTA per token
+
+// Softmax over the E routed logits, top-k on logits (strict '>' keeps the lower
+// index on ties), optional renormalisation, shared-expert sigmoid gate.
+template <int NE>
+__device__ __forceinline__ void finish_token(const float (&acc)[NE], int t, int E, int top_k, int renorm,
+                                             int has_shared, int32_t* __restrict__ topk_idx,
+                                             float* __restrict__ topk_w, float* __restrict__ shared_gate,
+                                             float* __restrict__ logits_out) {
+  if (logits_out) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e)
+      if (e < E) logits_out[(int64_t)t * E + e] = acc[e];
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < NE; ++e)
+    if (e < E) mx = fmaxf(mx, acc[e]);
+  float denom = 0.f;
+#pragma unroll
+  for (int e = 0; e < NE; ++e)
+    if (e < E) denom += expf(acc[e] - mx);
+
+  // top-k on logits; strict '>' keeps the lowest index on ties
+  uint32_t taken[(NE + 31) / 32];
+#pragma unroll
+  for (int i = 0; i < (NE + 31) / 32; ++i) taken[i] = 0;
+  float wsum = 0.f;
+  for (int s = 0; s < top_k; ++s) {
+    float best = -INFINITY;
+    int bi = -1;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const bool free_e = e < E && !((taken[e >> 5] >> (e & 31)) & 1u);
+      if (free_e && (bi < 0 || acc[e] > best)) {
+        best = acc[e];
+        bi = e;
+      }
+    }
+    taken[bi >> 5] |= 1u << (bi & 31);
+    const float p = expf(best - mx) / denom;
+    topk_idx[(int64_t)t * top_k + s] = bi;
+    topk_w[(int64_t)t * top_k + s] = p;
+    wsum += p;
+  }
+  if (renorm) {
+    const float inv = 1.f / wsum;
+    for (int s = 0; s < top_k; ++s) topk_w[(int64_t)t * top_k + s] *= inv;
+  }
+  if (has_shared && shared_gate) {
+    float g = 0.f;
+#pragma unroll
+    for (int e = 0; e < NE; ++e)
+      if (e == E) g = acc[e];
+    shared_gate[t] = 1.f / (1.f + expf(-g));
+  }
+}
+
+// Small-T variant (decode): one CTA per token; thread (p, e) runs exactly the
+// sequential fma chain the large kernel's lane runs for (token, expert e,
+// range p), so the logits are bit-identical between the two variants.
+template <int NE>
+__global__ void __launch_bounds__(kRanges * NE) router_small_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                    const __nv_bfloat16* __restrict__ w, int T,
+                                                                    int h, int n_rows_w, int E, int top_k,
+                                                                    int renorm, int has_shared,
+                                                                    int32_t* __restrict__ topk_idx,
+                                                                    float* __restrict__ topk_w,
+                                                                    float* __restrict__ shared_gate,
+                                                                    float* __restrict__ logits_out) {
+  extern __shared__ uint4 xs[];  // token row, h/8 vectors
+  __shared__ float part[kRanges][NE];
+  const int t = blockIdx.x;
+  const uint4* xrow = reinterpret_cast<const uint4*>(x + (int64_t)t * h);
+  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) xs[i] = __ldg(xrow + i);
+  __syncthreads();
+  const int p = threadIdx.x / NE, e = threadIdx.x % NE;
+  const int hr = h / kRanges;
+  float acc = 0.f;
+  if (e < n_rows_w) {
+    const uint4* wr = reinterpret_cast<const uint4*>(w + (int64_t)e * h + p * hr);
+    const uint4* xr = xs + p * (hr / 8);
+    const int nv = hr / 8;
+    uint4 wb[kPrefetch];
+#pragma unroll
+    for (int i = 0; i < kPrefetch; ++i) wb[i] = i < nv ? __ldg(wr + i) : make_uint4(0, 0, 0, 0);
+    for (int v0 = 0; v0 < nv; v0 += kPrefetch) {
+#pragma unroll
+      for (int i = 0; i < kPrefetch; ++i) {
+        const int v = v0 + i;
+        if (v >= nv) break;
+        const uint4 wv = wb[i];
+        if (v + kPrefetch < nv) wb[i] = __ldg(wr + v + kPrefetch);
+        const uint4 xv = xr[v];
+        const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+        const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 fx = unpack_bf16x2(xw[q]);
+          const float2 fw = unpack_bf16x2(ww[q]);
+          acc = __fmaf_rn(fx.x, fw.x, acc);
+          acc = __fmaf_rn(fx.y, fw.y, acc);
+        }
+      }
+    }
+  }
+  part[p][e] = acc;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  float tot[NE];
+#pragma unroll
+  for (int ee = 0; ee < NE; ++ee) {
+    float s2 = part[0][ee];
+#pragma unroll
+    for (int pp = 1; pp < kRanges; ++pp) s2 = __fadd_rn(s2, part[pp][ee]);
+    tot[ee] = s2;
+  }
+  finish_token<NE>(tot, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
+}
 
 template <int NE>
 __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* __restrict__ x,
@@ -94,53 +213,7 @@ __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* _
     acc[e] = s;
   }
 
-  if (logits_out) {
-#pragma unroll
-    for (int e = 0; e < NE; ++e)
-      if (e < E) logits_out[(int64_t)t * E + e] = acc[e];
-  }
-  float mx = -INFINITY;
-#pragma unroll
-  for (int e = 0; e < NE; ++e)
-    if (e < E) mx = fmaxf(mx, acc[e]);
-  float denom = 0.f;
-#pragma unroll
-  for (int e = 0; e < NE; ++e)
-    if (e < E) denom += expf(acc[e] - mx);
-
-  // top-k on logits; strict '>' keeps the lowest index on ties
-  uint32_t taken[(NE + 31) / 32];
-#pragma unroll
-  for (int i = 0; i < (NE + 31) / 32; ++i) taken[i] = 0;
-  float wsum = 0.f;
-  for (int s = 0; s < top_k; ++s) {
-    float best = -INFINITY;
-    int bi = -1;
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const bool free_e = e < E && !((taken[e >> 5] >> (e & 31)) & 1u);
-      if (free_e && (bi < 0 || acc[e] > best)) {
-        best = acc[e];
-        bi = e;
-      }
-    }
-    taken[bi >> 5] |= 1u << (bi & 31);
-    const float p = expf(best - mx) / denom;
-    topk_idx[(int64_t)t * top_k + s] = bi;
-    topk_w[(int64_t)t * top_k + s] = p;
-    wsum += p;
-  }
-  if (renorm) {
-    const float inv = 1.f / wsum;
-    for (int s = 0; s < top_k; ++s) topk_w[(int64_t)t * top_k + s] *= inv;
-  }
-  if (has_shared && shared_gate) {
-    float g = 0.f;
-#pragma unroll
-    for (int e = 0; e < NE; ++e)
-      if (e == E) g = acc[e];
-    shared_gate[t] = 1.f / (1.f + expf(-g));
-  }
+  finish_token<NE>(acc, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
 }
 
 template <int NE>
@@ -151,6 +224,20 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
   if (!configured) {
     if (configure_smem((const void*)router_kernel<NE>, smem)) return HAP_ERR_LAUNCH;
     configured = 1;
+  }
+  if (T <= kSmallT) {
+    const int xs_bytes = (int)(h / 8) * 16;
+    static int configured_small = 0;
+    if (!configured_small) {
+      if (configure_smem((const void*)router_small_kernel<NE>, 64 * 1024)) return HAP_ERR_LAUNCH;
+      configured_small = 1;
+    }
+    if (xs_bytes > 64 * 1024) return HAP_ERR_UNSUPPORTED;
+    router_small_kernel<NE><<<(int)T, kRanges * NE, xs_bytes, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h,
+        (int)(E + has_shared), (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits);
+    HAP_CHECK_LAUNCH();
+    return HAP_OK;
   }
   const int grid = (int)((T + 31) / 32);
   router_kernel<NE><<<grid, kThreads, smem, st>>>(

@@ -158,6 +158,25 @@ class HapMoEBlock:
             return self._forward(x_local, batch, 1, decode=True, kv_cache=kv_cache, positions=positions)
         raise ValueError(f"unknown stage {stage!r}")
 
+    def capture_graph(self, x_static: torch.Tensor, stage: str, batch: int, seq_len: int = 1,
+                kv_cache: Optional[KVCache] = None, positions: Optional[torch.Tensor] = None):
+        """Capture one forward into a CUDA graph over static buffers; returns
+        (graph, out_static).  Replaying the graph re-runs every kernel of the
+        block with no host work (decode is launch-bound otherwise).  Only for
+        plans without host synchronisation (no EP count exchange) on one GPU."""
+        if self.deg.e_ep > 1 or self.lay.n > 1:
+            raise RuntimeError("graph capture is supported for single-device, non-EP plans")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):  # warm-up: kernel attributes, allocator pools
+                self.forward(x_static, stage, batch, seq_len, kv_cache=kv_cache, positions=positions)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = self.forward(x_static, stage, batch, seq_len, kv_cache=kv_cache, positions=positions)
+        return g, out
+
     def _forward(self, x_local, batch, S, decode, kv_cache=None, positions=None):
         cfg, w, lay, ops = self.cfg, self.w, self.lay, self.ops
         dev = self.device

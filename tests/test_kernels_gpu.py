@@ -126,7 +126,11 @@ def test_grouped_gemm_segment_groups():
 
 # ---------------------------------------------------------------- router --
 @pytest.mark.parametrize("T,h,E,k,renorm,shared", [(1000, 512, 8, 2, True, False), (517, 2048, 60, 4, False, True),
-                                                   (300, 3584, 64, 8, False, True), (64, 4096, 8, 2, True, False)])
+                                                   (300, 3584, 64, 8, False, True), (64, 4096, 8, 2, True, False),
+                                                   (1, 3584, 64, 8, False, True),       # small-T kernel
+                                                   (3000, 4096, 8, 2, True, False),     # large-T kernel
+                                                   (2100, 3584, 64, 8, False, True),
+                                                   (1500, 2048, 60, 4, False, True)])
 def test_router_bit_exact(T, h, E, k, renorm, shared):
     x = bf16((T, h), seed=10)
     w = bf16((E + int(shared), h), 0.02, seed=11)
