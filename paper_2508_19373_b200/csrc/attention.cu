@@ -13,9 +13,15 @@
 //
 // Models: score+value term 4*n*kv_len*h of attention_flops (reference
 // arch.py:161); decode kv_len = input_len + output_len//2 (planner.py:226).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hap {
+int attn_prefill_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* out,
+                    int64_t ldo, int64_t n_seqs, int64_t S, int64_t n_q, int64_t n_kv, int64_t head_dim, float scale,
+                    int32_t causal, cudaStream_t st);
+
 namespace attn {
 
 constexpr int BM = 64;
@@ -467,6 +473,12 @@ extern "C" int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64
     return HAP_ERR_MISALIGNED;
   if (n_seqs == 0 || seq_len == 0) return HAP_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  static const bool legacy = getenv("HAP_ATTN_LEGACY_MMA") != nullptr;  // A/B switch for profiling only
+  if (!legacy) {
+    if ((ldq | ldk | ldv) % 8) return HAP_ERR_MISALIGNED;
+    return hap::attn_prefill_tc(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, seq_len, n_q_heads, n_kv_heads, head_dim,
+                                scale, causal, st);
+  }
   if (head_dim == 128)
     return launch_prefill<128>(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, seq_len, n_q_heads, n_kv_heads, scale, causal, st);
   return launch_prefill<64>(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, seq_len, n_q_heads, n_kv_heads, scale, causal, st);

@@ -79,13 +79,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
+  // try_wait with a suspend-time hint: the thread sleeps in hardware until the
+  // phase completes instead of spinning and stealing issue slots.
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "HAP_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra HAP_WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)
       : "memory");
+}
+
+// 2^x on the SFU (ftz; inputs here are <= 0 or small positive).
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // -------------------------------------------------------------------- TMA --
