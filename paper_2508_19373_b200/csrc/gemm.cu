@@ -17,21 +17,29 @@
 //
 // Models: expert_flops (reference arch.py:165-178) gated-MLP term and the
 // projection term of attention_flops (arch.py:157-160).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hap {
 namespace gemm {
 
-constexpr int BM = 128;
+constexpr int BM = 128;  // rows per CTA (a CTA pair covers 2*BM rows)
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kMaxBN = 256;
-constexpr int kStages = 4;
 constexpr int kMaxSegs = 512;
 constexpr int kAccCols = 256;  // TMEM columns per accumulator buffer
 constexpr int kThreads = 256;
-constexpr int kABytes = BM * BK * 2;       // 16 KB
-constexpr int kBBytes = kMaxBN * BK * 2;   // 32 KB
-constexpr int kSmemBytes = kStages * (kABytes + kBBytes) + 1024;
+constexpr int kABytes = BM * BK * 2;  // 16 KB
+
+// Per-CTA pipeline geometry: with a CTA pair each CTA stages only half of the
+// B tile, so the same smem holds more stages.
+template <int kPair>
+struct Geo {
+  static constexpr int kBBytes = (kMaxBN / kPair) * BK * 2;  // 32 KB (1 CTA) / 16 KB (pair)
+  static constexpr int kStages = kPair == 1 ? 4 : 6;
+  static constexpr int kSmemBytes = kStages * (kABytes + kBBytes) + 1024;
+};
 
 struct Params {
   int32_t a_rows;
@@ -66,6 +74,7 @@ struct TileCoord {
 
 // Map a linear tile index to (segment's weight group, row range, n block).
 // tile_start has n_segs+1 prefix entries; m-blocks vary fastest.
+template <int TM>
 __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, const int32_t* seg,
                                               const int32_t* seg_group, int n_segs, int n_blocks, int group_m) {
   int lo = 0, hi = n_segs - 1;
@@ -76,7 +85,7 @@ __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, 
   const int g = lo;
   const int local = t - tile_start[g];
   const int rows = seg[g + 1] - seg[g];
-  const int m_blocks = (rows + BM - 1) / BM;
+  const int m_blocks = (rows + TM - 1) / TM;
   // grouped raster: group_m m-blocks x all n-blocks, m fastest inside a group.
   // group_m is sized so a group's A rows fit the L2 budget: the weight tile of
   // an n-block is then read once per group while the group's A rows stay hot.
@@ -86,7 +95,7 @@ __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, 
   const int r = local - grp * group_m * n_blocks;
   TileCoord c;
   c.g = seg_group[g];
-  c.m0 = seg[g] + (g0 + r % gsz) * BM;
+  c.m0 = seg[g] + (g0 + r % gsz) * TM;
   c.m_end = seg[g + 1];
   c.n_blk = r / gsz;
   return c;
@@ -94,12 +103,25 @@ __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, 
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
+// kPair == 1: one CTA computes a 128 x BN tile (tcgen05 cta_group::1).
+// kPair == 2: a 2-CTA cluster computes a 256 x BN tile with cta_group::2 —
+// each CTA stages its 128 A rows and HALF of the B tile (BN/2 rows), the
+// leader CTA issues the M=256 MMAs and multicasts the commits, each CTA's
+// epilogue drains its own 128 TMEM lanes.  Halving B per SM halves the
+// L2->SM operand traffic per FLOP for B.
+template <int kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+  constexpr int kStages = Geo<kPair>::kStages;
+  constexpr int kBBytes = Geo<kPair>::kBBytes;
+  constexpr int TM = BM * kPair;  // rows per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + kStages * kABytes;
+  const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0;
+  const bool leader = crank == 0;
+  const int tile0 = blockIdx.x / kPair, tile_step = gridDim.x / kPair;
 
   __shared__ __align__(8) uint64_t full_bar[kStages];
   __shared__ __align__(8) uint64_t empty_bar[kStages];
@@ -137,23 +159,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 128);
+      mbar_init(&tempty_bar[s], 4 * kPair);  // one arrive per epilogue warp of each CTA
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(&tmem_base_s, 2 * kAccCols);
+  if (warp == 2) {
+    if (kPair == 2) tmem_alloc_pair(&tmem_base_s, 2 * kAccCols);
+    else tmem_alloc(&tmem_base_s, 2 * kAccCols);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int g = 0; g < n_segs; ++g) {
       tile_start_s[g] = acc;
       const int rows = seg_s[g + 1] - seg_s[g];
-      acc += ((rows + BM - 1) / BM) * n_blocks;
+      acc += ((rows + TM - 1) / TM) * n_blocks;
     }
     tile_start_s[n_segs] = acc;
   }
   tc_fence_before();
   __syncthreads();
+  if (kPair == 2) cluster_sync();  // peer barriers initialised, TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
   const int total_tiles = tile_start_s[n_segs];
@@ -162,29 +188,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ================= TMA producer =================
     if (lane == 0) {
-      const uint32_t tx_bytes = kABytes + p.BN * BK * 2;
+      const int bn_half = p.BN / kPair;
+      // the leader's full barrier receives both CTAs' bytes
+      const uint32_t tx_bytes = kPair * (kABytes + bn_half * BK * 2);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileCoord c = map_tile(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
-        const int b_row = c.g * p.N + c.n_blk * p.BN;
+      for (int t = tile0; t < total_tiles; t += tile_step) {
+        const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
+        const int b_row = c.g * p.N + c.n_blk * p.BN + (int)crank * bn_half;
+        const int a_row = c.m0 + (int)crank * BM;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
-          tma_load_2d(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, c.m0, kEvictNormal);
-          tma_load_2d(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
+          if (kPair == 1) {
+            mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
+            tma_load_2d(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, kEvictNormal);
+            tma_load_2d(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
+          } else {
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
+            tma_load_2d_pair(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, kEvictNormal);
+            tma_load_2d_pair(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(BM, p.BN);
+    if (lane == 0 && leader) {
+      const uint32_t idesc = make_idesc_bf16(TM, p.BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+      for (int t = tile0; t < total_tiles; t += tile_step, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -198,25 +233,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // +32 bytes per K=16 step inside the 128B swizzle atom (>>4 => +2)
-            umma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            if (kPair == 1) umma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            else umma_bf16_ss_pair(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty_bar[stage]);
+          if (kPair == 1) umma_commit(&empty_bar[stage]);
+          else umma_commit_pair_mc(&empty_bar[stage], 0x3);  // frees the stage in both CTAs
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull_bar[acc]);
+        if (kPair == 1) umma_commit(&tfull_bar[acc]);
+        else umma_commit_pair_mc(&tfull_bar[acc], 0x3);
       }
     }
   } else if (warp >= 4) {
     // ================= epilogue =================
     const int q = warp & 3;  // TMEM lane quadrant accessible by this warp
     int it = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
-      const TileCoord c = map_tile(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
+    for (int t = tile0; t < total_tiles; t += tile_step, ++it) {
+      const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row = c.m0 + q * 32 + lane;
+      const int row = c.m0 + (int)crank * BM + q * 32 + lane;
       const bool row_ok = row < c.m_end;
       const uint32_t t_row = tmem_base + acc * kAccCols + ((uint32_t)(q * 32) << 16);
       __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
@@ -338,15 +376,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      __syncwarp();
+      if (lane == 0) {  // accumulator drained by this warp -> the leader's MMA may reuse it
+        if (kPair == 1) mbar_arrive(&tempty_bar[acc]);
+        else mbar_arrive_cluster(&tempty_bar[acc], 0);
+      }
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (kPair == 2) cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * kAccCols);
+    if (kPair == 2) tmem_dealloc_pair(tmem_base, 2 * kAccCols);
+    else tmem_dealloc(tmem_base, 2 * kAccCols);
   }
 }
 
@@ -359,27 +403,62 @@ static int pick_bn(int64_t N) {
   return N < 256 ? (int)((N + 15) / 16 * 16) : 256;
 }
 
-static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
-                  int64_t n_groups, int64_t N, int64_t n_segs, void* stream) {
+template <int kPair>
+static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                       int64_t n_groups, int64_t N, int64_t n_segs, void* stream) {
+  constexpr int TM = BM * kPair;
   CUtensorMap tmA, tmB;
   if (!encode_tmap_2d_bf16(&tmA, A, (uint64_t)K, (uint64_t)a_rows, (uint64_t)lda * 2, BK, BM, true))
     return HAP_ERR_DRIVER;
-  if (!encode_tmap_2d_bf16(&tmB, B, (uint64_t)K, (uint64_t)(n_groups * N), (uint64_t)K * 2, BK, p.BN, true))
+  if (!encode_tmap_2d_bf16(&tmB, B, (uint64_t)K, (uint64_t)(n_groups * N), (uint64_t)K * 2, BK, p.BN / kPair,
+                           true))
     return HAP_ERR_DRIVER;
   static int configured = 0;
   if (!configured) {
-    if (configure_smem((const void*)grouped_gemm_kernel, kSmemBytes) != 0) return HAP_ERR_LAUNCH;
+    if (configure_smem((const void*)grouped_gemm_kernel<kPair>, Geo<kPair>::kSmemBytes) != 0) return HAP_ERR_LAUNCH;
     configured = 1;
   }
   // Upper bound on tiles without reading seg on the host.
   const int64_t n_blocks = (N + p.BN - 1) / p.BN;
-  int64_t gm = kRasterL2Bytes / (K * 2 * BM);
+  int64_t gm = kRasterL2Bytes / (K * 2 * TM);
   p.group_m = (int32_t)(gm < 1 ? 1 : (gm > 1024 ? 1024 : gm));
-  const int64_t max_tiles = ((a_rows + BM - 1) / BM + (n_segs - 1)) * n_blocks;
-  const int grid = (int)(max_tiles < kNumSMs ? max_tiles : kNumSMs);
-  grouped_gemm_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tmA, tmB, p);
+  const int64_t max_tiles = ((a_rows + TM - 1) / TM + (n_segs - 1)) * n_blocks;
+  const int64_t max_units = kNumSMs / kPair;
+  const int grid = (int)((max_tiles < max_units ? max_tiles : max_units) * kPair);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Geo<kPair>::kSmemBytes;
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<kPair>, tmA, tmB, p) != cudaSuccess) return HAP_ERR_LAUNCH;
   HAP_CHECK_LAUNCH();
   return HAP_OK;
+}
+
+static int pair_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("HAP_GEMM_CTA_PAIR");  // A/B switch for profiling; default on
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode;
+}
+
+static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                  int64_t n_groups, int64_t N, int64_t n_segs, void* stream) {
+  // CTA pairs need B split in two whole 8-row swizzle groups, and only pay off
+  // when segments fill 256-row tiles (prefill); weight-streaming decode shapes
+  // (a few rows per expert) keep 128-row single-CTA tiles.
+  if (pair_mode() && (p.BN / 2) % 8 == 0 && a_rows >= 256 * n_segs)
+    return launch_impl<2>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
+  return launch_impl<1>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
 }
 
 }  // namespace gemm

@@ -1,116 +1,51 @@
-"""Quick GPU check of the tcgen05 grouped GEMM against torch (dev script)."""
-import ctypes
-import sys
-import time
+"""Time the tcgen05 grouped GEMM on the Mixtral expert shapes (dev script).
 
+HAP_GEMM_CTA_PAIR=0 selects the 1-CTA variant for A/B comparison."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
 
-sys.path.insert(0, ".")
-from paper_2508_19373_b200._build import LIB_PATH
-
-lib = ctypes.CDLL(str(LIB_PATH))
-f = lib.hap_grouped_gemm_bf16
-V, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
-f.argtypes = [V, I64, I64, I64, V, I64, I64, V, V, I64, I32, I64, V, V, I64, V]
-f.restype = ctypes.c_int
+from paper_2508_19373_b200 import ops
 
 
-def run(A, B, n_groups, N, seg, C, epi=0, hw=0, bias=None, resid=None):
-    st = torch.cuda.current_stream().cuda_stream
-    r = f(A.data_ptr(), A.shape[0], A.stride(0), A.shape[1], B.data_ptr(), n_groups, N,
-          seg.data_ptr() if seg is not None else None, C.data_ptr(), C.stride(0), epi, hw,
-          bias.data_ptr() if bias is not None else None, resid.data_ptr() if resid is not None else None,
-          resid.stride(0) if resid is not None else 0, st)
-    assert r == 0, r
-
-
-def ref_grouped(A, B, seg, N, epi, hw):
-    out = []
-    for g in range(len(seg) - 1):
-        a = A[seg[g]:seg[g + 1]].float()
-        b = B[g * N:(g + 1) * N].float()
-        y = a @ b.t()
-        if epi == 1:
-            nb = N // (2 * hw)
-            y = y.view(-1, nb, 2, hw)
-            y = torch.nn.functional.silu(y[:, :, 0]) * y[:, :, 1]
-            y = y.reshape(-1, N // 2)
-        out.append(y)
-    return torch.cat(out)
-
-
-def check(name, got, ref):
-    err = (got.float() - ref).abs().max().item()
-    rel = err / ref.abs().max().item()
-    print(f"{name}: max abs err {err:.4g} rel {rel:.3g}", flush=True)
-    return rel
-
-
-torch.manual_seed(0)
-dev = "cuda"
-ok = True
-# 1) dense single group
-for (M, N, K) in [(128, 256, 64), (256, 512, 128), (1000, 768, 4096), (77, 4096, 512)]:
-    A = torch.randn(M, K, device=dev).bfloat16()
-    B = torch.randn(N, K, device=dev).bfloat16()
-    C = torch.zeros(M, N, device=dev, dtype=torch.bfloat16)
-    run(A, B, 1, N, None, C)
+def timed(fn, reps=10):
+    for _ in range(3):
+        fn()
     torch.cuda.synchronize()
-    ok &= check(f"dense M={M} N={N} K={K}", C, A.float() @ B.float().t()) < 1e-2
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
 
-# 2) grouped with ragged segments + swiglu
-E, N, K = 8, 512, 1024
-counts = torch.tensor([0, 130, 1, 257, 64, 0, 300, 128])
-seg = torch.zeros(E + 1, dtype=torch.int32)
-seg[1:] = torch.cumsum(counts, 0)
-R = int(seg[-1])
-A = torch.randn(R, K, device=dev).bfloat16()
-B = (torch.randn(E * N, K, device=dev) * 0.05).bfloat16()
-segd = seg.to(dev)
-C = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
-run(A, B, E, N, segd, C)
-torch.cuda.synchronize()
-ok &= check("grouped store", C, ref_grouped(A, B, seg.tolist(), N, 0, 0)) < 1e-2
-C2 = torch.zeros(R, N // 2, device=dev, dtype=torch.bfloat16)
-run(A, B, E, N, segd, C2, epi=1, hw=128)
-torch.cuda.synchronize()
-ok &= check("grouped swiglu", C2, ref_grouped(A, B, seg.tolist(), N, 1, 128)) < 2e-2
 
-# 3) bias + residual
-M, N, K = 300, 768, 256
-A = torch.randn(M, K, device=dev).bfloat16()
-B = torch.randn(N, K, device=dev).bfloat16()
-bias = torch.randn(N, device=dev).bfloat16()
-res = torch.randn(M, N, device=dev).bfloat16()
-C = torch.zeros(M, N, device=dev, dtype=torch.bfloat16)
-run(A, B, 1, N, None, C, bias=bias, resid=res)
-torch.cuda.synchronize()
-ok &= check("bias+resid", C, A.float() @ B.float().t() + bias.float() + res.float()) < 1e-2
-
-# 4) perf: Mixtral gate/up grouped, 8 experts x 4096 rows, N=28672, K=4096
-E, M_e, N, K = 8, 4096, 28672, 4096
+dev = "cuda"
+E, M_e, h, I = 8, 4096, 4096, 14336
 seg = torch.arange(0, (E + 1) * M_e, M_e, dtype=torch.int32, device=dev)
-A = torch.randn(E * M_e, K, device=dev).bfloat16()
-B = (torch.randn(E * N, K, device=dev) * 0.02).bfloat16()
-C = torch.empty(E * M_e, N // 2, device=dev, dtype=torch.bfloat16)
-for _ in range(3):
-    run(A, B, E, N, seg, C, epi=1, hw=128)
-torch.cuda.synchronize()
-t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
-t0.record()
-for _ in range(10):
-    run(A, B, E, N, seg, C, epi=1, hw=128)
-t1.record(); torch.cuda.synchronize()
-ms = t0.elapsed_time(t1) / 10
-fl = 2 * E * M_e * N * K
-print(f"gate/up grouped: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s", flush=True)
-# cuBLAS comparison (dense, same flops)
-A2 = A[:M_e]; B2 = B[:N]
-t0.record()
-for _ in range(10):
-    for e in range(E):
-        torch.matmul(A2, B2.t())
-t1.record(); torch.cuda.synchronize()
-ms2 = t0.elapsed_time(t1) / 10
-print(f"cuBLAS 8x dense: {ms2:.3f} ms  {fl / ms2 / 1e9:.1f} TFLOP/s", flush=True)
-print("ALL OK" if ok else "FAILED")
+A = torch.randn(E * M_e, h, device=dev).bfloat16()
+W13 = (torch.randn(E * 2 * I, h, device=dev) * 0.02).bfloat16()
+H = torch.empty(E * M_e, I, device=dev, dtype=torch.bfloat16)
+ms = timed(lambda: ops.grouped_gemm(A, W13, E, seg, H, swiglu_half=128))
+print(f"gate/up grouped (8 x 4096 x 28672 x 4096): {ms:.3f} ms  {2 * E * M_e * 2 * I * h / ms / 1e9:.1f} TFLOP/s")
+W2 = (torch.randn(E * h, I, device=dev) * 0.02).bfloat16()
+Y = torch.empty(E * M_e, h, device=dev, dtype=torch.bfloat16)
+ms = timed(lambda: ops.grouped_gemm(H, W2, E, seg, Y))
+print(f"down grouped (8 x 4096 x 4096 x 14336): {ms:.3f} ms  {2 * E * M_e * I * h / ms / 1e9:.1f} TFLOP/s")
+X = torch.randn(16384, h, device=dev).bfloat16()
+Wqkv = (torch.randn(6144, h, device=dev) * 0.02).bfloat16()
+pos = torch.arange(2048, device=dev, dtype=torch.int32).repeat(8)
+ms = timed(lambda: ops.gemm_qkv_rope(X, Wqkv, pos, 40, 128, 1e6))
+print(f"qkv+rope (16384 x 6144 x 4096): {ms:.3f} ms  {2 * 16384 * 6144 * h / ms / 1e9:.1f} TFLOP/s")
+Wo = (torch.randn(h, h, device=dev) * 0.02).bfloat16()
+ms = timed(lambda: ops.gemm(X, Wo, residual=X))
+print(f"o-proj (16384 x 4096 x 4096): {ms:.3f} ms  {2 * 16384 * h * h / ms / 1e9:.1f} TFLOP/s")
+# decode-shaped: 16 rows per expert
+segd = torch.arange(0, (E + 1) * 16, 16, dtype=torch.int32, device=dev)
+Ad = torch.randn(E * 16, h, device=dev).bfloat16()
+Hd = torch.empty(E * 16, I, device=dev, dtype=torch.bfloat16)
+ms = timed(lambda: ops.grouped_gemm(Ad, W13, E, segd, Hd, swiglu_half=128))
+print(f"decode gate/up (8 x 16 rows): {ms * 1e3:.1f} us  {E * 2 * I * h * 2 / ms / 1e9:.0f} GB/s weights")
