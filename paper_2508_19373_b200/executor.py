@@ -158,6 +158,45 @@ class HapMoEBlock:
             return self._forward(x_local, batch, 1, decode=True, kv_cache=kv_cache, positions=positions)
         raise ValueError(f"unknown stage {stage!r}")
 
+    def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor, batch: int, seq_len: int,
+                     n_chunks: int = 4) -> torch.Tensor:
+        """Prefill from/to pinned HOST buffers with transfers overlapped with
+        compute: the batch is streamed in sequence chunks — H2D of chunk i+1
+        and D2H of chunk i-1 run on copy streams while chunk i computes.
+        Sequences are independent in the block (causal attention per
+        sequence, per-token experts), so the output equals one forward over
+        the whole batch.  Single-device plans only."""
+        if self.lay.n > 1:
+            raise RuntimeError("forward_host streams chunks on one device; use forward() under a multi-GPU plan")
+        if not (x_host.is_pinned() and out_host.is_pinned()):
+            raise ValueError("host buffers must be pinned for asynchronous copies")
+        n_chunks = max(1, min(n_chunks, batch))
+        while batch % n_chunks:
+            n_chunks -= 1
+        bc = batch // n_chunks
+        rows = bc * seq_len
+        bufs = getattr(self, "_host_bufs", None)
+        if bufs is None or bufs[0].shape[0] != rows or len(bufs) != n_chunks:
+            bufs = [torch.empty(rows, self.cfg.hidden, device=self.device, dtype=BF16) for _ in range(n_chunks)]
+            self._host_bufs = bufs
+            self._streams = (torch.cuda.Stream(), torch.cuda.Stream())
+        h2d, d2h = self._streams
+        comp = torch.cuda.current_stream()
+        h2d.wait_stream(comp)  # device buffers may still be read by a previous call
+        outs = []
+        for i in range(n_chunks):
+            with torch.cuda.stream(h2d):
+                bufs[i].copy_(x_host[i * rows:(i + 1) * rows], non_blocking=True)
+            comp.wait_stream(h2d)
+            o = self.forward(bufs[i], "prefill", bc, seq_len)
+            outs.append(o)
+            d2h.wait_stream(comp)
+            with torch.cuda.stream(d2h):
+                out_host[i * rows:(i + 1) * rows].copy_(o, non_blocking=True)
+                o.record_stream(d2h)
+        comp.wait_stream(d2h)
+        return out_host
+
     def capture_graph(self, x_static: torch.Tensor, stage: str, batch: int, seq_len: int = 1,
                 kv_cache: Optional[KVCache] = None, positions: Optional[torch.Tensor] = None):
         """Capture one forward into a CUDA graph over static buffers; returns

@@ -132,6 +132,23 @@ def test_decode_step_matches_oracle():
     assert rel_err_rows(got[agree], ref["out"][agree]) <= 3e-2
 
 
+def test_forward_host_streams_chunks_identically():
+    """Pipelined host-buffer prefill (sequence chunks, copies overlapped) gives
+    bit-identical output to one device forward over the whole batch."""
+    from paper_2508_19373_b200.config import get_config, scaled
+
+    cfg = scaled(get_config("mixtral-8x7b"), hidden=1024, n_q_heads=8, n_kv_heads=2, inter=1792)
+    blk, x, out, _ = run_block(cfg, 4, 256)
+    xh = x.cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    blk.forward_host(xh, oh, 4, 256, n_chunks=4)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, out.cpu())
+    blk.forward_host(xh, oh, 4, 256, n_chunks=2)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, out.cpu())
+
+
 def test_full_size_mixtral_prefill_properties():
     """Mixtral-8x7B at the bench size (8 x 2048): routing and permutation
     bit-exact on a token sample; output finite; rows of the permuted buffer
