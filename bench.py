@@ -271,6 +271,11 @@ def run_reference(args):
     from paper_2508_19373_b200.config import get_config
 
     cfg = get_config(args.config)
+    # keep the whole --steps/--warmup run within a few minutes: shrink the per-step
+    # sample when many steps are requested (tokens/s is per-token work, so the
+    # sample size does not change the metric beyond fixed per-call overheads)
+    n_calls = args.steps + args.warmup
+    args.cpu_sample_tokens = int(max(32, min(args.cpu_sample_tokens, 256 * 23 // max(n_calls, 1))))
     fn = cpu_reference_setup(cfg, args.cpu_sample_tokens)
     for _ in range(args.warmup):
         fn()

@@ -25,7 +25,7 @@ namespace attn_tc {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 4 role warps + 2 softmax warpgroups
 constexpr int kChunkBytes = 128 * 128;  // 128 rows x 128 B (64 bf16) swizzle-atom column
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain
 
@@ -35,7 +35,7 @@ struct Smem {
   static constexpr int kK = (D / 64) * kChunkBytes;
   static constexpr int kV = (D / 64) * kChunkBytes;
   static constexpr int kP = (BN / 64) * kChunkBytes;
-  static constexpr int kTotal = kQ + 2 * kK + 2 * kV + 2 * kP + 1024;
+  static constexpr int kTotal = kQ + 2 * kK + 2 * kV + 1024;  // P lives in TMEM
 };
 
 // MN-major operand, 128B swizzle: MN chunks of 64 elements lbo bytes apart,
@@ -60,7 +60,30 @@ __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t* r) {
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T (A = P, bf16 pairs packed per 32-bit column).
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t desc_b, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_x16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 template <int D>
@@ -74,14 +97,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + SM::kQ;           // [2][kK]
   uint8_t* sV = sK + 2 * SM::kK;       // [2][kV]
-  uint8_t* sP = sV + 2 * SM::kV;       // [2][kP]
 
   __shared__ __align__(8) uint64_t q_full;
-  __shared__ __align__(8) uint64_t kv_full[2], kv_empty[2];
+  __shared__ __align__(8) uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   __shared__ __align__(8) uint64_t s_full[2], s_free[2];
   __shared__ __align__(8) uint64_t p_full[2], o_done[2];
   __shared__ __align__(8) uint64_t o_final;
   __shared__ uint32_t tmem_base_s;
+  __shared__ float red_max[2][2][BM];  // [tile parity][warpgroup][row]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_mblk = (S + BM - 1) / BM;
@@ -99,11 +122,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmV);
     mbar_init(&q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 128);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&s_free[i], 256);
+      mbar_init(&p_full[i], 256);
       mbar_init(&o_done[i], 1);
     }
     mbar_init(&o_final, 1);
@@ -118,21 +143,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tO = tmem + 256;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer: Q, then the K ring =====================
+    // K_j is consumed by S_j only, so its stage is released as soon as S_j
+    // completes and K runs ahead of V (separate ring, separate thread).
     if (lane == 0) {
       mbar_arrive_expect_tx(&q_full, SM::kQ);
       for (int c = 0; c < D / 64; ++c)
         tma_load_2d(sQ + c * kChunkBytes, &tmQ, &q_full, head * D + c * 64, tok0 + q0, kEvictFirst);
       for (int j = 0; j < nt; ++j) {
         const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[s], SM::kK + SM::kV);
-        for (int c = 0; c < D / 64; ++c) {
-          tma_load_2d(sK + s * SM::kK + c * kChunkBytes, &tmK, &kv_full[s], kvh * D + c * 64, tok0 + j * BN,
+        mbar_wait(&k_empty[s], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[s], SM::kK);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_2d(sK + s * SM::kK + c * kChunkBytes, &tmK, &k_full[s], kvh * D + c * 64, tok0 + j * BN,
                       kEvictLast);
-          tma_load_2d(sV + s * SM::kV + c * kChunkBytes, &tmV, &kv_full[s], kvh * D + c * 64, tok0 + j * BN,
+      }
+    }
+  } else if (warp == 3) {
+    // ===================== TMA producer: the V ring (released after PV_j) =====================
+    if (lane == 0) {
+      for (int j = 0; j < nt; ++j) {
+        const int s = j & 1;
+        mbar_wait(&v_empty[s], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[s], SM::kV);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_2d(sV + s * SM::kV + c * kChunkBytes, &tmV, &v_full[s], kvh * D + c * 64, tok0 + j * BN,
                       kEvictLast);
-        }
       }
     }
   } else if (warp == 1) {
@@ -143,23 +179,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&q_full, 0);
       auto issue_pv = [&](int jp) {
         const int bp = jp & 1;
+        mbar_wait(&v_full[jp & 1], (jp >> 1) & 1);
         mbar_wait(&p_full[bp], (jp >> 1) & 1);
         tc_fence_after();
-        const uint32_t pbase = smem_u32(sP + bp * SM::kP);
         const uint32_t vbase = smem_u32(sV + (jp & 1) * SM::kV);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t da = make_sdesc_sw128(pbase + (kk >> 2) * kChunkBytes) + 2 * (kk & 3);
+          // P_jp sits in its S buffer: warpgroup w's 64 keys packed into columns [w*64, w*64+32)
+          const uint32_t ta = tS[bp] + (kk >> 2) * 64 + (kk & 3) * 8;
           const uint64_t db = make_sdesc_mn_sw128(vbase + kk * 16 * 128, kChunkBytes);
-          umma_bf16_ss(tO, da, db, idPV, (jp | kk) != 0);
+          umma_bf16_ts(tO, ta, db, idPV, (jp | kk) != 0);
         }
         umma_commit(&o_done[bp]);
-        umma_commit(&kv_empty[jp & 1]);
+        umma_commit(&v_empty[jp & 1]);
       };
       for (int j = 0; j < nt; ++j) {
         const int s = j & 1;
-        mbar_wait(&kv_full[s], (j >> 1) & 1);
-        mbar_wait(&s_free[s], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&k_full[s], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t qbase = smem_u32(sQ);
         const uint32_t kbase = smem_u32(sK + s * SM::kK);
@@ -170,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_bf16_ss(tS[s], da, db, idS, kk != 0);
         }
         umma_commit(&s_full[s]);
+        umma_commit(&k_empty[s]);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(nt - 1);
@@ -177,37 +214,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== softmax + epilogue =====================
+    // Two warpgroups split every S row: wg 0 owns key columns [0, 64), wg 1
+    // [64, 128) (and the same halves of O); the row max is combined through
+    // smem with one named barrier per tile.  Two warps per SMSP hide the
+    // LDTM / MUFU latencies one warpgroup alone exposes.
     const int q = warp & 3;
+    const int wg = (warp - 4) >> 2;
     const int r = q * 32 + lane;  // row inside the tile == TMEM lane
     const int qi = q0 + r;        // query position inside the sequence
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    constexpr int HC = BN / 2;    // key columns per warpgroup
+    constexpr int HD = D / 2;     // O columns per warpgroup
+    const int c0 = wg * HC;
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < nt; ++j) {
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t sv[BN];
+      uint32_t sv[HC];
 #pragma unroll
-      for (int c = 0; c < BN; c += 32) tmem_ld_x32(tS[b] + lane_off + c, sv + c);
+      for (int c = 0; c < HC; c += 32) tmem_ld_x32(tS[b] + lane_off + c0 + c, sv + c);
       tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&s_free[b]);
       // mask (only tiles touching the diagonal / sequence end; branch-free
-      // select) + row max with 8 independent partial maxima (log2 domain)
-      const int key0 = j * BN;
-      const bool need_mask = (key0 + BN > kv_end) || (causal && key0 + BN > q0);
+      // select) + partial row max with 8 independent chains (raw scores)
+      const int key0 = j * BN + c0;
+      const bool need_mask = (j * BN + BN > kv_end) || (causal && j * BN + BN > q0);
       if (need_mask) {
         const int lim = causal ? min(S - key0, qi - key0 + 1) : (S - key0);  // keys [0, lim) valid
 #pragma unroll
-        for (int c = 0; c < BN; ++c) sv[c] = c < lim ? sv[c] : __float_as_uint(-INFINITY);
+        for (int c = 0; c < HC; ++c) sv[c] = c < lim ? sv[c] : __float_as_uint(-INFINITY);
       }
       float pm[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) pm[i] = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < BN; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sv[c]));
-      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * scale_log2;
+      for (int c = 0; c < HC; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sv[c]));
+      const float mloc = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                               fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      red_max[j & 1][wg][r] = mloc;
+      named_bar_sync(1, 256);  // both warpgroups of this tile
+      const float mx = fmaxf(mloc, red_max[j & 1][wg ^ 1][r]) * scale_log2;
       float alpha = 1.f;
       if (mx > m_run + kRescaleThreshold || m_run == -INFINITY) {
         alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mx);
@@ -215,55 +261,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         l_run *= alpha;
       }
       const float msub = (m_run == -INFINITY) ? 0.f : m_run;
-      // P_j overwrites the buffer PV_{j-2} read: wait for it
-      if (j >= 2) mbar_wait(&o_done[b], ((j - 2) >> 1) & 1);
-      uint8_t* prow = sP + b * SM::kP + r * 128;
+      // P_j (bf16) overwrites this warpgroup's first 32 columns of its own S region
       float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[HC / 2];
 #pragma unroll
-      for (int c8 = 0; c8 < BN / 8; ++c8) {
-        uint32_t pk[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          // p = 2^(s*scale_log2 - m): one FFMA + one MUFU.EX2 per element
-          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[c8 * 8 + 2 * i]), scale_log2, -msub));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(sv[c8 * 8 + 2 * i + 1]), scale_log2, -msub));
-          ls[i] += p0 + p1;
-          pk[i] = pack_bf16x2(p0, p1);
-        }
-        const int kc = c8 >> 3, cc = c8 & 7;
-        *reinterpret_cast<uint4*>(prow + kc * kChunkBytes + ((cc ^ (r & 7)) << 4)) =
-            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      for (int c2 = 0; c2 < HC / 2; ++c2) {
+        // p = 2^(s*scale_log2 - m): one FFMA + one MUFU.EX2 per element
+        const float p0 = fast_exp2(fmaf(__uint_as_float(sv[2 * c2]), scale_log2, -msub));
+        const float p1 = fast_exp2(fmaf(__uint_as_float(sv[2 * c2 + 1]), scale_log2, -msub));
+        ls[c2 & 3] += p0 + p1;
+        pk[c2] = pack_bf16x2(p0, p1);
       }
+#pragma unroll
+      for (int c = 0; c < HC / 2; c += 16) tmem_st_x16(tS[b] + lane_off + c0 + c, pk + c);
       l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-      // rescale O in TMEM when the running max moved (warp-collective ld/st)
+      // rescale this warpgroup's half of O in TMEM when the running max moved
       const bool corr = (j > 0) && (alpha != 1.f);
       if (__any_sync(0xffffffffu, corr)) {
         mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < D; c += 32) {
+        for (int c = 0; c < HD; c += 32) {
           uint32_t ov[32];
-          tmem_ld_x32(tO + lane_off + c, ov);
+          tmem_ld_x32(tO + lane_off + wg * HD + c, ov);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-          tmem_st_x32(tO + lane_off + c, ov);
+          tmem_st_x32(tO + lane_off + wg * HD + c, ov);
         }
         tmem_st_wait();
       }
-      fence_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[b]);
     }
-    // epilogue
+    // epilogue: combine the two partial row sums, normalise this half of O
+    red_max[nt & 1][wg][r] = l_run;  // parity nt&1 is no longer read by the loop
     mbar_wait(&o_final, 0);
     tc_fence_after();
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    __nv_bfloat16* orow = out + (int64_t)(tok0 + qi) * ldo + (int64_t)head * D;
+    named_bar_sync(1, 256);
+    const float l_tot = red_max[nt & 1][0][r] + red_max[nt & 1][1][r];
+    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
+    __nv_bfloat16* orow = out + (int64_t)(tok0 + qi) * ldo + (int64_t)head * D + wg * HD;
 #pragma unroll
-    for (int c = 0; c < D; c += 32) {
+    for (int c = 0; c < HD; c += 32) {
       uint32_t ov[32];
-      tmem_ld_x32(tO + lane_off + c, ov);
+      tmem_ld_x32(tO + lane_off + wg * HD + c, ov);
       tmem_ld_wait();
       if (qi < S) {
 #pragma unroll
