@@ -1,20 +1,13 @@
-// Attention core: causal GQA prefill (flash-attention style online softmax)
-// and split-KV GQA decode over a head-major KV cache.
-//
-// Prefill (first cut): 4 warps x 16 query rows, 64-key tiles double-buffered
-// with cp.async into 128B-swizzled shared memory, bf16 m16n8k16 tensor-core
-// MMAs with fp32 accumulation, exp2-domain online softmax.  Causal tiles past
-// the diagonal are skipped (half the non-causal FLOPs).
+// Attention core entry points: causal GQA prefill (tcgen05 flash attention,
+// attn_tc.cu) and split-KV GQA decode over a head-major KV cache.
 //
 // Decode: one CTA per (kv-head, 256-key split, sequence) streams K and V once
-// (16-byte coalesced rows) for all G = n_q/n_kv query heads of the group,
-// writes fp32 partial (o, m, l), and a merge kernel rescales the splits.  KV
-// cache layout: [B, n_kv, max_len, d].
+// (16-byte coalesced rows, several loads in flight per thread) for all
+// G = n_q/n_kv query heads of the group, writes fp32 partial (o, m, l), and a
+// merge kernel rescales the splits.  KV cache layout: [B, n_kv, max_len, d].
 //
 // Models: score+value term 4*n*kv_len*h of attention_flops (reference
 // arch.py:161); decode kv_len = input_len + output_len//2 (planner.py:226).
-#include <cstdlib>
-
 #include "common.cuh"
 
 namespace hap {
@@ -24,230 +17,7 @@ int attn_prefill_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, cons
 
 namespace attn {
 
-constexpr int BM = 64;
-constexpr int BN = 64;
 constexpr int kThreads = 128;
-
-template <int D>
-__device__ __forceinline__ uint32_t swz(int row, int col) {  // byte offset in a [rows][D] bf16 tile
-  return (uint32_t)(row * (D * 2) + ((((col >> 3) ^ (row & 7))) << 4) + (col & 7) * 2);
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(sz) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-
-__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-// Load a [64][D] bf16 tile (rows row0.., valid rows < row_lim) into swizzled smem.
-template <int D>
-__device__ __forceinline__ void load_tile(uint32_t smem_base, const __nv_bfloat16* g, int64_t ld, int row0,
-                                          int row_lim) {
-#pragma unroll
-  for (int i = 0; i < (64 * (D / 8)) / kThreads; ++i) {
-    const int idx = threadIdx.x + i * kThreads;
-    const int r = idx / (D / 8), c = (idx % (D / 8)) * 8;
-    const int gr = row0 + r;
-    const bool ok = gr < row_lim;
-    cp_async16(smem_base + swz<D>(r, c), g + (int64_t)(ok ? gr : 0) * ld + c, ok);
-  }
-}
-
-template <int D>
-__global__ void __launch_bounds__(kThreads) prefill_kernel(const __nv_bfloat16* __restrict__ q, int64_t ldq,
-                                                           const __nv_bfloat16* __restrict__ k, int64_t ldk,
-                                                           const __nv_bfloat16* __restrict__ v, int64_t ldv,
-                                                           __nv_bfloat16* __restrict__ out, int64_t ldo, int S,
-                                                           int n_q, int n_kv, float scale_log2, int causal) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  const uint32_t sQ = smem_u32(sm);
-  const uint32_t sK = sQ + BM * D * 2;
-  const uint32_t sV = sK + 2 * BN * D * 2;
-
-  const int n_mblk = (S + BM - 1) / BM;
-  const int mb = causal ? (n_mblk - 1 - blockIdx.x) : blockIdx.x;  // heavy tiles first
-  const int head = blockIdx.y;
-  const int seq = blockIdx.z;
-  const int kvh = head / (n_q / n_kv);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tok0 = (int64_t)seq * S;
-
-  const __nv_bfloat16* qg = q + tok0 * ldq + head * D;
-  const __nv_bfloat16* kg = k + tok0 * ldk + kvh * D;
-  const __nv_bfloat16* vg = v + tok0 * ldv + kvh * D;
-
-  const int q0 = mb * BM;
-  const int kv_end = causal ? min(S, q0 + BM) : S;
-  const int n_tiles = (kv_end + BN - 1) / BN;
-
-  load_tile<D>(sQ, qg, ldq, q0, S);
-  load_tile<D>(sK, kg, ldk, 0, S);
-  load_tile<D>(sV, vg, ldv, 0, S);
-  cp_async_commit();
-
-  uint32_t qf[D / 16][4];
-  float o[D / 8][4];
-#pragma unroll
-  for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m_r[2] = {-INFINITY, -INFINITY};
-  float l_r[2] = {0.f, 0.f};
-  const int g = lane >> 2, tq = lane & 3;
-  const int qrow0 = q0 + warp * 16 + g;  // rows qrow0 and qrow0 + 8
-
-  for (int j = 0; j < n_tiles; ++j) {
-    const int buf = j & 1;
-    if (j + 1 < n_tiles) {
-      load_tile<D>(sK + (buf ^ 1) * BN * D * 2, kg, ldk, (j + 1) * BN, S);
-      load_tile<D>(sV + (buf ^ 1) * BN * D * 2, vg, ldv, (j + 1) * BN, S);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    if (j == 0) {
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const int r = warp * 16 + (lane & 15);
-        const int c = kk * 16 + (lane >> 4) * 8;
-        ldsm_x4(sQ + swz<D>(r, c), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
-      }
-    }
-    const uint32_t kb = sK + buf * BN * D * 2;
-    const uint32_t vb = sV + buf * BN * D * 2;
-    // ---- S = Q K^T (16 x 64 per warp)
-    float s[8][4];
-#pragma unroll
-    for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-#pragma unroll
-      for (int np = 0; np < 4; ++np) {
-        const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
-        const int c = kk * 16 + ((lane >> 3) & 1) * 8;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(kb + swz<D>(key, c), b0, b1, b2, b3);
-        mma_bf16(s[2 * np], qf[kk], b0, b1);
-        mma_bf16(s[2 * np + 1], qf[kk], b2, b3);
-      }
-    }
-    // ---- mask + online softmax (log2 domain)
-    const int key0 = j * BN;
-    const bool need_mask = (key0 + BN > kv_end) || (causal && key0 + BN > q0);
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float x = s[n][e] * scale_log2;
-        if (need_mask) {
-          const int key = key0 + n * 8 + tq * 2 + (e & 1);
-          const int qr = qrow0 + (e >> 1) * 8;
-          if (key >= S || (causal && key > qr)) x = -INFINITY;
-        }
-        s[n][e] = x;
-      }
-    }
-    float mx[2] = {m_r[0], m_r[1]};
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      mx[0] = fmaxf(mx[0], fmaxf(s[n][0], s[n][1]));
-      mx[1] = fmaxf(mx[1], fmaxf(s[n][2], s[n][3]));
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-    }
-    float corr[2], msub[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      msub[r] = (mx[r] == -INFINITY) ? 0.f : mx[r];
-      corr[r] = exp2f(m_r[r] - msub[r]);
-      m_r[r] = mx[r];
-    }
-    float rs[2] = {0.f, 0.f};
-    uint32_t pf[4][4];
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      const float p0 = exp2f(s[n][0] - msub[0]);
-      const float p1 = exp2f(s[n][1] - msub[0]);
-      const float p2 = exp2f(s[n][2] - msub[1]);
-      const float p3 = exp2f(s[n][3] - msub[1]);
-      rs[0] += p0 + p1;
-      rs[1] += p2 + p3;
-      const int kk = n >> 1;
-      if ((n & 1) == 0) {
-        pf[kk][0] = pack_bf16x2(p0, p1);
-        pf[kk][1] = pack_bf16x2(p2, p3);
-      } else {
-        pf[kk][2] = pack_bf16x2(p0, p1);
-        pf[kk][3] = pack_bf16x2(p2, p3);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 1);
-      rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 2);
-      l_r[r] = l_r[r] * corr[r] + rs[r];
-    }
-#pragma unroll
-    for (int n = 0; n < D / 8; ++n) {
-      o[n][0] *= corr[0];
-      o[n][1] *= corr[0];
-      o[n][2] *= corr[1];
-      o[n][3] *= corr[1];
-    }
-    // ---- O += P V
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-#pragma unroll
-      for (int dp = 0; dp < D / 16; ++dp) {
-        const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        const int c = dp * 16 + (lane >> 4) * 8;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vb + swz<D>(key, c), b0, b1, b2, b3);
-        mma_bf16(o[2 * dp], pf[kk], b0, b1);
-        mma_bf16(o[2 * dp + 1], pf[kk], b2, b3);
-      }
-    }
-    __syncthreads();
-  }
-  // ---- epilogue
-  const float inv0 = l_r[0] > 0.f ? 1.f / l_r[0] : 0.f;
-  const float inv1 = l_r[1] > 0.f ? 1.f / l_r[1] : 0.f;
-  __nv_bfloat16* og = out + tok0 * ldo + head * D;
-#pragma unroll
-  for (int n = 0; n < D / 8; ++n) {
-    const int c = n * 8 + tq * 2;
-    if (qrow0 < S)
-      *reinterpret_cast<uint32_t*>(og + (int64_t)qrow0 * ldo + c) = pack_bf16x2(o[n][0] * inv0, o[n][1] * inv0);
-    if (qrow0 + 8 < S)
-      *reinterpret_cast<uint32_t*>(og + (int64_t)(qrow0 + 8) * ldo + c) = pack_bf16x2(o[n][2] * inv1, o[n][3] * inv1);
-  }
-}
 
 // ------------------------------------------------------------------ decode --
 constexpr int kSplit = 256;
@@ -442,46 +212,19 @@ __global__ void decode_merge_kernel(const float* __restrict__ ws_o, const float*
 
 using namespace hap::attn;
 
-template <int D>
-static int launch_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
-                          void* out, int64_t ldo, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
-                          int64_t n_kv_heads, float scale, int32_t causal, cudaStream_t st) {
-  const int smem = (BM + 4 * BN) * D * 2;
-  static int configured = 0;
-  if (!configured) {
-    if (hap::configure_smem((const void*)prefill_kernel<D>, smem)) return HAP_ERR_LAUNCH;
-    configured = 1;
-  }
-  dim3 grid((unsigned)((seq_len + BM - 1) / BM), (unsigned)n_q_heads, (unsigned)n_seqs);
-  const float scale_log2 = scale * 1.4426950408889634f;
-  prefill_kernel<D><<<grid, kThreads, smem, st>>>(
-      reinterpret_cast<const __nv_bfloat16*>(q), ldq, reinterpret_cast<const __nv_bfloat16*>(k), ldk,
-      reinterpret_cast<const __nv_bfloat16*>(v), ldv, reinterpret_cast<__nv_bfloat16*>(out), ldo, (int)seq_len,
-      (int)n_q_heads, (int)n_kv_heads, scale_log2, causal);
-  HAP_CHECK_LAUNCH();
-  return HAP_OK;
-}
-
 extern "C" int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                                 void* out, int64_t ldo, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
                                 int64_t n_kv_heads, int64_t head_dim, float scale, int32_t causal, void* stream) {
   if (!q || !k || !v || !out || n_seqs < 0 || seq_len < 0 || n_q_heads < 1 || n_kv_heads < 1) return HAP_ERR_INVALID_ARG;
   if (n_q_heads % n_kv_heads) return HAP_ERR_INVALID_ARG;
   if (head_dim != 64 && head_dim != 128) return HAP_ERR_UNSUPPORTED;
-  if (ldq % 8 || ldk % 8 || ldv % 8 || ldo % 2) return HAP_ERR_MISALIGNED;
-  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
+  if (ldq % 8 || ldk % 8 || ldv % 8 || ldo % 8) return HAP_ERR_MISALIGNED;
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+       reinterpret_cast<uintptr_t>(out)) & 15)
     return HAP_ERR_MISALIGNED;
   if (n_seqs == 0 || seq_len == 0) return HAP_OK;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  static const bool legacy = getenv("HAP_ATTN_LEGACY_MMA") != nullptr;  // A/B switch for profiling only
-  if (!legacy) {
-    if ((ldq | ldk | ldv) % 8) return HAP_ERR_MISALIGNED;
-    return hap::attn_prefill_tc(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, seq_len, n_q_heads, n_kv_heads, head_dim,
-                                scale, causal, st);
-  }
-  if (head_dim == 128)
-    return launch_prefill<128>(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, seq_len, n_q_heads, n_kv_heads, scale, causal, st);
-  return launch_prefill<64>(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, seq_len, n_q_heads, n_kv_heads, scale, causal, st);
+  return hap::attn_prefill_tc(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, seq_len, n_q_heads, n_kv_heads, head_dim,
+                              scale, causal, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" size_t hap_attn_decode_workspace_bytes(int64_t B, int64_t n_q_heads, int64_t head_dim, int64_t max_len) {

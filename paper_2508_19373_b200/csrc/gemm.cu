@@ -420,7 +420,11 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
   }
   // Upper bound on tiles without reading seg on the host.
   const int64_t n_blocks = (N + p.BN - 1) / p.BN;
-  int64_t gm = kRasterL2Bytes / (K * 2 * TM);
+  static const int64_t l2_budget = [] {
+    const char* e = getenv("HAP_GEMM_RASTER_MB");  // tuning experiments only
+    return e ? (int64_t)atoi(e) << 20 : kRasterL2Bytes;
+  }();
+  int64_t gm = l2_budget / (K * 2 * TM);
   p.group_m = (int32_t)(gm < 1 ? 1 : (gm > 1024 ? 1024 : gm));
   const int64_t max_tiles = ((a_rows + TM - 1) / TM + (n_segs - 1)) * n_blocks;
   const int64_t max_units = kNumSMs / kPair;
