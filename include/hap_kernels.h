@@ -169,6 +169,15 @@ int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk, con
                      int64_t n_kv_heads, int64_t head_dim, float scale, int32_t causal, void* stream);
 
 /*
+ * Prefill: copy the (post-RoPE) k and v of every token of n_seqs sequences of
+ * seq_len tokens (fused qkv rows, token (s,i) = row s*seq_len+i) into
+ * positions [0, seq_len) of a [n_seqs, n_kv, max_len, d] cache.
+ */
+int hap_kv_cache_fill(const void* qkv, int64_t ldqkv, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
+                      int64_t n_kv_heads, int64_t head_dim, void* k_cache, void* v_cache, int64_t max_len,
+                      void* stream);
+
+/*
  * Append one token's k/v (from a fused qkv row buffer) into a [B, max_len,
  * n_kv, d] cache at position pos[b], then split-KV GQA decode attention of
  * q over cache rows [0, pos[b]] for each sequence b.

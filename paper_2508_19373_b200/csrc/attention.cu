@@ -210,7 +210,50 @@ __global__ void decode_merge_kernel(const float* __restrict__ ws_o, const float*
 }  // namespace attn
 }  // namespace hap
 
+namespace hap {
+namespace attn {
+// Prefill: copy every token's (post-RoPE) k and v from the fused qkv rows into
+// the head-major cache rows [0, seq_len) of its sequence.
+template <int D>
+__global__ void kv_fill_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, int n_q, int n_kv, int S,
+                               __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int max_len) {
+  const int i = blockIdx.x, b = blockIdx.y;
+  const __nv_bfloat16* row = qkv + ((int64_t)b * S + i) * ld;
+  for (int v = threadIdx.x; v < n_kv * D / 8; v += blockDim.x) {
+    const int hh = v / (D / 8), c = (v % (D / 8)) * 8;
+    const int64_t dst = (((int64_t)b * n_kv + hh) * max_len + i) * D + c;
+    *reinterpret_cast<uint4*>(kc + dst) = *reinterpret_cast<const uint4*>(row + (int64_t)(n_q + hh) * D + c);
+    *reinterpret_cast<uint4*>(vc + dst) = *reinterpret_cast<const uint4*>(row + (int64_t)(n_q + n_kv + hh) * D + c);
+  }
+}
+}  // namespace attn
+}  // namespace hap
+
 using namespace hap::attn;
+
+extern "C" int hap_kv_cache_fill(const void* qkv, int64_t ldqkv, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
+                                 int64_t n_kv_heads, int64_t head_dim, void* k_cache, void* v_cache, int64_t max_len,
+                                 void* stream) {
+  if (!qkv || !k_cache || !v_cache || n_seqs < 0 || seq_len < 0 || n_q_heads < 1 || n_kv_heads < 1)
+    return HAP_ERR_INVALID_ARG;
+  if (seq_len > max_len) return HAP_ERR_INVALID_ARG;
+  if (head_dim != 64 && head_dim != 128) return HAP_ERR_UNSUPPORTED;
+  if (ldqkv % 8 || ((reinterpret_cast<uintptr_t>(qkv) | reinterpret_cast<uintptr_t>(k_cache) |
+                     reinterpret_cast<uintptr_t>(v_cache)) & 15))
+    return HAP_ERR_MISALIGNED;
+  if (n_seqs == 0 || seq_len == 0) return HAP_OK;
+  dim3 grid((unsigned)seq_len, (unsigned)n_seqs);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto* q = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  auto* kc = reinterpret_cast<__nv_bfloat16*>(k_cache);
+  auto* vc = reinterpret_cast<__nv_bfloat16*>(v_cache);
+  if (head_dim == 128)
+    kv_fill_kernel<128><<<grid, 128, 0, st>>>(q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len);
+  else
+    kv_fill_kernel<64><<<grid, 128, 0, st>>>(q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len);
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
+}
 
 extern "C" int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                                 void* out, int64_t ldo, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,

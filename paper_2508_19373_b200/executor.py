@@ -57,6 +57,7 @@ class CudaOps:
     rope_qk = staticmethod(K.rope_qk)
     attn_prefill = staticmethod(K.attn_prefill)
     attn_decode = staticmethod(K.attn_decode)
+    kv_cache_fill = staticmethod(K.kv_cache_fill)
     router_topk = staticmethod(K.router_topk)
     moe_permute = staticmethod(K.moe_permute)
     moe_combine = staticmethod(K.moe_combine)
@@ -249,6 +250,8 @@ class HapMoEBlock:
                 ops.attn_decode(qkv[:n_seq], kv_cache.k[:n_seq], kv_cache.v[:n_seq], pos[:n_seq], nq, nkv, d,
                                 attn[:n_seq], ws)
         elif n_seq:
+            if kv_cache is not None:  # keep this prefill's k/v for the decode steps that follow
+                ops.kv_cache_fill(qkv, nq, nkv, d, n_seq, S, kv_cache.k, kv_cache.v)
             ops.attn_prefill(qkv, nq, nkv, d, n_seq, S, attn)
         h1 = ops.gemm(attn, w.wo, residual=x if lay.a_tp_rank == 0 else None)
         self._coll("all_reduce", h1, "attn_tp_group")

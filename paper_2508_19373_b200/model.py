@@ -1,0 +1,86 @@
+"""Full-model loop: n_layers HAP blocks of one plan, prefill that fills the
+per-layer KV caches, then decode steps that append to them.
+
+This turns block tokens/s into the end-to-end latency the reference's
+simulator predicts (simulate.py:78-114: prefill = n_layers * (attn + experts
++ comm); decode = output_len * n_layers * (...)), so the predicted-vs-measured
+comparison covers the whole model (scripts/e2e_model.py).  Weights are random
+per layer (seed + layer), generated and packed one layer at a time.
+
+A plan whose expert layout differs between prefill and decode needs the
+weight reshard of transition.py:153-199 between the stages; that switch is
+not implemented yet, so such plans are rejected here.
+"""
+
+from __future__ import annotations
+
+from typing import List, Optional
+
+import torch
+
+from .config import BlockConfig
+from .executor import HapMoEBlock, KVCache
+from .layout import PlanDegrees, replica_sequences
+from .weights import synthetic_weights
+
+
+class HapModel:
+    def __init__(self, cfg: BlockConfig, attention, expert, *, n_layers: Optional[int] = None, rank: int = 0,
+                 device=None, seed: int = 0, ops=None, comm=None):
+        self.cfg = cfg
+        self.n_layers = n_layers or cfg.n_layers
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        self.blocks: List[HapMoEBlock] = []
+        for layer in range(self.n_layers):
+            W = synthetic_weights(cfg, self.device, seed=seed * 1000 + layer)
+            blk = HapMoEBlock(cfg, attention, expert, rank=rank, device=self.device, weights=W, ops=ops,
+                              comm=comm if comm is not None else (self.blocks[0].comm if self.blocks else None))
+            del W
+            self.blocks.append(blk)
+            if self.device.type == "cuda":
+                torch.cuda.empty_cache()
+        self.deg = self.blocks[0].deg
+        self.lay = self.blocks[0].lay
+
+    @classmethod
+    def from_plan(cls, cfg: BlockConfig, plan, **kw) -> "HapModel":
+        if plan.expert_prefill != plan.expert_decode:
+            raise NotImplementedError("prefill->decode expert layout switch (weight reshard) is not implemented yet")
+        return cls(cfg, plan.attention, plan.expert_prefill, **kw)
+
+    def new_caches(self, batch: int, max_len: int) -> List[KVCache]:
+        s0, s1 = replica_sequences(batch, self.deg.a_dp, self.lay.a_rep)
+        nkv = self.blocks[0].w.n_kv_local
+        return [KVCache.empty(max(s1 - s0, 1), nkv, max_len, self.cfg.head_dim, self.device)
+                for _ in range(self.n_layers)]
+
+    def prefill(self, x_local: torch.Tensor, batch: int, seq_len: int, caches: List[KVCache]) -> torch.Tensor:
+        h = x_local
+        for blk, cache in zip(self.blocks, caches):
+            h = blk.forward(h, "prefill", batch, seq_len, kv_cache=cache)
+        return h
+
+    def decode_step(self, x_local: torch.Tensor, batch: int, caches: List[KVCache],
+                    positions: torch.Tensor) -> torch.Tensor:
+        h = x_local
+        for blk, cache in zip(self.blocks, caches):
+            h = blk.forward(h, "decode", batch, kv_cache=cache, positions=positions)
+        return h
+
+    def capture_decode(self, x_static: torch.Tensor, batch: int, caches: List[KVCache], positions: torch.Tensor):
+        """One CUDA graph for a whole decode step (all layers).  `positions` is
+        read on device, so advancing it in place between replays is enough."""
+        if self.deg.e_ep > 1 or self.lay.n > 1:
+            raise RuntimeError("graph capture is supported for single-device, non-EP plans")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                self.decode_step(x_static, batch, caches, positions)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = self.decode_step(x_static, batch, caches, positions)
+        return g, out

@@ -227,6 +227,20 @@ def attn_prefill(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, n_seqs: 
     return out
 
 
+def kv_cache_fill(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, n_seqs: int, seq_len: int,
+                  k_cache: torch.Tensor, v_cache: torch.Tensor) -> None:
+    """Write the prefill tokens' k/v (post-RoPE, fused qkv rows) into cache positions [0, seq_len)."""
+    lib = _lib.load()
+    _need(qkv, "qkv", BF16); _need(k_cache, "k_cache", BF16); _need(v_cache, "v_cache", BF16)
+    _rowmajor(qkv, "qkv")
+    if k_cache.dim() != 4 or not k_cache.is_contiguous() or not v_cache.is_contiguous():
+        raise ValueError("caches must be contiguous [B, n_kv, max_len, d]")
+    st = lib.hap_kv_cache_fill(qkv.data_ptr(), qkv.stride(0), n_seqs, seq_len, n_q, n_kv, head_dim,
+                               k_cache.data_ptr(), v_cache.data_ptr(), k_cache.shape[2], _stream())
+    check(st, "hap_kv_cache_fill")
+    _count(1 if n_seqs * seq_len else 0)
+
+
 def attn_decode_workspace_bytes(B: int, n_q: int, head_dim: int, max_len: int) -> int:
     return int(_lib.load().hap_attn_decode_workspace_bytes(B, n_q, head_dim, max_len))
 

@@ -112,6 +112,13 @@ class CpuOps:
         return out
 
     @staticmethod
+    def kv_cache_fill(qkv, nq, nkv, d, n_seqs, S, kc, vc):
+        for s in range(n_seqs):
+            blk = qkv[s * S:(s + 1) * S]
+            kc[s, :, :S] = blk[:, nq * d:(nq + nkv) * d].view(S, nkv, d).transpose(0, 1)
+            vc[s, :, :S] = blk[:, (nq + nkv) * d:(nq + 2 * nkv) * d].view(S, nkv, d).transpose(0, 1)
+
+    @staticmethod
     def attn_decode(qkv, kc, vc, pos, nq, nkv, d, out, ws):
         B = qkv.shape[0]
         for b in range(B):

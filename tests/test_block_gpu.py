@@ -132,6 +132,53 @@ def test_decode_step_matches_oracle():
     assert rel_err_rows(got[agree], ref["out"][agree]) <= 3e-2
 
 
+def test_model_prefill_then_decode_matches_oracle():
+    """Two stacked tiny blocks: prefill fills the KV caches (checked against
+    the oracle's post-RoPE k/v), then graph-replayed decode steps append and
+    attend; every output vs the chained oracle (bf16 tolerance)."""
+    from paper_2508_19373_b200.config import get_config
+    from paper_2508_19373_b200.layout import PlanDegrees
+    from paper_2508_19373_b200.model import HapModel
+    from paper_2508_19373_b200.weights import synthetic_weights
+
+    cfg = get_config("tiny")
+    L, B, S, steps, max_len = 2, 2, 64, 3, 80
+    model = HapModel(cfg, PlanDegrees(1, 1, 1, 1), None, n_layers=L, seed=5)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    x = torch.randn(B * S, cfg.hidden, device="cuda", generator=g).to(torch.bfloat16)
+    caches = model.new_caches(B, max_len)
+    out = model.prefill(x, B, S, caches)
+    spec = oracle_spec(cfg)
+    Ws = [{k: np32(v) for k, v in synthetic_weights(cfg, "cuda", seed=5 * 1000 + l).items()} for l in range(L)]
+    h = np32(x)
+    ocaches = []
+    for l in range(L):
+        res = O.block_forward(spec, Ws[l], h, B, bf16_mirror=True)
+        ocaches.append(list(O.caches_from_prefill(res, B, max_len)))
+        if l == 0:  # cache fill: post-RoPE k and v of every prompt token
+            assert rel_err_rows(np32(caches[0].k)[:, :, :S], ocaches[0][0][:, :, :S]) < 2e-2
+            assert rel_err_rows(np32(caches[0].v)[:, :, :S], ocaches[0][1][:, :, :S]) < 2e-2
+        h = res["out"]
+    assert rel_err_rows(np32(out), h) < 3e-2
+    pos = torch.full((B,), S, device="cuda", dtype=torch.int32)
+    xd = torch.empty(B, cfg.hidden, device="cuda", dtype=torch.bfloat16)
+    graph, gout = model.capture_decode(xd, B, caches, pos)
+    for step in range(steps):
+        xs = torch.randn(B, cfg.hidden, device="cuda", generator=g).to(torch.bfloat16)
+        xd.copy_(xs)
+        graph.replay()
+        torch.cuda.synchronize()
+        hp = np32(xs)
+        p = np.full(B, S + step)
+        for l in range(L):
+            res = O.decode_forward(spec, Ws[l], hp, ocaches[l][0], ocaches[l][1], p)
+            O.append_kv(ocaches[l][0], ocaches[l][1], res, p)
+            hp = res["out"]
+        assert rel_err_rows(np32(gout), hp) < 3e-2, step
+        pos += 1
+
+
 def test_forward_host_streams_chunks_identically():
     """Pipelined host-buffer prefill (sequence chunks, copies overlapped) gives
     bit-identical output to one device forward over the whole batch."""
