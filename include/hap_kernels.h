@@ -188,6 +188,19 @@ int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, void* v_cache
                     const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads, int64_t head_dim,
                     float scale, void* out, int64_t ldo, void* workspace, size_t ws_bytes, void* stream);
 
+/*
+ * INT4 per-group dequantization of a GQI4 tensor (reference quant.py:19-22,
+ * 61-116): codes packed low-nibble-first (4-byte aligned), float64 scale and
+ * zero point per group of group_size elements, n original elements.
+ * out_bf16 == 0: out is float64 and equals quant.py:dequantize bit for bit
+ * (code*scale rounded, then + zero rounded; no FMA).  out_bf16 == 1: out is
+ * bf16, the same value rounded to fp32 then bf16.
+ * Replaces: the v_dequant / DequantTimeTable term of the stage-switch cost
+ * (transition.py:46-97, 180-199).
+ */
+int hap_int4_dequant(const uint8_t* codes, const double* scales, const double* zero_points, int64_t group_size,
+                     int64_t n, void* out, int32_t out_bf16, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,6 +80,10 @@ SIGNATURES = {
         ctypes.c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_void_p],
     ),
+    "hap_int4_dequant": (
+        ctypes.c_int,
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int32, c_void_p],
+    ),
     "hap_attn_decode_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int64]),
     "hap_attn_decode": (
         ctypes.c_int,

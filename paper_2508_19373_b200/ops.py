@@ -241,6 +241,21 @@ def kv_cache_fill(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, n_seqs:
     _count(1 if n_seqs * seq_len else 0)
 
 
+def int4_dequant(codes: torch.Tensor, scales: torch.Tensor, zero_points: torch.Tensor, group_size: int, n: int,
+                 out: torch.Tensor) -> torch.Tensor:
+    """GQI4 dequantization on the GPU: out (float64 -> bit-exact vs moeplan quant.dequantize, or bf16)."""
+    lib = _lib.load()
+    _need(codes, "codes", torch.uint8); _need(scales, "scales", torch.float64)
+    _need(zero_points, "zero_points", torch.float64); _need(out, "out")
+    if out.dtype not in (torch.float64, BF16) or out.numel() < n:
+        raise ValueError("out must be float64 or bf16 with >= n elements")
+    st = lib.hap_int4_dequant(codes.data_ptr(), scales.data_ptr(), zero_points.data_ptr(), int(group_size), int(n),
+                              out.data_ptr(), int(out.dtype == BF16), _stream())
+    check(st, "hap_int4_dequant")
+    _count(1 if n else 0)
+    return out
+
+
 def attn_decode_workspace_bytes(B: int, n_q: int, head_dim: int, max_len: int) -> int:
     return int(_lib.load().hap_attn_decode_workspace_bytes(B, n_q, head_dim, max_len))
 
