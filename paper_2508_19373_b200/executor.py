@@ -107,6 +107,22 @@ class HapMoEBlock:
         self.timers = None        # set to {} to record CUDA events around the expert GEMMs (bench)
 
     @classmethod
+    def from_rank_weights(cls, cfg: BlockConfig, deg: PlanDegrees, rank: int, w: RankWeights, *, device=None,
+                          ops=None, comm: Optional[Comm] = None) -> "HapMoEBlock":
+        """A block over already-packed weights (e.g. after an expert-layout switch)."""
+        blk = cls.__new__(cls)
+        blk.cfg, blk.deg = cfg, deg
+        blk.lay = RankLayout(deg, rank, cfg.n_q_heads, cfg.n_kv_heads, cfg.n_experts, cfg.inter, cfg.n_shared)
+        blk.ops = ops if ops is not None else CudaOps()
+        blk.device = torch.device(device) if device is not None else w.w13.device
+        blk.w = w
+        blk.comm = comm if comm is not None else (Comm(blk.lay) if blk.lay.n > 1 else None)
+        blk.last_routing = None
+        blk.capture = None
+        blk.timers = None
+        return blk
+
+    @classmethod
     def from_plan(cls, cfg: BlockConfig, plan, stage: str = "prefill", **kw) -> "HapMoEBlock":
         """Build from a moeplan Plan (planner.py:142-166) for one stage."""
         exp = plan.expert_prefill if stage == "prefill" else plan.expert_decode

@@ -46,9 +46,51 @@ class HapModel:
 
     @classmethod
     def from_plan(cls, cfg: BlockConfig, plan, **kw) -> "HapModel":
-        if plan.expert_prefill != plan.expert_decode:
-            raise NotImplementedError("prefill->decode expert layout switch (weight reshard) is not implemented yet")
-        return cls(cfg, plan.attention, plan.expert_prefill, **kw)
+        """Model laid out for the plan's prefill stage; call switch_to_decode()
+        before decoding when the plan's expert layouts differ (Eq.6)."""
+        m = cls(cfg, plan.attention, plan.expert_prefill, **kw)
+        m._attention, m._expert_decode = plan.attention, plan.expert_decode
+        return m
+
+    def switch_expert_layout(self, expert) -> float:
+        """HAP's stage switch: reshard every layer's expert weights to a new
+        expert strategy with one minimal-volume all-to-all per layer
+        (transition.reshard_expert_weights); returns the device seconds spent
+        (max over ranks when distributed)."""
+        from .transition import reshard_expert_weights
+
+        new_deg = PlanDegrees(self.deg.a_tp, self.deg.a_dp, expert.tp_degree, expert.ep_degree,
+                              getattr(expert, "dp_degree", 1))
+        if new_deg == self.deg:
+            return 0.0
+        lay_dst = None
+        cuda = self.device.type == "cuda"
+        if cuda:
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+        new_blocks, comm = [], None
+        for blk in self.blocks:
+            from .layout import RankLayout
+
+            lay_dst = RankLayout(new_deg, blk.lay.rank, self.cfg.n_q_heads, self.cfg.n_kv_heads, self.cfg.n_experts,
+                                 self.cfg.inter, self.cfg.n_shared)
+            w_new = reshard_expert_weights(self.cfg, blk.w, blk.lay, lay_dst)
+            nb = HapMoEBlock.from_rank_weights(self.cfg, new_deg, blk.lay.rank, w_new, device=self.device,
+                                               ops=blk.ops, comm=comm)
+            comm = nb.comm
+            new_blocks.append(nb)
+        seconds = 0.0
+        if cuda:
+            e.record()
+            torch.cuda.synchronize()
+            seconds = s.elapsed_time(e) / 1e3
+        self.blocks, self.deg, self.lay = new_blocks, new_deg, new_blocks[0].lay
+        return seconds
+
+    def switch_to_decode(self) -> float:
+        exp = getattr(self, "_expert_decode", None)
+        return 0.0 if exp is None else self.switch_expert_layout(exp)
 
     def new_caches(self, batch: int, max_len: int) -> List[KVCache]:
         s0, s1 = replica_sequences(batch, self.deg.a_dp, self.lay.a_rep)

@@ -55,6 +55,138 @@ class Int4Backup:
         return out
 
 
+# ------------------------------------------------------------------ reshard --
+def _owned(lay, n_slices: int):
+    """(unit, slice) pairs a rank holds — the reference's _ownership (transition.py:127-150):
+    routed units [0, E), shared units E + u, each cut into n_slices TP slices."""
+    per = lay.inter // n_slices
+    i0, i1 = lay.inter_slice
+    slices = range(i0 // per, i1 // per)
+    e0, e1 = lay.experts
+    own = {(e, s) for e in range(e0, e1) for s in slices}
+    own |= {(lay.n_experts + u, s) for u in range(lay.n_shared) for s in slices}
+    return own
+
+
+def _unpack(cfg, w):
+    """Packed RankWeights -> per-unit (gate [I_l,h], up [I_l,h], down^T [I_l,h]) views."""
+    El, Il, h = w.n_experts_local, w.inter_local, cfg.hidden
+    g13 = w.w13.view(El, Il // w.hw, 2, w.hw, h)
+    gate = g13[:, :, 0].reshape(El, Il, h)
+    up = g13[:, :, 1].reshape(El, Il, h)
+    down_t = w.w2.transpose(1, 2)  # [El, Il, h]
+    units = [(gate[e], up[e], down_t[e]) for e in range(El)]
+    if cfg.n_shared:
+        sil = w.shared_inter_local
+        s13 = w.ws13.view(sil // w.hw_s, 2, w.hw_s, h)
+        sg = s13[:, 0].reshape(sil, h)
+        su = s13[:, 1].reshape(sil, h)
+        sd = w.ws2.t()
+        units += [(sg[u * Il:(u + 1) * Il], su[u * Il:(u + 1) * Il], sd[u * Il:(u + 1) * Il])
+                  for u in range(cfg.n_shared)]
+    return units
+
+
+def reshard_plan(lay_src_list, lay_dst_list, n_slices: int):
+    """Deterministic transfer plan: for every destination rank, each (unit,
+    slice) it needs and does not hold is fetched from one holder under the
+    source layout (greedy: the holder with the least assigned volume)."""
+    n = len(lay_src_list)
+    own_src = [_owned(l, n_slices) for l in lay_src_list]
+    own_dst = [_owned(l, n_slices) for l in lay_dst_list]
+    sends = [[[] for _ in range(n)] for _ in range(n)]  # sends[src][dst] -> [(unit, slice)]
+    load = [0] * n
+    for r in range(n):
+        for key in sorted(own_dst[r] - own_src[r]):
+            holders = [q for q in range(n) if key in own_src[q]]
+            q = min(holders, key=lambda x: (load[x], (x - r) % n))
+            sends[q][r].append(key)
+            load[q] += 1
+    return own_src, own_dst, sends
+
+
+def reshard_expert_weights(cfg, w, lay_src, lay_dst, group=None):
+    """Move this rank's expert weights from layout lay_src to lay_dst with one
+    all-to-all that carries exactly the (unit, slice) pieces each rank is
+    missing (the per-device volume the reference charges in reshard_volume,
+    transition.py:153-177).  Attention weights are unchanged (a plan has one
+    attention strategy).  Returns a new RankWeights packed for lay_dst."""
+    import dataclasses
+    from math import gcd
+
+    import torch.distributed as dist
+
+    from .layout import RankLayout
+    from .weights import interleave_gate_up, swiglu_half_width
+
+    n = lay_src.n
+    tp_i, tp_j = lay_src.deg.e_tp, lay_dst.deg.e_tp
+    n_slices = tp_i * tp_j // gcd(tp_i, tp_j)
+    per = cfg.inter // n_slices
+    h = cfg.hidden
+    mk = lambda deg, r: RankLayout(deg, r, cfg.n_q_heads, cfg.n_kv_heads, cfg.n_experts, cfg.inter, cfg.n_shared)  # noqa: E731
+    srcs = [mk(lay_src.deg, r) for r in range(n)]
+    dsts = [mk(lay_dst.deg, r) for r in range(n)]
+    own_src, own_dst, sends = reshard_plan(srcs, dsts, n_slices)
+    me = lay_src.rank
+    units = _unpack(cfg, w)
+    e0 = lay_src.experts[0]
+    s0 = lay_src.inter_slice[0] // per
+
+    def local_piece(unit, s):
+        if unit < cfg.n_experts:
+            u = units[unit - e0]
+        else:
+            u = units[(lay_src.experts[1] - e0) + (unit - cfg.n_experts)]
+        k = s - s0
+        return torch.stack([t[k * per:(k + 1) * per] for t in u])  # [3, per, h]
+
+    piece_elems = 3 * per * h
+    send_chunks = [local_piece(uu, s) for r in range(n) for (uu, s) in sends[me][r]]
+    in_splits = [len(sends[me][r]) * piece_elems for r in range(n)]
+    out_splits = [len(sends[q][me]) * piece_elems for q in range(n)]
+    dev, dt = w.w13.device, w.w13.dtype
+    send = torch.cat([c.reshape(-1) for c in send_chunks]) if send_chunks else torch.empty(0, dtype=dt, device=dev)
+    recv = torch.empty(sum(out_splits), dtype=dt, device=dev)
+    if n > 1:
+        dist.all_to_all_single(recv, send, output_split_sizes=out_splits, input_split_sizes=in_splits, group=group)
+    received = {}
+    off = 0
+    for q in range(n):
+        for key in sends[q][me]:
+            received[key] = recv[off:off + piece_elems].view(3, per, h)
+            off += piece_elems
+
+    def piece(key):
+        return local_piece(*key) if key in own_src[me] else received[key]
+
+    d = lay_dst
+    de0, de1 = d.experts
+    ds0, ds1 = d.inter_slice[0] // per, d.inter_slice[1] // per
+    il = (ds1 - ds0) * per
+
+    def assemble(unit):
+        p = torch.cat([piece((unit, s)) for s in range(ds0, ds1)], dim=1)  # [3, il, h]
+        return p[0], p[1], p[2]
+
+    rout = [assemble(e) for e in range(de0, de1)]
+    hw = swiglu_half_width(il)
+    w13 = interleave_gate_up(torch.stack([g for g, _, _ in rout]), torch.stack([u for _, u, _ in rout]), hw)
+    w2 = torch.stack([dn.t() for _, _, dn in rout]).contiguous()
+    ws13 = ws2 = None
+    hw_s, sil = 0, 0
+    if cfg.n_shared:
+        sh = [assemble(cfg.n_experts + u) for u in range(cfg.n_shared)]
+        sg = torch.cat([g for g, _, _ in sh])
+        su = torch.cat([u for _, u, _ in sh])
+        sil = sg.shape[0]
+        hw_s = swiglu_half_width(sil)
+        ws13 = interleave_gate_up(sg, su, hw_s)
+        ws2 = torch.cat([dn for _, _, dn in sh]).t().contiguous()
+    return dataclasses.replace(w, w13=w13, w2=w2, hw=hw, ws13=ws13, ws2=ws2, hw_s=hw_s,
+                               n_experts_local=de1 - de0, inter_local=il, shared_inter_local=sil)
+
+
 def _time(fn, reps: int = 5) -> float:
     fn()
     torch.cuda.synchronize()
