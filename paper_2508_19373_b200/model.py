@@ -7,9 +7,10 @@ simulator predicts (simulate.py:78-114: prefill = n_layers * (attn + experts
 comparison covers the whole model (scripts/e2e_model.py).  Weights are random
 per layer (seed + layer), generated and packed one layer at a time.
 
-A plan whose expert layout differs between prefill and decode needs the
-weight reshard of transition.py:153-199 between the stages; that switch is
-not implemented yet, so such plans are rejected here.
+A plan whose expert layout differs between prefill and decode switches
+between the stages with switch_to_decode(): every layer's expert weights are
+resharded by one minimal-volume all-to-all (transition.reshard_expert_weights,
+the volume the reference charges in transition.py:153-177).
 """
 
 from __future__ import annotations
