@@ -97,6 +97,26 @@ int hap_gemm_qkv_rope(const void* A, int64_t M, int64_t lda, int64_t K, const vo
                       int64_t head_dim, float theta, void* stream);
 
 /*
+ * Split-K variants of the two GEMM entry points (same semantics).  With a
+ * workspace, shapes whose tiles cannot cover the 148 SMs (small-M weight
+ * streaming: decode projections, TP-sharded layers) cut K into slices run by
+ * different CTAs, each writing fp32 partials to the workspace; a second kernel
+ * sums the slices in slice order (deterministic, no atomics) and applies the
+ * epilogue.  workspace: device scratch of ws_bytes (hap_gemm_splitk_workspace_bytes()
+ * is the size the library plans for; smaller => fewer slices); it must not be
+ * shared by GEMMs running concurrently.  NULL workspace == the plain entry points.
+ */
+size_t hap_gemm_splitk_workspace_bytes(void);
+int hap_grouped_gemm_bf16_ex(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                             int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
+                             const int32_t* seg_group, void* C, int64_t ldc, int32_t epilogue,
+                             int64_t swiglu_half, const void* bias, const void* residual, int64_t ldr,
+                             void* workspace, size_t ws_bytes, void* stream);
+int hap_gemm_qkv_rope_ex(const void* A, int64_t M, int64_t lda, int64_t K, const void* W, int64_t N,
+                         const void* bias, void* C, int64_t ldc, const int32_t* positions, int64_t n_rope_heads,
+                         int64_t head_dim, float theta, void* workspace, size_t ws_bytes, void* stream);
+
+/*
  * Router: logits[t,e] = x[t,:] . w[e,:] in fp32 with a FIXED reduction
  * order — h is cut into 8 equal contiguous ranges; in range p the partial is
  * the sequential chain acc = fma(x[t,j], w[e,j], acc) (bf16*bf16 products are

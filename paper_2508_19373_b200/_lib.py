@@ -47,6 +47,17 @@ SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
          c_int64, c_int64, c_float, c_void_p],
     ),
+    "hap_gemm_splitk_workspace_bytes": (c_size_t, []),
+    "hap_grouped_gemm_bf16_ex": (
+        ctypes.c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+         c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_size_t, c_void_p],
+    ),
+    "hap_gemm_qkv_rope_ex": (
+        ctypes.c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
+         c_int64, c_int64, c_float, c_void_p, c_size_t, c_void_p],
+    ),
     "hap_router_topk": (
         ctypes.c_int,
         [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int32, c_int32, c_void_p, c_void_p,

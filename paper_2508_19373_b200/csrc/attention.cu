@@ -1,13 +1,15 @@
 // Attention core entry points: causal GQA prefill (tcgen05 flash attention,
 // attn_tc.cu) and split-KV GQA decode over a head-major KV cache.
 //
-// Decode: one CTA per (kv-head, 256-key split, sequence) streams K and V once
-// (16-byte coalesced rows, several loads in flight per thread) for all
-// G = n_q/n_kv query heads of the group, writes fp32 partial (o, m, l), and a
-// merge kernel rescales the splits.  KV cache layout: [B, n_kv, max_len, d].
+// Decode: warp-pipelined split-KV (decode_mma_kernel below) writes fp32
+// partial (o, m, l) per (sequence, query head, key split) and a merge kernel
+// rescales the splits.  KV cache layout: [B, n_kv, max_len, d].
 //
 // Models: score+value term 4*n*kv_len*h of attention_flops (reference
 // arch.py:161); decode kv_len = input_len + output_len//2 (planner.py:226).
+#include <climits>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hap {
@@ -17,10 +19,8 @@ int attn_prefill_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, cons
 
 namespace attn {
 
-constexpr int kThreads = 128;
 
 // ------------------------------------------------------------------ decode --
-constexpr int kSplit = 256;
 constexpr int kMaxG = 8;
 
 // Copy the new token's k and v (from the fused qkv row, after RoPE) into the cache.
@@ -39,152 +39,206 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t 
   }
 }
 
-template <int D, int G>
-__global__ void __launch_bounds__(kThreads) decode_split_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld,
-                                                                const __nv_bfloat16* __restrict__ kc,
-                                                                const __nv_bfloat16* __restrict__ vc, int max_len,
-                                                                const int32_t* __restrict__ pos, int n_q, int n_kv,
-                                                                float scale_log2, float* __restrict__ ws_o,
-                                                                float* __restrict__ ws_ml, int n_splits) {
-  constexpr int LPK = D / 8;              // lanes per key row (16 B each)
-  constexpr int KPP = kThreads / LPK;     // keys per CTA pass
-  constexpr int U = 4;                    // passes in flight per thread
-  __shared__ float qs[G][D];
-  __shared__ float sc[G][kSplit];
-  __shared__ float red[KPP][G][D];
-  __shared__ float mstat[G], lstat[G];
-  const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
-  const int L = pos[b] + 1;
-  const int k0 = split * kSplit;
-  const int k1 = min(L, k0 + kSplit);
-  const int nk = k1 - k0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t out_base = (((int64_t)b * n_q + (int64_t)kvh * G) * n_splits + split);
-  if (nk <= 0) {
-    if (threadIdx.x < G) {
-      float* ml = ws_ml + (out_base + (int64_t)threadIdx.x * n_splits) * 2;
-      ml[0] = -INFINITY;
-      ml[1] = 0.f;
-    }
-    return;
-  }
-  for (int i = threadIdx.x; i < G * D; i += kThreads) {
-    const int gg = i / D, d = i % D;
-    qs[gg][d] = __bfloat162float(qkv[(int64_t)b * ld + (int64_t)(kvh * G + gg) * D + d]);
-  }
-  __syncthreads();
-  const __nv_bfloat16* kbase = kc + (((int64_t)b * n_kv + kvh) * max_len + k0) * D;
-  const __nv_bfloat16* vbase = vc + (((int64_t)b * n_kv + kvh) * max_len + k0) * D;
-  const int kr = threadIdx.x / LPK;   // key slot within a pass
-  const int l16 = threadIdx.x % LPK;  // 8-dim slice
-  float qreg[G][8];
-#pragma unroll
-  for (int gg = 0; gg < G; ++gg)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) qreg[gg][i] = qs[gg][l16 * 8 + i];
+// Warp-pipelined decode (the production path).  Each warp is an independent
+// worker over items (sequence, kv head, key split): a 3-stage ring of 16-key
+// chunks of K and V arrives by TMA (2-D view of the cache, 128B swizzle), the
+// G query heads of the group (rows of an m16 tile) meet the chunk through
+// mma.sync m16n8k16 bf16 (S = Q K^T, then O += P V with P kept in registers),
+// with an online base-2 softmax per row.  The item's (o, m, l) goes to the
+// workspace for decode_merge_kernel.  Memory-level parallelism comes from
+// 8 warps x 3 stages in flight per SM; the FLOPs are negligible.
+constexpr int kDecWarps = 8;
+constexpr int kDecStages = 3;
+constexpr int kDecChunk = 16;
 
-  // ---- scores: U passes of KPP keys in flight
-  for (int kb = 0; kb < nk; kb += KPP * U) {
-    uint4 kv4[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int kk = kb + u * KPP + kr;
-      kv4[u] = kk < nk ? __ldg(reinterpret_cast<const uint4*>(kbase + (int64_t)kk * D + l16 * 8))
-                       : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int kk = kb + u * KPP + kr;
-      const uint32_t kw[4] = {kv4[u].x, kv4[u].y, kv4[u].z, kv4[u].w};
-      float kf[8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = unpack_bf16x2(kw[i]);
-        kf[2 * i] = f.x;
-        kf[2 * i + 1] = f.y;
-      }
-#pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        float acc = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc = fmaf(qreg[gg][i], kf[i], acc);
-#pragma unroll
-        for (int o2 = LPK / 2; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
-        if (l16 == 0 && kk < nk) sc[gg][kk] = acc * scale_log2;
-      }
-    }
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// byte offset of (row r, element e) in a [rows][64 bf16] tile written by TMA with SWIZZLE_128B
+__device__ __forceinline__ uint32_t sw128(int r, int e) {
+  return (uint32_t)(r * 128 + ((((e >> 3) ^ r) & 7) << 4) + ((e & 7) << 1));
+}
+
+struct DecItem {
+  int b, kvh, k0, nk;
+};
+
+__device__ __forceinline__ DecItem dec_item(int item, int n_kv, int ns, int split, const int32_t* pos) {
+  DecItem it;
+  const int bk = item / ns, s = item - bk * ns;
+  it.b = bk / n_kv;
+  it.kvh = bk - it.b * n_kv;
+  it.k0 = s * split;
+  it.nk = max(0, min(pos[it.b] + 1, it.k0 + split) - it.k0);
+  return it;
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(kDecWarps * 32, 1)
+    decode_mma_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                      const __nv_bfloat16* __restrict__ qkv, int64_t ld, int max_len, const int32_t* __restrict__ pos,
+                      int B, int n_q, int n_kv, float scale_log2, float* __restrict__ ws_o,
+                      float* __restrict__ ws_ml, int ns, int split) {
+  constexpr int H = D / 64;                        // 128-byte column halves of a row
+  constexpr int kHalfBytes = kDecChunk * 128;      // 2 KB
+  constexpr int kStageBytes = 2 * H * kHalfBytes;  // K + V of one chunk
+  constexpr int NT = D / 8;                        // O n-tiles
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t bars[kDecWarps][kDecStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = dsm + warp * kDecStages * kStageBytes;
+  uint64_t* full = bars[warp];
+  if (lane == 0) {
+    for (int s = 0; s < kDecStages; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
   }
-  __syncthreads();
-  // ---- softmax statistics per query head
-  for (int gg = warp; gg < G; gg += kThreads / 32) {
-    float m = -INFINITY;
-    for (int i = lane; i < nk; i += 32) m = fmaxf(m, sc[gg][i]);
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o2));
-    float l = 0.f;
-    for (int i = lane; i < nk; i += 32) {
-      const float p = exp2f(sc[gg][i] - m);
-      sc[gg][i] = p;
-      l += p;
+  __syncwarp();
+  const int n_items = B * n_kv * ns;
+  const int W = gridDim.x * kDecWarps;
+  const int worker = blockIdx.x * kDecWarps + warp;
+
+  // ---- load cursor: runs kDecStages chunks ahead over this warp's item stream
+  DecItem li{};
+  int l_item = worker, l_c = 0;
+  auto skip_empty = [&]() {
+    while (l_item < n_items) {
+      li = dec_item(l_item, n_kv, ns, split, pos);
+      if (li.nk > 0) return;
+      l_item += W;
     }
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o2);
+  };
+  auto issue = [&](int stage) {
+    if (l_item >= n_items) return;
     if (lane == 0) {
-      mstat[gg] = m;
-      lstat[gg] = l;
-    }
-  }
-  __syncthreads();
-  // ---- O = P V: thread owns an 8-dim slice of key slot kr, U rows in flight
-  float acc[G][8];
+      const int row = (li.b * n_kv + li.kvh) * max_len + li.k0 + l_c * kDecChunk;
+      uint8_t* dst = ring + stage * kStageBytes;
+      mbar_arrive_expect_tx(&full[stage], kStageBytes);
 #pragma unroll
-  for (int gg = 0; gg < G; ++gg)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[gg][i] = 0.f;
-  for (int kb = 0; kb < nk; kb += KPP * U) {
-    uint4 vv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int kk = kb + u * KPP + kr;
-      vv[u] = kk < nk ? __ldg(reinterpret_cast<const uint4*>(vbase + (int64_t)kk * D + l16 * 8))
-                      : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int kk = kb + u * KPP + kr;
-      if (kk >= nk) continue;
-      const uint32_t vw[4] = {vv[u].x, vv[u].y, vv[u].z, vv[u].w};
-      float vf[8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = unpack_bf16x2(vw[i]);
-        vf[2 * i] = f.x;
-        vf[2 * i + 1] = f.y;
-      }
-#pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        const float p = sc[gg][kk];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[gg][i] = fmaf(p, vf[i], acc[gg][i]);
+      for (int h = 0; h < H; ++h) {
+        tma_load_2d(dst + h * kHalfBytes, &tmK, &full[stage], h * 64, row, kEvictFirst);
+        tma_load_2d(dst + (H + h) * kHalfBytes, &tmV, &full[stage], h * 64, row, kEvictFirst);
       }
     }
-  }
+    if (++l_c * kDecChunk >= li.nk) {
+      l_c = 0;
+      l_item += W;
+      skip_empty();
+    }
+  };
+  skip_empty();
 #pragma unroll
-  for (int gg = 0; gg < G; ++gg)
+  for (int s = 0; s < kDecStages; ++s) issue(s);
+
+  const int g = lane >> 2;  // query-head row of this lane (rows >= G are padding)
+  const int q2 = 2 * (lane & 3);
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int item = worker; item < n_items; item += W) {
+    const DecItem it = dec_item(item, n_kv, ns, split, pos);
+    const int sidx = item % ns;
+    const int64_t obase = ((int64_t)it.b * n_q + it.kvh * G + g) * ns + sidx;
+    if (it.nk == 0) {
+      if (g < G && (lane & 3) == 0) {
+        ws_ml[obase * 2] = -INFINITY;
+        ws_ml[obase * 2 + 1] = 0.f;
+      }
+      continue;
+    }
+    uint32_t qa[D / 16][2];
+    {
+      const __nv_bfloat16* qrow = qkv + (int64_t)it.b * ld + (int64_t)(it.kvh * G + g) * D;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) red[kr][gg][l16 * 8 + i] = acc[gg][i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < G * D; i += kThreads) {
-    const int gg = i / D, d = i % D;
-    float sacc = 0.f;
+      for (int ks = 0; ks < D / 16; ++ks) {
+        qa[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + q2) : 0u;
+        qa[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + q2) : 0u;
+      }
+    }
+    float o[NT][4];
 #pragma unroll
-    for (int q2 = 0; q2 < KPP; ++q2) sacc += red[q2][gg][d];
-    ws_o[(out_base + (int64_t)gg * n_splits) * D + d] = sacc;
-  }
-  if (threadIdx.x < G) {
-    float* ml = ws_ml + (out_base + (int64_t)threadIdx.x * n_splits) * 2;
-    ml[0] = mstat[threadIdx.x];
-    ml[1] = lstat[threadIdx.x];
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    const int nch = (it.nk + kDecChunk - 1) / kDecChunk;
+    for (int c = 0; c < nch; ++c) {
+      mbar_wait(&full[stage], phase);
+      const uint32_t kb = smem_u32(ring + stage * kStageBytes), vb = kb + H * kHalfBytes;
+      // S = Q K^T over the chunk's 16 keys (two n8 tiles)
+      float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+      {
+        const int mi = lane >> 3, key = (mi >> 1) * 8 + (lane & 7);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const int e = ks * 16 + (mi & 1) * 8;
+          uint32_t b00, b01, b10, b11;
+          ldsm_x4(kb + (e >> 6) * kHalfBytes + sw128(key, e & 63), b00, b01, b10, b11);
+          mma_bf16_16816(s0, qa[ks][0], 0u, qa[ks][1], 0u, b00, b01);
+          mma_bf16_16816(s1, qa[ks][0], 0u, qa[ks][1], 0u, b10, b11);
+        }
+      }
+      // online softmax (base 2) on row g: keys c*16 + {q2, q2+1, 8+q2, 9+q2}
+      const int kbase = c * kDecChunk + q2;
+      float x0 = kbase < it.nk ? s0[0] * scale_log2 : -INFINITY;
+      float x1 = kbase + 1 < it.nk ? s0[1] * scale_log2 : -INFINITY;
+      float x2 = kbase + 8 < it.nk ? s1[0] * scale_log2 : -INFINITY;
+      float x3 = kbase + 9 < it.nk ? s1[1] * scale_log2 : -INFINITY;
+      float mx = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float m_new = fmaxf(m, mx);
+      const float alpha = exp2f(m - m_new);
+      const float p0 = exp2f(x0 - m_new), p1 = exp2f(x1 - m_new), p2 = exp2f(x2 - m_new), p3 = exp2f(x3 - m_new);
+      l = l * alpha + (p0 + p1) + (p2 + p3);
+      m = m_new;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        o[n][0] *= alpha;
+        o[n][1] *= alpha;
+      }
+      const uint32_t pa0 = pack_bf16x2(p0, p1), pa2 = pack_bf16x2(p2, p3);
+      // O += P V (V rows = keys, ldmatrix.trans gives the k-major B fragments)
+      {
+        const int mi = lane >> 3, key = (mi & 1) * 8 + (lane & 7);
+#pragma unroll
+        for (int np = 0; np < NT / 2; ++np) {
+          const int e = np * 16 + (mi >> 1) * 8;
+          uint32_t v0, v1, v2, v3;
+          ldsm_x4_t(vb + (e >> 6) * kHalfBytes + sw128(key, e & 63), v0, v1, v2, v3);
+          mma_bf16_16816(o[2 * np], pa0, 0u, pa2, 0u, v0, v1);
+          mma_bf16_16816(o[2 * np + 1], pa0, 0u, pa2, 0u, v2, v3);
+        }
+      }
+      __syncwarp();
+      issue(stage);  // refill the freed stage kDecStages chunks ahead
+      if (++stage == kDecStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    l += __shfl_xor_sync(0xffffffffu, l, 1);
+    l += __shfl_xor_sync(0xffffffffu, l, 2);
+    if (g < G) {
+      float* dst = ws_o + obase * D;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) *reinterpret_cast<float2*>(dst + n * 8 + q2) = make_float2(o[n][0], o[n][1]);
+      if ((lane & 3) == 0) {
+        ws_ml[obase * 2] = m;
+        ws_ml[obase * 2 + 1] = l;
+      }
+    }
   }
 }
 
@@ -229,6 +283,7 @@ __global__ void kv_fill_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld
 }  // namespace attn
 }  // namespace hap
 
+using namespace hap;
 using namespace hap::attn;
 
 extern "C" int hap_kv_cache_fill(const void* qkv, int64_t ldqkv, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
@@ -270,25 +325,72 @@ extern "C" int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64
                               scale, causal, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// Key-split size for the warp-pipelined decode: items = B * n_kv * ceil(len/split)
+// spread round-robin over 148 x kDecWarps warp workers; minimise
+// rounds x (chunks per item + ~1 chunk of per-item overhead).
+static void plan_decode(int64_t B, int64_t n_kv, int64_t max_len, int* split, int* ns) {
+  const int64_t workers = (int64_t)kNumSMs * kDecWarps;
+  const int64_t cps = (max_len + kDecChunk - 1) / kDecChunk;
+  int64_t best_sc = cps, best_cost = INT64_MAX;
+  for (int64_t sc = 1; sc <= cps; ++sc) {
+    const int64_t n = (cps + sc - 1) / sc;
+    if (sc > 1 && (cps + sc - 2) / (sc - 1) == n) continue;  // same split count as a smaller sc
+    const int64_t rounds = (B * n_kv * n + workers - 1) / workers;
+    const int64_t cost = rounds * (sc + 1);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best_sc = sc;
+    }
+  }
+  *split = (int)(best_sc * kDecChunk);
+  *ns = (int)((max_len + best_sc * kDecChunk - 1) / (best_sc * kDecChunk));
+}
+
 extern "C" size_t hap_attn_decode_workspace_bytes(int64_t B, int64_t n_q_heads, int64_t head_dim, int64_t max_len) {
   if (B < 0 || n_q_heads < 1 || head_dim < 1 || max_len < 1) return 0;
-  const int64_t ns = (max_len + kSplit - 1) / kSplit;
-  return (size_t)(B * n_q_heads * ns) * (size_t)(head_dim + 2) * sizeof(float);
+  // the split count depends on n_kv (unknown here): take the largest over every
+  // kv-head count that divides n_q
+  int64_t n = 1;
+  for (int64_t nkv = 1; nkv <= n_q_heads; ++nkv) {
+    if (n_q_heads % nkv) continue;
+    int split, ns;
+    plan_decode(B, nkv, max_len, &split, &ns);
+    if (ns > n) n = ns;
+  }
+  return (size_t)(B * n_q_heads * n) * (size_t)(head_dim + 2) * sizeof(float);
 }
 
 template <int D>
 static int launch_decode(const __nv_bfloat16* q, int64_t ldqkv, __nv_bfloat16* kc, __nv_bfloat16* vc, int64_t max_len,
                          const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads, float scale,
-                         float* ws_o, float* ws_ml, int ns, cudaStream_t st) {
+                         float* ws_o, float* ws_ml, int* ns_out, cudaStream_t st) {
   const int G = (int)(n_q_heads / n_kv_heads);
   kv_append_kernel<D><<<(unsigned)B, 128, 0, st>>>(q, ldqkv, (int)n_q_heads, (int)n_kv_heads, kc, vc, (int)max_len, pos);
-  dim3 grid((unsigned)ns, (unsigned)n_kv_heads, (unsigned)B);
   const float sl2 = scale * 1.4426950408889634f;
+  int split, ns;
+  plan_decode(B, n_kv_heads, max_len, &split, &ns);
+  *ns_out = ns;  // <= the count hap_attn_decode_workspace_bytes provisions for
+  const uint64_t rows = (uint64_t)(B * n_kv_heads * max_len);
+  CUtensorMap tmK, tmV;
+  if (!encode_tmap_2d_bf16(&tmK, kc, D, rows, D * 2, 64, kDecChunk, true) ||
+      !encode_tmap_2d_bf16(&tmV, vc, D, rows, D * 2, 64, kDecChunk, true))
+    return HAP_ERR_DRIVER;
+  const int smem = kDecWarps * kDecStages * 2 * (D / 64) * kDecChunk * 128 + 1024;
+  const int64_t items = B * n_kv_heads * ns;
+  const int64_t ctas = (items + kDecWarps - 1) / kDecWarps;
+  const unsigned grid = (unsigned)(ctas < kNumSMs ? ctas : kNumSMs);
 #define HAP_DEC_CASE(GG)                                                                                          \
-  case GG:                                                                                                        \
-    decode_split_kernel<D, GG><<<grid, kThreads, 0, st>>>(q, ldqkv, kc, vc, (int)max_len, pos, (int)n_q_heads,    \
-                                                          (int)n_kv_heads, sl2, ws_o, ws_ml, ns);                 \
-    break;
+  case GG: {                                                                                                      \
+    static bool cfg = false;                                                                                      \
+    if (!cfg) {                                                                                                   \
+      if (configure_smem((const void*)decode_mma_kernel<D, GG>, smem) != 0) return HAP_ERR_LAUNCH;                \
+      cfg = true;                                                                                                 \
+    }                                                                                                             \
+    decode_mma_kernel<D, GG><<<grid, kDecWarps * 32, smem, st>>>(tmK, tmV, q, ldqkv, (int)max_len, pos, (int)B,   \
+                                                                 (int)n_q_heads, (int)n_kv_heads, sl2, ws_o,      \
+                                                                 ws_ml, ns, split);                               \
+    break;                                                                                                        \
+  }
   switch (G) {
     HAP_DEC_CASE(1)
     HAP_DEC_CASE(2)
@@ -322,14 +424,16 @@ extern "C" int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, vo
   const size_t need = hap_attn_decode_workspace_bytes(B, n_q_heads, head_dim, max_len);
   if (!workspace || ws_bytes < need) return HAP_ERR_WORKSPACE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int ns = (int)((max_len + kSplit - 1) / kSplit);
+  // ws_ml sits after the largest o block the workspace size accounts for
+  const size_t n_units = need / ((size_t)(head_dim + 2) * sizeof(float));
   float* ws_o = reinterpret_cast<float*>(workspace);
-  float* ws_ml = ws_o + (size_t)B * n_q_heads * ns * head_dim;
+  float* ws_ml = ws_o + n_units * head_dim;
+  int ns = 0;
   const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(qkv);
   __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(k_cache);
   __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(v_cache);
-  const int rc = head_dim == 128 ? launch_decode<128>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, ns, st)
-                                 : launch_decode<64>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, ns, st);
+  const int rc = head_dim == 128 ? launch_decode<128>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st)
+                                 : launch_decode<64>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st);
   if (rc != HAP_OK) return rc;
   decode_merge_kernel<<<dim3((unsigned)n_q_heads, (unsigned)B), 128, 0, st>>>(ws_o, ws_ml, ns, (int)n_q_heads, (int)head_dim,
                                                                               reinterpret_cast<__nv_bfloat16*>(out), ldo);

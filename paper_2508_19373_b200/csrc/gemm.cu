@@ -63,9 +63,18 @@ struct Params {
   int32_t rope_cols;
   float theta;
   int32_t group_m;  // raster group (m-blocks)
+  // split-K (small-M, weight-streaming shapes): each tile's K range is cut in
+  // ksplit slices computed by different CTAs; slice ks writes its fp32
+  // partial to part[ks][row][col] (row-major over the B rows N) and
+  // splitk_reduce_kernel sums the slices in slice order and applies the
+  // epilogue — deterministic, no atomics.
+  int32_t ksplit;
+  float* part;
 };
 
 constexpr int kEpiRope = 2;     // internal epilogue id (hap_gemm_qkv_rope)
+constexpr int64_t kSplitMax = 16;
+constexpr size_t kSplitWorkspaceBytes = (size_t)32 << 20;
 constexpr int64_t kRasterL2Bytes = 48ll << 20;  // A rows of one raster group kept L2-resident across n-blocks
 
 struct TileCoord {
@@ -182,7 +191,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (kPair == 2) cluster_sync();  // peer barriers initialised, TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
-  const int total_tiles = tile_start_s[n_segs];
+  const int ksplit = p.ksplit;
+  const int total_units = tile_start_s[n_segs] * ksplit;
   const int num_kb = (p.K + BK - 1) / BK;
 
   if (warp == 0) {
@@ -193,11 +203,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tx_bytes = kPair * (kABytes + bn_half * BK * 2);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = tile0; t < total_tiles; t += tile_step) {
+      for (int u = tile0; u < total_units; u += tile_step) {
+        const int t = u / ksplit, ks = u - t * ksplit;
         const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
         const int b_row = c.g * p.N + c.n_blk * p.BN + (int)crank * bn_half;
         const int a_row = c.m0 + (int)crank * BM;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           if (kPair == 1) {
             mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
@@ -219,13 +231,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = tile0; t < total_tiles; t += tile_step, ++it) {
+      for (int u = tile0; u < total_units; u += tile_step, ++it) {
+        const int ks = u % ksplit;
+        const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint64_t da = make_sdesc_sw128(smem_u32(smA + stage * kABytes));
@@ -233,8 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // +32 bytes per K=16 step inside the 128B swizzle atom (>>4 => +2)
-            if (kPair == 1) umma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
-            else umma_bf16_ss_pair(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            if (kPair == 1) umma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb != kb0) | (k != 0));
+            else umma_bf16_ss_pair(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb != kb0) | (k != 0));
           }
           if (kPair == 1) umma_commit(&empty_bar[stage]);
           else umma_commit_pair_mc(&empty_bar[stage], 0x3);  // frees the stage in both CTAs
@@ -248,7 +262,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================= epilogue =================
     const int q = warp & 3;  // TMEM lane quadrant accessible by this warp
     int it = 0;
-    for (int t = tile0; t < total_tiles; t += tile_step, ++it) {
+    for (int u = tile0; u < total_units; u += tile_step, ++it) {
+      const int t = u / ksplit, ks = u - t * ksplit;
       const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
@@ -258,7 +273,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_ok = row < c.m_end;
       const uint32_t t_row = tmem_base + acc * kAccCols + ((uint32_t)(q * 32) << 16);
       __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
-      if (p.epi == HAP_EPI_SWIGLU) {
+      bool do_epi = true;
+      if (ksplit > 1) {
+        // tcgen05.ld is warp-collective: every lane loads, stores are predicated
+        do_epi = false;
+        float* dst = p.part + ((int64_t)ks * p.a_rows + row) * p.N + c.n_blk * p.BN;
+        const int ncols = min(p.BN, p.N - c.n_blk * p.BN);
+        for (int j = 0; j < p.BN; j += 32) {
+          uint32_t v[32];
+          tmem_ld_x32(t_row + j, v);
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              if (j + i < ncols)
+                __stcg(reinterpret_cast<float4*>(dst + j + i),
+                       make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                                   __uint_as_float(v[i + 3])));
+          }
+        }
+      }
+      if (!do_epi) {
+      } else if (p.epi == HAP_EPI_SWIGLU) {
         const int hw = p.hw;
         const int col0 = c.n_blk * hw;
         for (int j = 0; j < hw; j += 8) {
@@ -403,6 +439,145 @@ static int pick_bn(int64_t N) {
   return N < 256 ? (int)((N + 15) / 16 * 16) : 256;
 }
 
+// ---- split-K reduction + epilogue (phase 2) --------------------------------
+// One thread per 8 outputs of a row: sums the fp32 slice partials in slice
+// order, then the same epilogue math as the TMEM path (bias, residual, SwiGLU,
+// RoPE with inv_freq = 1/theta^(2i/d)), one bf16 rounding.
+__device__ __forceinline__ void sum_slices8(const float* part, int64_t slice, int ks, int64_t off, float (&f)[8]) {
+  float4 a = __ldcg(reinterpret_cast<const float4*>(part + off));
+  float4 b = __ldcg(reinterpret_cast<const float4*>(part + off + 4));
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  for (int s = 1; s < ks; ++s) {
+    a = __ldcg(reinterpret_cast<const float4*>(part + s * slice + off));
+    b = __ldcg(reinterpret_cast<const float4*>(part + s * slice + off + 4));
+    f[0] += a.x; f[1] += a.y; f[2] += a.z; f[3] += a.w; f[4] += b.x; f[5] += b.y; f[6] += b.z; f[7] += b.w;
+  }
+}
+
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(Params p) {
+  const int N = p.N;
+  const int items = p.epi == HAP_EPI_SWIGLU ? N / 16 : (p.epi == kEpiRope ? N / 16 : N / 8);
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(idx / items), it = (int)(idx % items);
+  if (row >= p.a_rows) return;
+  if (p.seg && (row < p.seg[0] || row >= p.seg[p.n_segs])) return;
+  const int64_t slice = (int64_t)p.a_rows * N;
+  const int64_t rbase = (int64_t)row * N;
+  __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+  if (p.epi == HAP_EPI_SWIGLU) {
+    const int hw = p.hw, o = it * 8, j = o / hw, i0 = o % hw;
+    float g[8], u[8];
+    sum_slices8(p.part, slice, p.ksplit, rbase + j * 2 * hw + i0, g);
+    sum_slices8(p.part, slice, p.ksplit, rbase + j * 2 * hw + hw + i0, u);
+    uint32_t out[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = pack_bf16x2(silu(g[2 * i]) * u[2 * i], silu(g[2 * i + 1]) * u[2 * i + 1]);
+    *reinterpret_cast<uint4*>(crow + o) = make_uint4(out[0], out[1], out[2], out[3]);
+  } else if (p.epi == kEpiRope) {
+    const int d = p.head_dim, half = d >> 1, per_head = half / 8;
+    const int hcol = (it / per_head) * d, i0 = (it % per_head) * 8;
+    float x1[8], x2[8];
+    sum_slices8(p.part, slice, p.ksplit, rbase + hcol + i0, x1);
+    sum_slices8(p.part, slice, p.ksplit, rbase + hcol + half + i0, x2);
+    if (p.bias) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        x1[k] += __bfloat162float(p.bias[hcol + i0 + k]);
+        x2[k] += __bfloat162float(p.bias[hcol + half + i0 + k]);
+      }
+    }
+    if (hcol < p.rope_cols) {
+      const float pos = (float)p.positions[row];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float inv_freq = 1.0f / powf(p.theta, (float)(2 * (i0 + k)) / (float)d);
+        float sn, cs;
+        sincosf(pos * inv_freq, &sn, &cs);
+        const float y1 = x1[k] * cs - x2[k] * sn;
+        const float y2 = x2[k] * cs + x1[k] * sn;
+        x1[k] = y1;
+        x2[k] = y2;
+      }
+    }
+    uint32_t o1[4], o2[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      o1[k] = pack_bf16x2(x1[2 * k], x1[2 * k + 1]);
+      o2[k] = pack_bf16x2(x2[2 * k], x2[2 * k + 1]);
+    }
+    *reinterpret_cast<uint4*>(crow + hcol + i0) = make_uint4(o1[0], o1[1], o1[2], o1[3]);
+    *reinterpret_cast<uint4*>(crow + hcol + half + i0) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
+  } else {
+    const int col = it * 8;
+    float f[8];
+    sum_slices8(p.part, slice, p.ksplit, rbase + col, f);
+    if (p.bias) {
+      const uint4 b = *reinterpret_cast<const uint4*>(p.bias + col);
+      const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 bb = unpack_bf16x2(bw[i]);
+        f[2 * i] += bb.x;
+        f[2 * i + 1] += bb.y;
+      }
+    }
+    if (p.resid) {
+      const uint4 r = *reinterpret_cast<const uint4*>(p.resid + (int64_t)row * p.ldr + col);
+      const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 rr = unpack_bf16x2(rw[i]);
+        f[2 * i] += rr.x;
+        f[2 * i + 1] += rr.y;
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = pack_bf16x2(f[2 * i], f[2 * i + 1]);
+    *reinterpret_cast<uint4*>(crow + col) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Choose (BN, ksplit) for a single-CTA launch whose tiles cannot cover the
+// SMs: the smallest split reaching ~85% of the SMs (fewest partial bytes),
+// preferring the larger tile; partials must fit the workspace.
+static void plan_split(Params& p, int64_t a_rows, int64_t K, int64_t N, int64_t n_segs, size_t ws_bytes) {
+  p.ksplit = 1;
+  auto tiles = [&](int64_t bn) { return ((a_rows + BM - 1) / BM + (n_segs - 1)) * ((N + bn - 1) / bn); };
+  if (2 * tiles(p.BN) > kNumSMs || N % 8) return;
+  const int64_t num_kb = (K + BK - 1) / BK;
+  int64_t cands[3] = {p.BN, 0, 0};
+  int nc = 1;
+  if (p.epi == HAP_EPI_STORE) {
+    for (int64_t bn : {(int64_t)128, (int64_t)64})
+      if (bn < p.BN && N % bn == 0) cands[nc++] = bn;
+  } else if (p.epi == kEpiRope && p.head_dim < p.BN) {
+    cands[nc++] = p.head_dim;
+  }
+  int64_t best_bn = p.BN, best_ks = 1, best_units = tiles(p.BN);
+  bool best_ok = false;
+  for (int c = 0; c < nc; ++c) {
+    const int64_t t = tiles(cands[c]);
+    int64_t ks = kNumSMs / t;
+    if (ks > num_kb / 4) ks = num_kb / 4;  // >= 4 k-blocks (256 K) per slice
+    if (ks > kSplitMax) ks = kSplitMax;
+    while (ks > 1 && (size_t)ks * a_rows * N * sizeof(float) > ws_bytes) --ks;
+    if (ks < 1) ks = 1;
+    const int64_t units = t * ks;
+    const bool ok = units * 100 >= kNumSMs * 85;
+    if ((ok && (!best_ok || ks < best_ks)) || (!ok && !best_ok && units > best_units)) {
+      best_bn = cands[c];
+      best_ks = ks;
+      best_units = units;
+      best_ok = ok;
+    }
+  }
+  if (best_ks > 1) {
+    p.BN = (int32_t)best_bn;
+    p.ksplit = (int32_t)best_ks;
+  }
+}
+
 template <int kPair>
 static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
                        int64_t n_groups, int64_t N, int64_t n_segs, void* stream) {
@@ -428,7 +603,8 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
   p.group_m = (int32_t)(gm < 1 ? 1 : (gm > 1024 ? 1024 : gm));
   const int64_t max_tiles = ((a_rows + TM - 1) / TM + (n_segs - 1)) * n_blocks;
   const int64_t max_units = kNumSMs / kPair;
-  const int grid = (int)((max_tiles < max_units ? max_tiles : max_units) * kPair);
+  const int64_t units = max_tiles * p.ksplit;
+  const int grid = (int)((units < max_units ? units : max_units) * kPair);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -456,13 +632,28 @@ static int pair_mode() {
 }
 
 static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
-                  int64_t n_groups, int64_t N, int64_t n_segs, void* stream) {
+                  int64_t n_groups, int64_t N, int64_t n_segs, void* ws, size_t ws_bytes, void* stream) {
   // CTA pairs need B split in two whole 8-row swizzle groups, and only pay off
   // when segments fill 256-row tiles (prefill); weight-streaming decode shapes
   // (a few rows per expert) keep 128-row single-CTA tiles.
+  p.ksplit = 1;
   if (pair_mode() && (p.BN / 2) % 8 == 0 && a_rows >= 256 * n_segs)
     return launch_impl<2>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
-  return launch_impl<1>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
+  // Small-M weight streaming (decode projections, TP-sharded shapes): split K
+  // over more CTAs when a workspace is supplied, then reduce + epilogue.
+  // Only single-m-block launches split, so the slice plan depends on (N, K)
+  // alone and results are identical for every M <= 128 (batch invariance).
+  if (ws && ws_bytes >= 16 && a_rows <= BM) {
+    plan_split(p, a_rows, K, N, n_segs, ws_bytes);
+    p.part = reinterpret_cast<float*>(ws);
+  }
+  const int st = launch_impl<1>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
+  if (st != HAP_OK || p.ksplit == 1) return st;
+  const int items = p.epi == HAP_EPI_STORE ? (int)(N / 8) : (int)(N / 16);
+  const int64_t threads = a_rows * items;
+  splitk_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
 }
 
 }  // namespace gemm
@@ -477,11 +668,15 @@ extern "C" int64_t hap_swiglu_half_width(int64_t inter_dim) {
   return -1;
 }
 
-extern "C" int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
-                                     int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
-                                     const int32_t* seg_group, void* C, int64_t ldc, int32_t epilogue,
-                                     int64_t swiglu_half, const void* bias, const void* residual, int64_t ldr,
-                                     void* stream) {
+extern "C" size_t hap_gemm_splitk_workspace_bytes(void) {
+  return hap::gemm::kSplitWorkspaceBytes;
+}
+
+extern "C" int hap_grouped_gemm_bf16_ex(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                                        int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
+                                        const int32_t* seg_group, void* C, int64_t ldc, int32_t epilogue,
+                                        int64_t swiglu_half, const void* bias, const void* residual, int64_t ldr,
+                                        void* workspace, size_t ws_bytes, void* stream) {
   using namespace hap::gemm;
   if (!A || !B || !C || a_rows < 0 || K <= 0 || N <= 0 || n_groups <= 0) return HAP_ERR_INVALID_ARG;
   if (!seg) n_segs = 1;
@@ -525,12 +720,22 @@ extern "C" int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda,
     return HAP_ERR_INVALID_ARG;
   }
 
-  return hap::gemm::launch(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
+  return hap::gemm::launch(p, A, a_rows, lda, K, B, n_groups, N, n_segs, workspace, ws_bytes, stream);
 }
 
-extern "C" int hap_gemm_qkv_rope(const void* A, int64_t M, int64_t lda, int64_t K, const void* W, int64_t N,
-                                 const void* bias, void* C, int64_t ldc, const int32_t* positions,
-                                 int64_t n_rope_heads, int64_t head_dim, float theta, void* stream) {
+extern "C" int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                                     int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
+                                     const int32_t* seg_group, void* C, int64_t ldc, int32_t epilogue,
+                                     int64_t swiglu_half, const void* bias, const void* residual, int64_t ldr,
+                                     void* stream) {
+  return hap_grouped_gemm_bf16_ex(A, a_rows, lda, K, B, n_groups, N, seg, n_segs, seg_group, C, ldc, epilogue,
+                                  swiglu_half, bias, residual, ldr, nullptr, 0, stream);
+}
+
+extern "C" int hap_gemm_qkv_rope_ex(const void* A, int64_t M, int64_t lda, int64_t K, const void* W, int64_t N,
+                                    const void* bias, void* C, int64_t ldc, const int32_t* positions,
+                                    int64_t n_rope_heads, int64_t head_dim, float theta, void* workspace,
+                                    size_t ws_bytes, void* stream) {
   using namespace hap::gemm;
   if (!A || !W || !C || !positions || M < 0 || K <= 0 || N <= 0) return HAP_ERR_INVALID_ARG;
   if (head_dim != 64 && head_dim != 128) return HAP_ERR_UNSUPPORTED;
@@ -558,5 +763,12 @@ extern "C" int hap_gemm_qkv_rope(const void* A, int64_t M, int64_t lda, int64_t 
   p.BN = (int32_t)head_dim;
   for (int bn = 256; bn >= head_dim; bn -= (int)head_dim)
     if (N % bn == 0) { p.BN = bn; break; }
-  return launch(p, A, M, lda, K, W, 1, N, 1, stream);
+  return launch(p, A, M, lda, K, W, 1, N, 1, workspace, ws_bytes, stream);
+}
+
+extern "C" int hap_gemm_qkv_rope(const void* A, int64_t M, int64_t lda, int64_t K, const void* W, int64_t N,
+                                 const void* bias, void* C, int64_t ldc, const int32_t* positions,
+                                 int64_t n_rope_heads, int64_t head_dim, float theta, void* stream) {
+  return hap_gemm_qkv_rope_ex(A, M, lda, K, W, N, bias, C, ldc, positions, n_rope_heads, head_dim, theta, nullptr,
+                              0, stream);
 }

@@ -8,6 +8,7 @@ back to PyTorch math: if the library is missing, ``_lib.load`` raises.
 
 from __future__ import annotations
 
+import os
 from typing import Optional, Tuple
 
 import torch
@@ -45,6 +46,25 @@ def _need(t: torch.Tensor, name: str, dtype=None, cuda=True):
 def _rowmajor(t: torch.Tensor, name: str):
     if t.dim() != 2 or t.stride(1) != 1:
         raise ValueError(f"{name} must be a 2-D row-major view")
+
+
+# Split-K workspace per device: allocated once and never reallocated,
+# so CUDA graphs that captured a GEMM keep a valid pointer.  SPLITK[0] = False
+# runs the plain entry points (A/B experiments and tests).
+SPLITK = [os.environ.get("HAP_GEMM_SPLITK", "1") != "0"]
+_SPLITK_WS = {}
+
+
+def splitk_workspace(device: torch.device) -> Tuple[int, int]:
+    if not SPLITK[0]:
+        return 0, 0
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    ws = _SPLITK_WS.get(idx)
+    if ws is None:
+        n = int(_lib.load().hap_gemm_splitk_workspace_bytes())
+        ws = torch.empty(n, device=torch.device("cuda", idx), dtype=torch.uint8)
+        _SPLITK_WS[idx] = ws
+    return ws.data_ptr(), ws.numel()
 
 
 def swiglu_half_width(inter: int) -> int:
@@ -86,12 +106,13 @@ def grouped_gemm(a: torch.Tensor, b: torch.Tensor, n_groups: int, seg: Optional[
         _need(residual, "residual", BF16); _rowmajor(residual, "residual")
     if bias is not None:
         _need(bias, "bias", BF16)
-    st = lib.hap_grouped_gemm_bf16(a.data_ptr(), a.shape[0], a.stride(0), K, b2.data_ptr(), n_groups, N,
-                                   _ptr(seg), n_segs, _ptr(seg_group), out.data_ptr(), out.stride(0), epi,
-                                   int(swiglu_half),
-                                   _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0,
-                                   _stream())
-    check(st, "hap_grouped_gemm_bf16")
+    ws, ws_bytes = splitk_workspace(a.device)
+    st = lib.hap_grouped_gemm_bf16_ex(a.data_ptr(), a.shape[0], a.stride(0), K, b2.data_ptr(), n_groups, N,
+                                      _ptr(seg), n_segs, _ptr(seg_group), out.data_ptr(), out.stride(0), epi,
+                                      int(swiglu_half),
+                                      _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0,
+                                      ws or None, ws_bytes, _stream())
+    check(st, "hap_grouped_gemm_bf16_ex")
     _count(1 if a.shape[0] else 0)
     return out
 
@@ -120,10 +141,11 @@ def gemm_qkv_rope(a: torch.Tensor, w: torch.Tensor, positions: torch.Tensor, n_r
     if out is None:
         out = torch.empty(a.shape[0], N, device=a.device, dtype=BF16)
     _need(out, "out", BF16); _rowmajor(out, "out")
-    st = lib.hap_gemm_qkv_rope(a.data_ptr(), a.shape[0], a.stride(0), a.shape[1], w.data_ptr(), N, _ptr(bias),
-                               out.data_ptr(), out.stride(0), positions.data_ptr(), n_rope_heads, head_dim,
-                               float(theta), _stream())
-    check(st, "hap_gemm_qkv_rope")
+    ws, ws_bytes = splitk_workspace(a.device)
+    st = lib.hap_gemm_qkv_rope_ex(a.data_ptr(), a.shape[0], a.stride(0), a.shape[1], w.data_ptr(), N, _ptr(bias),
+                                  out.data_ptr(), out.stride(0), positions.data_ptr(), n_rope_heads, head_dim,
+                                  float(theta), ws or None, ws_bytes, _stream())
+    check(st, "hap_gemm_qkv_rope_ex")
     _count(1 if a.shape[0] else 0)
     return out
 

@@ -49,6 +49,72 @@ def test_dense_gemm(M, N, Kd):
     assert rel_err(np32(c), ref) < 1e-2  # bf16 output rounding
 
 
+@pytest.mark.parametrize("M,N,Kd", [(1, 4096, 4096), (64, 4096, 4096), (130, 768, 4096), (64, 512, 14336)])
+def test_gemm_splitk(M, N, Kd):
+    """Small-M split-K path (decode projections): vs fp64, vs the unsplit
+    kernel, bit-identical across repeated launches (tickets reset, fixed
+    slice-sum order)."""
+    ops = K()
+    a, b = bf16((M, Kd), seed=3), bf16((N, Kd), 0.05, seed=4)
+    bias, res = bf16((N,), seed=5), bf16((M, N), seed=6)
+    outs = [ops.gemm(a, b, bias=bias, residual=res) for _ in range(3)]
+    ops.SPLITK[0] = False
+    try:
+        plain = ops.gemm(a, b, bias=bias, residual=res)
+    finally:
+        ops.SPLITK[0] = True
+    torch.cuda.synchronize()
+    ref = np32(a).astype(np.float64) @ np32(b).astype(np.float64).T + np32(bias) + np32(res)
+    assert rel_err(np32(outs[0]), ref) < 1e-2
+    assert rel_err(np32(outs[0]), np32(plain)) < 1e-2
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+def test_gemm_qkv_rope_splitk_decode_shape():
+    """Mixtral decode QKV (64 x 4096 -> 6144, RoPE on 40 heads): split-K vs unsplit."""
+    ops = K()
+    T, h, d = 64, 4096, 128
+    a, w = bf16((T, h), seed=7), bf16((48 * d, h), 0.02, seed=8)
+    pos = torch.randint(0, 4096, (T,), device=dev, dtype=torch.int32)
+    got = ops.gemm_qkv_rope(a, w, pos, 40, d, 1e6)
+    ops.SPLITK[0] = False
+    try:
+        plain = ops.gemm_qkv_rope(a, w, pos, 40, d, 1e6)
+    finally:
+        ops.SPLITK[0] = True
+    torch.cuda.synchronize()
+    assert rel_err(np32(got), np32(plain)) < 1e-2
+
+
+def test_grouped_gemm_splitk_small_segments():
+    """Grouped SwiGLU + down with a few rows per expert and few tiles (TP-sharded decode)."""
+    from paper_2508_19373_b200.weights import interleave_gate_up, swiglu_half_width
+
+    ops = K()
+    E, h, inter = 4, 2048, 256
+    counts = [5, 0, 17, 3]
+    seg = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), device=dev, dtype=torch.int32)
+    R = sum(counts)
+    x = bf16((R, h), seed=9)
+    wg, wu, wd = bf16((E, inter, h), 0.03, 10), bf16((E, inter, h), 0.03, 11), bf16((E, h, inter), 0.03, 12)
+    hw = swiglu_half_width(inter)
+    w13 = interleave_gate_up(wg, wu, hw).contiguous()
+    H = torch.empty(R, inter, device=dev, dtype=torch.bfloat16)
+    ops.grouped_gemm(x, w13, E, seg, H, swiglu_half=hw)
+    Y = torch.empty(R, h, device=dev, dtype=torch.bfloat16)
+    ops.grouped_gemm(H, wd.contiguous(), E, seg, Y)
+    torch.cuda.synchronize()
+    xs, Hn = np32(x).astype(np.float64), np32(H).astype(np.float64)
+    r0 = 0
+    for e, c in enumerate(counts):
+        if c:
+            g = xs[r0:r0 + c] @ np32(wg[e]).T
+            u = xs[r0:r0 + c] @ np32(wu[e]).T
+            assert rel_err(Hn[r0:r0 + c], g / (1 + np.exp(-g)) * u) < 2e-2
+            assert rel_err(np32(Y[r0:r0 + c]), Hn[r0:r0 + c] @ np32(wd[e]).astype(np.float64).T) < 1e-2
+        r0 += c
+
+
 @pytest.mark.parametrize("d,nq,nkv,bias", [(128, 32, 8, False), (64, 8, 2, False), (128, 16, 16, True),
                                            (128, 4, 1, True)])
 def test_gemm_qkv_rope(d, nq, nkv, bias):
@@ -293,5 +359,27 @@ def test_attn_decode(d, nq, nkv):
         assert np.array_equal(kcn[b, :, p], knew) and np.array_equal(vcn[b, :, p], vnew)
         kk = np.concatenate([kc0[b, :, :p], knew[:, None]], 1).transpose(1, 0, 2)
         vv = np.concatenate([vc0[b, :, :p], vnew[:, None]], 1).transpose(1, 0, 2)
+        ref = O.attention(a[b, :nq * d].reshape(1, nq, d), kk, vv, causal=True).reshape(-1)
+        assert rel_err(np32(out[b]), ref) < 2e-2
+
+
+def test_attn_decode_many_items_per_warp():
+    """More (sequence, kv head, split) items than warp workers, ragged lengths:
+    every warp walks several items through its TMA ring."""
+    B, Lmax, nq, nkv, d = 300, 160, 8, 2, 128
+    qkv = bf16((B, (nq + 2 * nkv) * d), seed=41)
+    kc, vc = bf16((B, nkv, Lmax, d), seed=42), bf16((B, nkv, Lmax, d), seed=43)
+    g = torch.Generator().manual_seed(44)
+    pos = torch.randint(0, Lmax, (B,), generator=g, dtype=torch.int32).to(dev)
+    ops = K()
+    out = torch.empty(B, nq * d, device=dev, dtype=torch.bfloat16)
+    ws = torch.empty(ops.attn_decode_workspace_bytes(B, nq, d, Lmax), device=dev, dtype=torch.uint8)
+    ops.attn_decode(qkv, kc, vc, pos, nq, nkv, d, out, ws)
+    torch.cuda.synchronize()
+    a, kcn, vcn = np32(qkv), np32(kc), np32(vc)
+    for b in range(0, B, 7):
+        p = int(pos[b])
+        kk = kcn[b, :, :p + 1].transpose(1, 0, 2)
+        vv = vcn[b, :, :p + 1].transpose(1, 0, 2)
         ref = O.attention(a[b, :nq * d].reshape(1, nq, d), kk, vv, causal=True).reshape(-1)
         assert rel_err(np32(out[b]), ref) < 2e-2
