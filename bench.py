@@ -104,8 +104,16 @@ def dist_setup(n_gpus: int):
     if world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # HAP_DIST_BACKEND=gloo: validation mode for the multi-rank path on a
+        # single GPU (ranks share the device, collectives staged through host
+        # memory; the numbers are not scaling measurements).  NCCL otherwise.
+        backend = os.environ.get("HAP_DIST_BACKEND", "nccl")
+        dev = local % torch.cuda.device_count() if backend == "gloo" else local
+        torch.cuda.set_device(dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
@@ -126,7 +134,8 @@ def max_over_ranks(v: float) -> float:
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized():
-        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
     return v
@@ -356,7 +365,7 @@ def main():
             blocks[key] = HapMoEBlock(cfg, key, None, rank=rank, weights=weights)
         return blocks[key]
 
-    sampler = ClockSampler(physical_gpu(local))
+    sampler = ClockSampler(physical_gpu(torch.cuda.current_device()))
     sampler.start()
     results = {}
     launches0 = K.LAUNCHES[0]

@@ -20,11 +20,20 @@ from .layout import RankLayout
 GROUP_KINDS = ("attn_tp_group", "exp_tp_group", "gather_group", "a2a_group")
 
 
+def _staged() -> bool:
+    """gloo cannot run collectives on CUDA tensors: stage them through host
+    memory.  Only the single-GPU validation of the multi-rank bench uses this
+    (several ranks sharing one device, HAP_DIST_BACKEND=gloo); NCCL is the
+    product backend."""
+    return dist.is_initialized() and dist.get_backend() == "gloo"
+
+
 class Comm:
     """Per-rank handles to the process groups a plan needs."""
 
     def __init__(self, lay: RankLayout):
         self.lay = lay
+        self.staged = _staged()
         self.groups: Dict[str, Tuple[List[int], Optional[object]]] = {}
         distributed = dist.is_available() and dist.is_initialized()
         if lay.n > 1 and not distributed:
@@ -54,13 +63,23 @@ class Comm:
     # All ops are no-ops on singleton groups.
     def all_reduce(self, t: torch.Tensor, kind: str) -> torch.Tensor:
         if self.size(kind) > 1:
-            dist.all_reduce(t, group=self._g(kind))
+            if self.staged and t.is_cuda:
+                h = t.cpu()
+                dist.all_reduce(h, group=self._g(kind))
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, group=self._g(kind))
         return t
 
     def all_gather(self, out: torch.Tensor, inp: torch.Tensor, kind: str) -> torch.Tensor:
         if self.size(kind) == 1:
             if out.data_ptr() != inp.data_ptr():
                 out.copy_(inp)
+            return out
+        if self.staged and out.is_cuda:
+            h = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_gather_into_tensor(h, inp.contiguous().cpu(), group=self._g(kind))
+            out.copy_(h)
             return out
         dist.all_gather_into_tensor(out, inp.contiguous(), group=self._g(kind))
         return out
@@ -70,6 +89,11 @@ class Comm:
             if out.data_ptr() != inp.data_ptr():
                 out.copy_(inp)
             return out
+        if self.staged and out.is_cuda:
+            h = torch.empty(out.shape, dtype=out.dtype)
+            dist.reduce_scatter_tensor(h, inp.contiguous().cpu(), group=self._g(kind))
+            out.copy_(h)
+            return out
         dist.reduce_scatter_tensor(out, inp.contiguous(), group=self._g(kind))
         return out
 
@@ -77,6 +101,12 @@ class Comm:
                    kind: str) -> torch.Tensor:
         if self.size(kind) == 1:
             out.copy_(inp)
+            return out
+        if self.staged and out.is_cuda:
+            h = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_to_all_single(h, inp.cpu(), output_split_sizes=out_splits, input_split_sizes=in_splits,
+                                   group=self._g(kind))
+            out.copy_(h)
             return out
         dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits,
                                group=self._g(kind))
