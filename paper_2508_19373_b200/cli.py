@@ -106,7 +106,6 @@ def cmd_plan(args) -> Dict:
 def cmd_measure(args) -> Dict:
     from . import calib
 
-    mp = import_moeplan()
     cfg = _block_config(args)
     n = args.devices or 1
     stages = tuple(args.stage) if args.stage else None
@@ -114,7 +113,9 @@ def cmd_measure(args) -> Dict:
                                  stages=stages)
     samples = calib.to_samples(meas)
     out_csv = args.out_csv
-    mp.write_samples_csv(samples, out_csv)
+    from moeplan.costmodel import write_samples_csv
+
+    write_samples_csv(samples, out_csv)
     return {"model": cfg.name, "n_devices": n, "samples_csv": out_csv, "n_samples": len(samples),
             "cells": [{"module": m.module, "stage": m.stage, "strategy": m.strategy,
                        "measured_us": m.measured_s * 1e6, "roofline_us": m.roofline_s * 1e6, "eta": m.eta}

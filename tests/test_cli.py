@@ -61,9 +61,12 @@ def test_run_tiny_prefill_and_decode():
 def test_measure_writes_reference_calibration_csv(tmp_path):
     from paper_2508_19373_b200.config import import_moeplan
 
+    import_moeplan()
+    from moeplan.costmodel import read_samples_csv
+
     csv = tmp_path / "cal.csv"
     rc, out, err = run("measure", "--preset", "tiny", "--devices", "2", "--batch", "4", "--input", "128",
                        "--stage", "prefill", "--reps", "1", "--out-csv", str(csv))
     assert rc == 0, err
-    samples = import_moeplan().read_samples_csv(str(csv))
+    samples = read_samples_csv(str(csv))
     assert len(samples) == json.loads(out)["n_samples"] > 0
