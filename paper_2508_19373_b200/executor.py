@@ -176,15 +176,20 @@ class HapMoEBlock:
         raise ValueError(f"unknown stage {stage!r}")
 
     def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor, batch: int, seq_len: int,
-                     n_chunks: int = 4) -> torch.Tensor:
-        """Prefill from/to pinned HOST buffers with transfers overlapped with
-        compute: the batch is streamed in sequence chunks — H2D of chunk i+1
-        and D2H of chunk i-1 run on copy streams while chunk i computes.
-        Sequences are independent in the block (causal attention per
-        sequence, per-token experts), so the output equals one forward over
-        the whole batch.  Single-device plans only."""
+                     n_chunks: int = 1) -> torch.Tensor:
+        """Prefill from/to pinned HOST buffers, asynchronous and pipelined.
+
+        The call queues H2D (copy stream) -> block forward (current stream) ->
+        D2H (second copy stream) and returns; device input buffers are double
+        buffered across calls, so the H2D of call i+1 overlaps the forward of
+        call i and the D2H of call i overlaps the forward of call i+1 (a
+        serving loop streams batches this way).  ``out_host`` is valid after
+        ``host_sync()`` + a stream synchronisation.  With n_chunks > 1 the batch
+        is additionally split into sequence chunks inside the call (sequences
+        are independent in the block, so the output equals one forward over the
+        whole batch).  Single-device plans only."""
         if self.lay.n > 1:
-            raise RuntimeError("forward_host streams chunks on one device; use forward() under a multi-GPU plan")
+            raise RuntimeError("forward_host streams batches on one device; use forward() under a multi-GPU plan")
         if not (x_host.is_pinned() and out_host.is_pinned()):
             raise ValueError("host buffers must be pinned for asynchronous copies")
         n_chunks = max(1, min(n_chunks, batch))
@@ -192,27 +197,45 @@ class HapMoEBlock:
             n_chunks -= 1
         bc = batch // n_chunks
         rows = bc * seq_len
-        bufs = getattr(self, "_host_bufs", None)
-        if bufs is None or bufs[0].shape[0] != rows or len(bufs) != n_chunks:
-            bufs = [torch.empty(rows, self.cfg.hidden, device=self.device, dtype=BF16) for _ in range(n_chunks)]
-            self._host_bufs = bufs
-            self._streams = (torch.cuda.Stream(), torch.cuda.Stream())
-        h2d, d2h = self._streams
+        st = getattr(self, "_host", None)
+        if st is None or st["rows"] != rows or st["n_chunks"] != n_chunks:
+            st = {"rows": rows, "n_chunks": n_chunks, "i": 0,
+                  "streams": (torch.cuda.Stream(), torch.cuda.Stream()),
+                  "slots": [{"bufs": [torch.empty(rows, self.cfg.hidden, device=self.device, dtype=BF16)
+                                      for _ in range(n_chunks)], "free": [None] * n_chunks} for _ in range(2)]}
+            self._host = st
+        h2d, d2h = st["streams"]
+        slot = st["slots"][st["i"] % 2]
+        st["i"] += 1
         comp = torch.cuda.current_stream()
-        h2d.wait_stream(comp)  # device buffers may still be read by a previous call
-        outs = []
-        for i in range(n_chunks):
+        for c in range(n_chunks):
+            buf = slot["bufs"][c]
+            if slot["free"][c] is not None:  # the forward that last read this buffer has finished
+                h2d.wait_event(slot["free"][c])
+            else:
+                h2d.wait_stream(comp)
             with torch.cuda.stream(h2d):
-                bufs[i].copy_(x_host[i * rows:(i + 1) * rows], non_blocking=True)
-            comp.wait_stream(h2d)
-            o = self.forward(bufs[i], "prefill", bc, seq_len)
-            outs.append(o)
-            d2h.wait_stream(comp)
+                buf.copy_(x_host[c * rows:(c + 1) * rows], non_blocking=True)
+                loaded = torch.cuda.Event()
+                loaded.record(h2d)
+            comp.wait_event(loaded)
+            o = self.forward(buf, "prefill", bc, seq_len)
+            done = torch.cuda.Event()
+            done.record(comp)
+            slot["free"][c] = done
+            d2h.wait_event(done)
             with torch.cuda.stream(d2h):
-                out_host[i * rows:(i + 1) * rows].copy_(o, non_blocking=True)
+                out_host[c * rows:(c + 1) * rows].copy_(o, non_blocking=True)
                 o.record_stream(d2h)
-        comp.wait_stream(d2h)
         return out_host
+
+    def host_sync(self) -> None:
+        """Order the current stream after every queued forward_host copy."""
+        st = getattr(self, "_host", None)
+        if st is not None:
+            comp = torch.cuda.current_stream()
+            for s in st["streams"]:
+                comp.wait_stream(s)
 
     def capture_graph(self, x_static: torch.Tensor, stage: str, batch: int, seq_len: int = 1,
                 kv_cache: Optional[KVCache] = None, positions: Optional[torch.Tensor] = None):

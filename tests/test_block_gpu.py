@@ -180,20 +180,38 @@ def test_model_prefill_then_decode_matches_oracle():
 
 
 def test_forward_host_streams_chunks_identically():
-    """Pipelined host-buffer prefill (sequence chunks, copies overlapped) gives
-    bit-identical output to one device forward over the whole batch."""
+    """Host-buffer prefill (pipelined across calls, optional sequence chunks)
+    gives bit-identical output to one device forward over the whole batch."""
     from paper_2508_19373_b200.config import get_config, scaled
 
     cfg = scaled(get_config("mixtral-8x7b"), hidden=1024, n_q_heads=8, n_kv_heads=2, inter=1792)
     blk, x, out, _ = run_block(cfg, 4, 256)
     xh = x.cpu().pin_memory()
-    oh = torch.empty_like(xh).pin_memory()
-    blk.forward_host(xh, oh, 4, 256, n_chunks=4)
+    for chunks in (1, 4, 2):
+        oh = torch.zeros_like(xh).pin_memory()
+        blk.forward_host(xh, oh, 4, 256, n_chunks=chunks)
+        blk.host_sync()
+        torch.cuda.synchronize()
+        assert torch.equal(oh, out.cpu())
+
+
+def test_forward_host_pipelines_successive_batches():
+    """Three batches queued back to back (H2D of i+1 and D2H of i overlap the
+    forward of i): every output equals its own device forward."""
+    from paper_2508_19373_b200.config import get_config, scaled
+
+    cfg = scaled(get_config("mixtral-8x7b"), hidden=1024, n_q_heads=8, n_kv_heads=2, inter=1792)
+    blk, _, _, _ = run_block(cfg, 2, 256)
+    xs = [torch.randn(512, cfg.hidden, device="cuda").to(torch.bfloat16) for _ in range(3)]
+    refs = [blk.forward(x, "prefill", 2, 256).cpu() for x in xs]
+    hs = [x.cpu().pin_memory() for x in xs]
+    outs = [torch.zeros_like(h).pin_memory() for h in hs]
+    for h, o in zip(hs, outs):
+        blk.forward_host(h, o, 2, 256)
+    blk.host_sync()
     torch.cuda.synchronize()
-    assert torch.equal(oh, out.cpu())
-    blk.forward_host(xh, oh, 4, 256, n_chunks=2)
-    torch.cuda.synchronize()
-    assert torch.equal(oh, out.cpu())
+    for o, r in zip(outs, refs):
+        assert torch.equal(o, r)
 
 
 def test_full_size_mixtral_prefill_properties():
