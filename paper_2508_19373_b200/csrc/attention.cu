@@ -28,6 +28,8 @@ template <int D>
 __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, int n_q, int n_kv,
                                  __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int max_len,
                                  const int32_t* __restrict__ pos) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x;
   const int p = pos[b];
   const __nv_bfloat16* row = qkv + (int64_t)b * ld;
@@ -93,6 +95,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
                       const __nv_bfloat16* __restrict__ qkv, int64_t ld, int max_len, const int32_t* __restrict__ pos,
                       int B, int n_q, int n_kv, float scale_log2, float* __restrict__ ws_o,
                       float* __restrict__ ws_ml, int ns, int split) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int H = D / 64;                        // 128-byte column halves of a row
   constexpr int kHalfBytes = kDecChunk * 128;      // 2 KB
   constexpr int kStageBytes = 2 * H * kHalfBytes;  // K + V of one chunk
@@ -244,6 +248,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
 
 __global__ void decode_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_ml, int n_splits,
                                     int n_q, int D, __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  pdl_trigger();
+  pdl_wait();
   const int hq = blockIdx.x, b = blockIdx.y;
   const int64_t base = ((int64_t)b * n_q + hq) * n_splits;
   float M = -INFINITY;
@@ -271,6 +277,8 @@ namespace attn {
 template <int D>
 __global__ void kv_fill_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, int n_q, int n_kv, int S,
                                __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int max_len) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x, b = blockIdx.y;
   const __nv_bfloat16* row = qkv + ((int64_t)b * S + i) * ld;
   for (int v = threadIdx.x; v < n_kv * D / 8; v += blockDim.x) {
@@ -303,9 +311,9 @@ extern "C" int hap_kv_cache_fill(const void* qkv, int64_t ldqkv, int64_t n_seqs,
   auto* kc = reinterpret_cast<__nv_bfloat16*>(k_cache);
   auto* vc = reinterpret_cast<__nv_bfloat16*>(v_cache);
   if (head_dim == 128)
-    kv_fill_kernel<128><<<grid, 128, 0, st>>>(q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len);
+    { if (hap::launch_k(kv_fill_kernel<128>, dim3(grid), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len) != cudaSuccess) return HAP_ERR_LAUNCH; }
   else
-    kv_fill_kernel<64><<<grid, 128, 0, st>>>(q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len);
+    { if (hap::launch_k(kv_fill_kernel<64>, dim3(grid), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }
@@ -365,7 +373,7 @@ static int launch_decode(const __nv_bfloat16* q, int64_t ldqkv, __nv_bfloat16* k
                          const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads, float scale,
                          float* ws_o, float* ws_ml, int* ns_out, cudaStream_t st) {
   const int G = (int)(n_q_heads / n_kv_heads);
-  kv_append_kernel<D><<<(unsigned)B, 128, 0, st>>>(q, ldqkv, (int)n_q_heads, (int)n_kv_heads, kc, vc, (int)max_len, pos);
+  { if (hap::launch_k(kv_append_kernel<D>, dim3((unsigned)B), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, kc, vc, (int)max_len, pos) != cudaSuccess) return HAP_ERR_LAUNCH; }
   const float sl2 = scale * 1.4426950408889634f;
   int split, ns;
   plan_decode(B, n_kv_heads, max_len, &split, &ns);
@@ -386,9 +394,9 @@ static int launch_decode(const __nv_bfloat16* q, int64_t ldqkv, __nv_bfloat16* k
       if (configure_smem((const void*)decode_mma_kernel<D, GG>, smem) != 0) return HAP_ERR_LAUNCH;                \
       cfg = true;                                                                                                 \
     }                                                                                                             \
-    decode_mma_kernel<D, GG><<<grid, kDecWarps * 32, smem, st>>>(tmK, tmV, q, ldqkv, (int)max_len, pos, (int)B,   \
+    { if (hap::launch_k(decode_mma_kernel<D, GG>, dim3(grid), dim3(kDecWarps * 32), smem, st, tmK, tmV, q, ldqkv, (int)max_len, pos, (int)B,   \
                                                                  (int)n_q_heads, (int)n_kv_heads, sl2, ws_o,      \
-                                                                 ws_ml, ns, split);                               \
+                                                                 ws_ml, ns, split) != cudaSuccess) return HAP_ERR_LAUNCH; }                               \
     break;                                                                                                        \
   }
   switch (G) {
@@ -435,8 +443,8 @@ extern "C" int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, vo
   const int rc = head_dim == 128 ? launch_decode<128>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st)
                                  : launch_decode<64>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st);
   if (rc != HAP_OK) return rc;
-  decode_merge_kernel<<<dim3((unsigned)n_q_heads, (unsigned)B), 128, 0, st>>>(ws_o, ws_ml, ns, (int)n_q_heads, (int)head_dim,
-                                                                              reinterpret_cast<__nv_bfloat16*>(out), ldo);
+  { if (hap::launch_k(decode_merge_kernel, dim3(dim3((unsigned)n_q_heads, (unsigned)B)), dim3(128), 0, st, ws_o, ws_ml, ns, (int)n_q_heads, (int)head_dim,
+                                                                              reinterpret_cast<__nv_bfloat16*>(out), ldo) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }

@@ -83,6 +83,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out, int64_t ldo, int S,
                    int n_q, int n_kv, float scale_log2, int causal) {
+  pdl_trigger();
+  pdl_wait();
   using SM = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -339,9 +341,9 @@ static int launch(const void* q, int64_t ldq, const void* k, int64_t ldk, const 
     configured = 1;
   }
   dim3 grid((unsigned)((S + BM - 1) / BM), (unsigned)n_q, (unsigned)n_seqs);
-  attn_tc_kernel<D><<<grid, kThreads, Smem<D>::kTotal, st>>>(mq, mk, mv, reinterpret_cast<__nv_bfloat16*>(out), ldo,
+  { if (hap::launch_k(attn_tc_kernel<D>, dim3(grid), dim3(kThreads), Smem<D>::kTotal, st, mq, mk, mv, reinterpret_cast<__nv_bfloat16*>(out), ldo,
                                                               (int)S, (int)n_q, (int)n_kv,
-                                                              scale * 1.4426950408889634f, causal);
+                                                              scale * 1.4426950408889634f, causal) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }

@@ -9,6 +9,8 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/hap_kernels.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -288,5 +290,35 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uin
                          uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, bool swizzle128);
 
 int configure_smem(const void* kernel, int bytes);
+
+// ------------------------------------------------ programmatic dependent launch --
+// Every kernel of the library is launched with programmatic stream
+// serialisation: it may be scheduled while its predecessor drains, runs its
+// prologue (barrier init, TMEM alloc, descriptor prefetch, weight prefetch of
+// dense GEMMs), and executes pdl_wait() before its first access to memory a
+// predecessor may write or read (activations, workspaces).  Each kernel calls
+// pdl_trigger() first thing, so a dependent is launched once all of its CTAs
+// are resident.  The attribute is opt-in (HAP_PDL=1, see host.cu); without it
+// the two instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace hap

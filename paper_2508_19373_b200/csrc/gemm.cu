@@ -146,6 +146,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const int n_segs = p.n_segs;
   const int n_blocks = (p.N + p.BN - 1) / p.BN;
+  // PDL: a grouped GEMM's tile list comes from the predecessor (permute's seg),
+  // so it waits first; a dense GEMM's does not, and its producer streams the
+  // first weight stages before waiting (weights are never written).
+  const bool dense = p.seg == nullptr;
+  pdl_trigger();
+  if (!dense) pdl_wait();
 
   // ---- setup: segment table, tile prefix, barriers, TMEM
   for (int i = threadIdx.x; i <= n_segs; i += blockDim.x) {
@@ -203,6 +209,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tx_bytes = kPair * (kABytes + bn_half * BK * 2);
       int stage = 0;
       uint32_t phase = 0;
+      // weight (B) loads of the first stages, issued before the PDL wait
+      int npre = 0;
+      if (dense && tile0 < total_units) {
+        const int t = tile0 / ksplit, ks = tile0 - t * ksplit;
+        const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
+        const int b_row = c.g * p.N + c.n_blk * p.BN + (int)crank * bn_half;
+        const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
+        npre = min(kStages, kb1 - kb0);
+        for (int i = 0; i < npre; ++i) {
+          if (kPair == 1) {
+            mbar_arrive_expect_tx(&full_bar[i], tx_bytes);
+            tma_load_2d(smB + i * kBBytes, &tmB, &full_bar[i], (kb0 + i) * BK, b_row, kEvictNormal);
+          } else {
+            if (leader) mbar_arrive_expect_tx(&full_bar[i], tx_bytes);
+            tma_load_2d_pair(smB + i * kBBytes, &tmB, &full_bar[i], (kb0 + i) * BK, b_row, kEvictNormal);
+          }
+        }
+      }
+      if (dense) pdl_wait();
       for (int u = tile0; u < total_units; u += tile_step) {
         const int t = u / ksplit, ks = u - t * ksplit;
         const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
@@ -210,15 +235,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int a_row = c.m0 + (int)crank * BM;
         const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+          const bool pre = u == tile0 && kb - kb0 < npre;  // B already in flight
+          if (!pre) mbar_wait(&empty_bar[stage], phase ^ 1);
           if (kPair == 1) {
-            mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
+            if (!pre) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
             tma_load_2d(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, kEvictNormal);
-            tma_load_2d(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
+            if (!pre) tma_load_2d(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
           } else {
-            if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
+            if (leader && !pre) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
             tma_load_2d_pair(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, kEvictNormal);
-            tma_load_2d_pair(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
+            if (!pre)
+              tma_load_2d_pair(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -260,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ================= epilogue =================
+    if (dense) pdl_wait();  // reads bias / residual / positions, writes C
     const int q = warp & 3;  // TMEM lane quadrant accessible by this warp
     int it = 0;
     for (int u = tile0; u < total_units; u += tile_step, ++it) {
@@ -455,6 +483,8 @@ __device__ __forceinline__ void sum_slices8(const float* part, int64_t slice, in
 }
 
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(Params p) {
+  pdl_trigger();
+  pdl_wait();
   const int N = p.N;
   const int items = p.epi == HAP_EPI_SWIGLU ? N / 16 : (p.epi == kEpiRope ? N / 16 : N / 8);
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -610,13 +640,15 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Geo<kPair>::kSmemBytes;
   cfg.stream = reinterpret_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kPair;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   if (cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<kPair>, tmA, tmB, p) != cudaSuccess) return HAP_ERR_LAUNCH;
   HAP_CHECK_LAUNCH();
   return HAP_OK;
@@ -651,7 +683,9 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
   if (st != HAP_OK || p.ksplit == 1) return st;
   const int items = p.epi == HAP_EPI_STORE ? (int)(N / 8) : (int)(N / 16);
   const int64_t threads = a_rows * items;
-  splitk_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p);
+  { if (hap::launch_k(splitk_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0,
+               reinterpret_cast<cudaStream_t>(stream), p) != cudaSuccess)
+    return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }

@@ -1,5 +1,6 @@
 // Host-side helpers shared by all kernels: TMA descriptor encoding through the
 // driver entry point, dynamic shared-memory opt-in, status strings.
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -36,6 +37,19 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uin
                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// Off by default: on the graph-replayed Mixtral decode step PDL measured
+// 679 us vs 668 us without (scripts: 3 x 15 windows of 50 replays); the waiting
+// dependents' smem/TMEM reservations cost more than the launch gaps they hide.
+// HAP_PDL=1 turns it on for experiments.
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HAP_PDL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 int configure_smem(const void* kernel, int bytes) {

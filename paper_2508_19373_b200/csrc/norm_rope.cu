@@ -16,6 +16,8 @@ template <int VPL>  // 16-byte vectors per lane
 __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const uint4* __restrict__ x, int T, int hv, int ldxv,
                                                            const uint4* __restrict__ w, float eps,
                                                            uint4* __restrict__ out, int ldov) {
+  pdl_trigger();
+  pdl_wait();
   const int row = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= T) return;
@@ -59,6 +61,8 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const uint4* __restri
 __global__ void __launch_bounds__(kThreads) rope_kernel(__nv_bfloat16* __restrict__ qkv, int T, int64_t ld,
                                                         int n_heads_rot, int d, const int32_t* __restrict__ pos,
                                                         float theta) {
+  pdl_trigger();
+  pdl_wait();
   const int item = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (item >= T * n_heads_rot) return;
@@ -100,7 +104,7 @@ extern "C" int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, con
   const uint4* wv = reinterpret_cast<const uint4*>(w);
   uint4* ov = reinterpret_cast<uint4*>(out);
 #define HAP_NORM_CASE(V) \
-  if (vpl <= V) { rmsnorm_kernel<V><<<grid, kThreads, 0, st>>>(xv, (int)T, hv, (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8)); HAP_CHECK_LAUNCH(); return HAP_OK; }
+  if (vpl <= V) { { if (hap::launch_k(rmsnorm_kernel<V>, dim3(grid), dim3(kThreads), 0, st, xv, (int)T, hv, (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8)) != cudaSuccess) return HAP_ERR_LAUNCH; } HAP_CHECK_LAUNCH(); return HAP_OK; }
   HAP_NORM_CASE(2)
   HAP_NORM_CASE(4)
   HAP_NORM_CASE(8)
@@ -120,8 +124,8 @@ extern "C" int hap_rope_qk(void* qkv, int64_t T, int64_t ld, int64_t n_q_heads, 
   const int heads = (int)(n_q_heads + n_kv_heads);
   const int64_t items = T * heads;
   const int grid = (int)((items * 32 + kThreads - 1) / kThreads);
-  rope_kernel<<<grid, kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<__nv_bfloat16*>(qkv), (int)T, ld, heads, (int)head_dim, positions, theta);
+  { if (hap::launch_k(rope_kernel, dim3(grid), dim3(kThreads), 0, reinterpret_cast<cudaStream_t>(stream), 
+      reinterpret_cast<__nv_bfloat16*>(qkv), (int)T, ld, heads, (int)head_dim, positions, theta) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }

@@ -46,6 +46,8 @@ static size_t ws_bytes(int64_t R, int64_t E, int64_t* nb_out) {
 __global__ void __launch_bounds__(kThreads) rank_kernel(const int32_t* __restrict__ eid, int R, int E,
                                                         int32_t* __restrict__ local_rank,
                                                         int32_t* __restrict__ block_counts) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ int32_t sm[];
   int32_t* running = sm;             // [E]
   int32_t* warp_cnt = sm + E;        // [kWarps][E]
@@ -87,6 +89,8 @@ __global__ void __launch_bounds__(kThreads) rank_kernel(const int32_t* __restric
 
 __global__ void scan_kernel(const int32_t* __restrict__ block_counts, int NB, int E, int32_t* __restrict__ block_base,
                             int32_t* __restrict__ seg) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int32_t totals[kMaxExperts];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int s = 0;
@@ -119,6 +123,8 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const int32_t* __rest
                                                            const int32_t* __restrict__ block_base,
                                                            const uint4* __restrict__ x, int src_div, int hv,
                                                            uint4* __restrict__ x_out, int32_t* __restrict__ dst_of_row) {
+  pdl_trigger();
+  pdl_wait();
   const int warp_global = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int n_warps = (gridDim.x * kThreads) >> 5;
@@ -152,6 +158,8 @@ __global__ void __launch_bounds__(kThreads) combine_kernel(const uint4* __restri
                                                            int res_rows, const uint4* __restrict__ shared_y,
                                                            const float* __restrict__ shared_gate,
                                                            uint4* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int warp_global = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int n_warps = (gridDim.x * kThreads) >> 5;
@@ -240,14 +248,14 @@ extern "C" int hap_moe_permute(const int32_t* expert_of_row, int64_t R, int64_t 
     return HAP_OK;
   }
   const int smem = (int)((1 + kWarps) * E * sizeof(int32_t));
-  rank_kernel<<<(int)nb, kThreads, smem, st>>>(expert_of_row, (int)R, E, local_rank, block_counts);
-  scan_kernel<<<1, 256, 0, st>>>(block_counts, (int)nb, E, block_base, seg);
+  { if (hap::launch_k(rank_kernel, dim3((int)nb), dim3(kThreads), smem, st, expert_of_row, (int)R, E, local_rank, block_counts) != cudaSuccess) return HAP_ERR_LAUNCH; }
+  { if (hap::launch_k(scan_kernel, dim3(1), dim3(256), 0, st, block_counts, (int)nb, E, block_base, seg) != cudaSuccess) return HAP_ERR_LAUNCH; }
   const int64_t warps_needed = R;
   int grid = (int)((warps_needed * 32 + kThreads - 1) / kThreads);
   if (grid > 148 * 16) grid = 148 * 16;
-  scatter_kernel<<<grid, kThreads, 0, st>>>(expert_of_row, (int)R, E, local_rank, block_base,
+  { if (hap::launch_k(scatter_kernel, dim3(grid), dim3(kThreads), 0, st, expert_of_row, (int)R, E, local_rank, block_base,
                                             reinterpret_cast<const uint4*>(x), (int)(src_row_div > 0 ? src_row_div : 1),
-                                            (int)(h / 8), reinterpret_cast<uint4*>(x_out), dst_of_row);
+                                            (int)(h / 8), reinterpret_cast<uint4*>(x_out), dst_of_row) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }
@@ -267,10 +275,10 @@ extern "C" int hap_moe_combine(const void* y, const int32_t* dst_of_row, const f
   const int64_t items = T * ((h / 8 + 31) / 32);
   int grid = (int)((items * 32 + kThreads - 1) / kThreads);
   if (grid > 148 * 16) grid = 148 * 16;
-  combine_kernel<<<grid, kThreads, 0, st>>>(reinterpret_cast<const uint4*>(y), dst_of_row, topk_w, (int)T, (int)k,
+  { if (hap::launch_k(combine_kernel, dim3(grid), dim3(kThreads), 0, st, reinterpret_cast<const uint4*>(y), dst_of_row, topk_w, (int)T, (int)k,
                                             (int)(h / 8), reinterpret_cast<const uint4*>(residual), (int)res_row0,
                                             (int)res_rows, reinterpret_cast<const uint4*>(shared_y), shared_gate,
-                                            reinterpret_cast<uint4*>(out));
+                                            reinterpret_cast<uint4*>(out)) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }

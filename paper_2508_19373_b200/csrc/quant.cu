@@ -24,6 +24,8 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const uint8_t* __rest
                                                            const double* __restrict__ scales,
                                                            const double* __restrict__ zeros, int64_t group_size,
                                                            int64_t n, void* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t n8 = (n + 7) / 8;
   for (int64_t v = (int64_t)blockIdx.x * kThreads + threadIdx.x; v < n8; v += (int64_t)gridDim.x * kThreads) {
     const int64_t e0 = v * 8;
@@ -93,9 +95,9 @@ extern "C" int hap_int4_dequant(const uint8_t* codes, const double* scales, cons
   if (grid > 148 * 32) grid = 148 * 32;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (out_bf16)
-    dequant_kernel<true><<<(int)grid, kThreads, 0, st>>>(codes, scales, zero_points, group_size, n, out);
+    { if (hap::launch_k(dequant_kernel<true>, dim3((int)grid), dim3(kThreads), 0, st, codes, scales, zero_points, group_size, n, out) != cudaSuccess) return HAP_ERR_LAUNCH; }
   else
-    dequant_kernel<false><<<(int)grid, kThreads, 0, st>>>(codes, scales, zero_points, group_size, n, out);
+    { if (hap::launch_k(dequant_kernel<false>, dim3((int)grid), dim3(kThreads), 0, st, codes, scales, zero_points, group_size, n, out) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }

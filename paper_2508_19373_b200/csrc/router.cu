@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(kRanges * NE) router_small_kernel(const __nv_b
                                                                     float* __restrict__ topk_w,
                                                                     float* __restrict__ shared_gate,
                                                                     float* __restrict__ logits_out) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ uint4 xs[];  // token row, h/8 vectors
   __shared__ float part[kRanges][NE];
   const int t = blockIdx.x;
@@ -151,6 +153,8 @@ __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* _
                                                           int has_shared, int32_t* __restrict__ topk_idx,
                                                           float* __restrict__ topk_w, float* __restrict__ shared_gate,
                                                           float* __restrict__ logits_out) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float part[];  // [kRanges][NE][33]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 32 + lane;
@@ -233,16 +237,16 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
       configured_small = 1;
     }
     if (xs_bytes > 64 * 1024) return HAP_ERR_UNSUPPORTED;
-    router_small_kernel<NE><<<(int)T, kRanges * NE, xs_bytes, st>>>(
+    { if (hap::launch_k(router_small_kernel<NE>, dim3((int)T), dim3(kRanges * NE), xs_bytes, st, 
         reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h,
-        (int)(E + has_shared), (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits);
+        (int)(E + has_shared), (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
     HAP_CHECK_LAUNCH();
     return HAP_OK;
   }
   const int grid = (int)((T + 31) / 32);
-  router_kernel<NE><<<grid, kThreads, smem, st>>>(
+  { if (hap::launch_k(router_kernel<NE>, dim3(grid), dim3(kThreads), smem, st, 
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h,
-      (int)(E + has_shared), (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits);
+      (int)(E + has_shared), (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }

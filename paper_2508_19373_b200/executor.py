@@ -274,8 +274,11 @@ class HapMoEBlock:
         xn = ops.rmsnorm(x, w.ln1, cfg.rms_eps)
         nq, nkv = w.n_q_local, w.n_kv_local
         if decode:
-            pos = torch.zeros(rows, device=dev, dtype=torch.int32)
-            pos[:n_seq].copy_(positions)
+            if rows == n_seq and positions.dtype == torch.int32 and positions.is_contiguous():
+                pos = positions
+            else:
+                pos = torch.zeros(rows, device=dev, dtype=torch.int32)
+                pos[:n_seq].copy_(positions)
         else:
             pos = self._prefill_positions(bpr, S, rows)
         # QKV projection with RoPE fused into the GEMM epilogue
