@@ -1,23 +1,30 @@
 // Causal GQA prefill attention on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
 //
-// One CTA per (128-query tile, q head, sequence); 8 warps:
-//   warp 0      TMA producer: Q once, then K_j / V_j 128-key tiles into a
-//               2-stage ring (128B-swizzled, K-major Q/K, MN-major V)
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into a double-buffered
-//               TMEM S tile (128x128 fp32), then O += P_{j-1} V_{j-1} into the
-//               TMEM O accumulator (128 x d fp32), so S_{j+1} overlaps the
-//               softmax of tile j and PV_j overlaps the softmax of tile j+1
-//   warp 2      TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4..7  softmax + epilogue: thread = one query row (its TMEM lane);
-//               tcgen05.ld the S row, causal mask, exp2-domain online softmax
-//               with a lazily updated running max (O is rescaled in TMEM only
-//               when the max grows by > 2^8 — exact, as the same stale max is
-//               used for P and l), P written as bf16 into a swizzled K-major
-//               smem tile that is the A operand of the PV MMA
-// Final: O row / l -> bf16 -> global.
+// Persistent: one CTA per SM walks work items (128-query tile, q head,
+// sequence), heaviest causal tiles first, round-robin over the grid.  The
+// pipelines run across item boundaries, so the next item's Q load and first
+// S = Q K^T MMA overlap the current item's last softmax and its epilogue (a
+// one-CTA-per-item launch paid ~5.8 us of fill/drain per item).  12 warps:
+//   warp 0      TMA producer: Q (double-buffered per item), then the K ring
+//   warp 3      TMA producer: the V ring
+//   warp 1      MMA issuer (one thread): S_j into a double-buffered TMEM S
+//               tile (128x128 fp32); O += P_{j-1} V_{j-1} into the item's TMEM
+//               O buffer (two O buffers alternate between items), so S_{j+1}
+//               overlaps the softmax of tile j and PV_j the softmax of j+1
+//   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1)
+//   warps 4..11 softmax + epilogue, two warpgroups splitting each row: thread
+//               = one query row (its TMEM lane); tcgen05.ld the S row, causal
+//               mask, exp2-domain online softmax with a lazily updated running
+//               max (O is rescaled in TMEM only when the max grows by > 2^8 —
+//               exact, as the same stale max is used for P and l); P is written
+//               back as bf16 over its own S columns (TS-form PV MMA reads it
+//               from TMEM)
+// Final per item: O row / l -> bf16 -> global, then the O buffer is released.
 //
 // Models: score+value term 4*n*kv_len*h of attention_flops (reference
 // arch.py:161); causal: tiles above the diagonal are skipped.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hap {
@@ -35,7 +42,7 @@ struct Smem {
   static constexpr int kK = (D / 64) * kChunkBytes;
   static constexpr int kV = (D / 64) * kChunkBytes;
   static constexpr int kP = (BN / 64) * kChunkBytes;
-  static constexpr int kTotal = kQ + 2 * kK + 2 * kV + 1024;  // P lives in TMEM
+  static constexpr int kTotal = 2 * kQ + 2 * kK + 2 * kV + 1024;  // P lives in TMEM
 };
 
 // MN-major operand, 128B swizzle: MN chunks of 64 elements lbo bytes apart,
@@ -48,21 +55,6 @@ __device__ __forceinline__ uint64_t make_sdesc_mn_sw128(uint32_t smem_addr, uint
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
-}
-
-// 2^x on the FMA pipe (B200's SFU issues only ~8 ex2/clk/SM, the softmax's
-// bottleneck): round-to-nearest split x = n + f via the 1.5*2^23 trick, a
-// degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (max rel err 1.4e-4,
-// far below the bf16 rounding of P), and n added to the exponent bits.
-// x is clamped at -125 so masked (-inf) scores give ~2e-38 instead of 0.
-__device__ __forceinline__ float exp2_poly(float x) {
-  x = fmaxf(x, -125.f);
-  const float t = x + 12582912.f;
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(f, 0.05502926558256149f, 0.2422569841146469f);
-  p = fmaf(f, p, 0.6932530403137207f);
-  p = fmaf(f, p, 0.9999513626098633f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 // D[tmem] (+)= A[tmem] * B[smem]^T (A = P, bf16 pairs packed per 32-bit column).
@@ -78,54 +70,82 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+struct AttnItem {
+  int mb, head, seq, kvh, q0, tok0, kv_end, nt;
+};
+
+__device__ __forceinline__ AttnItem attn_item(int it, int S, int n_q, int n_kv, int n_seqs, int causal) {
+  // q-tiles of one (head, sequence) are consecutive, longest causal rows first:
+  // concurrently running items share K/V in L2, and the tail of the dynamic
+  // schedule is made of the shortest rows
+  AttnItem a;
+  const int n_mblk = (S + BM - 1) / BM;
+  const int m = it % n_mblk, hs = it / n_mblk;
+  a.mb = causal ? (n_mblk - 1 - m) : m;
+  a.head = hs % n_q;
+  a.seq = hs / n_q;
+  a.kvh = a.head / (n_q / n_kv);
+  a.q0 = a.mb * BM;
+  a.tok0 = a.seq * S;
+  a.kv_end = causal ? min(S, a.q0 + BM) : S;
+  a.nt = (a.kv_end + BN - 1) / BN;
+  return a;
+}
+
+// Dynamic item scheduler: items are numbered by decreasing cost (causal rows
+// longest first) and fetched with an atomic ticket by each CTA's Q producer,
+// which forwards them to the other roles through an 8-slot smem ring (the
+// producer runs at most ~3 items ahead of the slowest reader).  The last CTA
+// to run out of work re-zeroes the tickets, so the kernel leaves them ready for
+// the next launch on the stream (launches of this kernel must not run
+// concurrently on several streams of one device).
+__device__ int g_attn_sched[2];
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out, int64_t ldo, int S,
-                   int n_q, int n_kv, float scale_log2, int causal) {
+                   int n_q, int n_kv, int n_seqs, float scale_log2, int causal) {
   pdl_trigger();
   pdl_wait();
   using SM = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + SM::kQ;           // [2][kK]
+  uint8_t* sQ = smem;                  // [2][kQ]
+  uint8_t* sK = sQ + 2 * SM::kQ;       // [2][kK]
   uint8_t* sV = sK + 2 * SM::kK;       // [2][kV]
 
-  __shared__ __align__(8) uint64_t q_full;
+  __shared__ __align__(8) uint64_t q_full[2], q_empty[2];
   __shared__ __align__(8) uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-  __shared__ __align__(8) uint64_t s_full[2], s_free[2];
-  __shared__ __align__(8) uint64_t p_full[2], o_done[2];
-  __shared__ __align__(8) uint64_t o_final;
+  __shared__ __align__(8) uint64_t s_full[2], p_full[2], o_done[2];
+  __shared__ __align__(8) uint64_t o_final[2], o_free[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ float red_max[2][2][BM];  // [tile parity][warpgroup][row]
+  __shared__ float red_l[2][BM];       // [warpgroup][row], item epilogue
+  __shared__ int item_ring[8];
+  __shared__ __align__(8) uint64_t item_full[8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_mblk = (S + BM - 1) / BM;
-  const int mb = causal ? (n_mblk - 1 - (int)blockIdx.x) : (int)blockIdx.x;
-  const int head = blockIdx.y, seq = blockIdx.z;
-  const int kvh = head / (n_q / n_kv);
-  const int q0 = mb * BM;
-  const int tok0 = seq * S;
-  const int kv_end = causal ? min(S, q0 + BM) : S;
-  const int nt = (kv_end + BN - 1) / BN;
+  const int n_items = ((S + BM - 1) / BM) * n_q * n_seqs;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    mbar_init(&q_full, 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 256);
       mbar_init(&p_full[i], 256);
       mbar_init(&o_done[i], 1);
+      mbar_init(&o_final[i], 1);
+      mbar_init(&o_free[i], 256);
     }
-    mbar_init(&o_final, 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&item_full[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(&tmem_base_s, 512);
@@ -134,35 +154,61 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
   const uint32_t tS[2] = {tmem, tmem + 128};
-  const uint32_t tO = tmem + 256;
+  const uint32_t tOb[2] = {tmem + 256, tmem + 384};
 
   if (warp == 0) {
-    // ===================== TMA producer: Q, then the K ring =====================
+    // ===================== TMA producer: Q per item, then the K ring =====================
     // K_j is consumed by S_j only, so its stage is released as soon as S_j
     // completes and K runs ahead of V (separate ring, separate thread).
     if (lane == 0) {
-      mbar_arrive_expect_tx(&q_full, SM::kQ);
-      for (int c = 0; c < D / 64; ++c)
-        tma_load_2d(sQ + c * kChunkBytes, &tmQ, &q_full, head * D + c * 64, tok0 + q0, kEvictFirst);
-      for (int j = 0; j < nt; ++j) {
-        const int s = j & 1;
-        mbar_wait(&k_empty[s], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[s], SM::kK);
+      int kc = 0;
+      for (int ii = 0;; ++ii) {
+        const int v = atomicAdd(&g_attn_sched[0], 1);
+        const int it = v < n_items ? v : -1;
+        item_ring[ii & 7] = it;
+        mbar_arrive(&item_full[ii & 7]);
+        if (it < 0) {
+          // the last CTA out of work leaves the scheduler zeroed for the next launch
+          if (atomicAdd(&g_attn_sched[1], 1) == (int)gridDim.x - 1) {
+            g_attn_sched[0] = 0;
+            g_attn_sched[1] = 0;
+          }
+          break;
+        }
+        const AttnItem a = attn_item(it, S, n_q, n_kv, n_seqs, causal);
+        const int qb = ii & 1;
+        mbar_wait(&q_empty[qb], ((ii >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], SM::kQ);
         for (int c = 0; c < D / 64; ++c)
-          tma_load_2d(sK + s * SM::kK + c * kChunkBytes, &tmK, &k_full[s], kvh * D + c * 64, tok0 + j * BN,
-                      kEvictLast);
+          tma_load_2d(sQ + qb * SM::kQ + c * kChunkBytes, &tmQ, &q_full[qb], a.head * D + c * 64, a.tok0 + a.q0,
+                      kEvictFirst);
+        for (int j = 0; j < a.nt; ++j, ++kc) {
+          const int s = kc & 1;
+          mbar_wait(&k_empty[s], ((kc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[s], SM::kK);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_2d(sK + s * SM::kK + c * kChunkBytes, &tmK, &k_full[s], a.kvh * D + c * 64, a.tok0 + j * BN,
+                        kEvictLast);
+        }
       }
     }
   } else if (warp == 3) {
     // ===================== TMA producer: the V ring (released after PV_j) =====================
     if (lane == 0) {
-      for (int j = 0; j < nt; ++j) {
-        const int s = j & 1;
-        mbar_wait(&v_empty[s], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&v_full[s], SM::kV);
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_2d(sV + s * SM::kV + c * kChunkBytes, &tmV, &v_full[s], kvh * D + c * 64, tok0 + j * BN,
-                      kEvictLast);
+      int vc = 0;
+      for (int ii = 0;; ++ii) {
+        mbar_wait(&item_full[ii & 7], (ii >> 3) & 1);
+        const int it = item_ring[ii & 7];
+        if (it < 0) break;
+        const AttnItem a = attn_item(it, S, n_q, n_kv, n_seqs, causal);
+        for (int j = 0; j < a.nt; ++j, ++vc) {
+          const int s = vc & 1;
+          mbar_wait(&v_empty[s], ((vc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&v_full[s], SM::kV);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_2d(sV + s * SM::kV + c * kChunkBytes, &tmV, &v_full[s], a.kvh * D + c * 64, a.tok0 + j * BN,
+                        kEvictLast);
+        }
       }
     }
   } else if (warp == 1) {
@@ -170,151 +216,185 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t idS = make_idesc_bf16(BM, BN);
       const uint32_t idPV = make_idesc_bf16(BM, D) | (1u << 16);  // B (V) is MN-major
-      mbar_wait(&q_full, 0);
-      auto issue_pv = [&](int jp) {
-        const int bp = jp & 1;
-        mbar_wait(&v_full[jp & 1], (jp >> 1) & 1);
-        mbar_wait(&p_full[bp], (jp >> 1) & 1);
+      // PV of tile tcp (index jp inside its item) into O buffer ob; the last
+      // tile of an item also commits o_final[ob]
+      auto issue_pv = [&](int tcp, int jp, int ob, bool last) {
+        const int bp = tcp & 1;
+        mbar_wait(&v_full[bp], (tcp >> 1) & 1);
+        mbar_wait(&p_full[bp], (tcp >> 1) & 1);
         tc_fence_after();
-        const uint32_t vbase = smem_u32(sV + (jp & 1) * SM::kV);
+        const uint32_t vbase = smem_u32(sV + bp * SM::kV);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
-          // P_jp sits in its S buffer: warpgroup w's 64 keys packed into columns [w*64, w*64+32)
+          // P sits in its S buffer: warpgroup w's 64 keys packed into columns [w*64, w*64+32)
           const uint32_t ta = tS[bp] + (kk >> 2) * 64 + (kk & 3) * 8;
           const uint64_t db = make_sdesc_mn_sw128(vbase + kk * 16 * 128, kChunkBytes);
-          umma_bf16_ts(tO, ta, db, idPV, (jp | kk) != 0);
+          umma_bf16_ts(tOb[ob], ta, db, idPV, (jp | kk) != 0);
         }
         umma_commit(&o_done[bp]);
-        umma_commit(&v_empty[jp & 1]);
+        umma_commit(&v_empty[bp]);
+        if (last) umma_commit(&o_final[ob]);
       };
-      for (int j = 0; j < nt; ++j) {
-        const int s = j & 1;
-        mbar_wait(&k_full[s], (j >> 1) & 1);
+      // PV_j is issued after S_{j+1} (the next item's S_0 for an item's last
+      // tile); the first PV into an O buffer waits for the epilogue of the item
+      // two back to release it (o_free[ob] completes once per item)
+      int tc = 0;
+      int pend_tc = -1, pend_j = 0, pend_ii = 0;
+      bool pend_last = false;
+      auto issue_pend = [&]() {
+        const int pob = pend_ii & 1;
+        if (pend_j == 0) mbar_wait(&o_free[pob], ((pend_ii >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t qbase = smem_u32(sQ);
-        const uint32_t kbase = smem_u32(sK + s * SM::kK);
+        issue_pv(pend_tc, pend_j, pob, pend_last);
+      };
+      for (int ii = 0;; ++ii) {
+        mbar_wait(&item_full[ii & 7], (ii >> 3) & 1);
+        const int it = item_ring[ii & 7];
+        if (it < 0) break;
+        const AttnItem a = attn_item(it, S, n_q, n_kv, n_seqs, causal);
+        const int qb = ii & 1;
+        mbar_wait(&q_full[qb], (ii >> 1) & 1);
+        const uint32_t qbase = smem_u32(sQ + qb * SM::kQ);
+        for (int j = 0; j < a.nt; ++j, ++tc) {
+          const int s = tc & 1;
+          mbar_wait(&k_full[s], (tc >> 1) & 1);
+          tc_fence_after();
+          const uint32_t kbase = smem_u32(sK + s * SM::kK);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t da = make_sdesc_sw128(qbase + (kk >> 2) * kChunkBytes) + 2 * (kk & 3);
-          const uint64_t db = make_sdesc_sw128(kbase + (kk >> 2) * kChunkBytes) + 2 * (kk & 3);
-          umma_bf16_ss(tS[s], da, db, idS, kk != 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t da = make_sdesc_sw128(qbase + (kk >> 2) * kChunkBytes) + 2 * (kk & 3);
+            const uint64_t db = make_sdesc_sw128(kbase + (kk >> 2) * kChunkBytes) + 2 * (kk & 3);
+            umma_bf16_ss(tS[s], da, db, idS, kk != 0);
+          }
+          umma_commit(&s_full[s]);
+          umma_commit(&k_empty[s]);
+          if (j == a.nt - 1) umma_commit(&q_empty[qb]);  // last read of this item's Q
+          if (pend_tc >= 0) issue_pend();
+          pend_tc = tc;
+          pend_j = j;
+          pend_ii = ii;
+          pend_last = j == a.nt - 1;
         }
-        umma_commit(&s_full[s]);
-        umma_commit(&k_empty[s]);
-        if (j > 0) issue_pv(j - 1);
       }
-      issue_pv(nt - 1);
-      umma_commit(&o_final);
+      if (pend_tc >= 0) issue_pend();
     }
   } else if (warp >= 4) {
     // ===================== softmax + epilogue =====================
     // Two warpgroups split every S row: wg 0 owns key columns [0, 64), wg 1
     // [64, 128) (and the same halves of O); the row max is combined through
-    // smem with one named barrier per tile.  Two warps per SMSP hide the
-    // LDTM / MUFU latencies one warpgroup alone exposes.
+    // smem with one named barrier per tile.
     const int q = warp & 3;
     const int wg = (warp - 4) >> 2;
     const int r = q * 32 + lane;  // row inside the tile == TMEM lane
-    const int qi = q0 + r;        // query position inside the sequence
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     constexpr int HC = BN / 2;    // key columns per warpgroup
     constexpr int HD = D / 2;     // O columns per warpgroup
     const int c0 = wg * HC;
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < nt; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sv[HC];
-#pragma unroll
-      for (int c = 0; c < HC; c += 32) tmem_ld_x32(tS[b] + lane_off + c0 + c, sv + c);
-      tmem_ld_wait();
-      // mask (only tiles touching the diagonal / sequence end; branch-free
-      // select) + partial row max with 8 independent chains (raw scores)
-      const int key0 = j * BN + c0;
-      const bool need_mask = (j * BN + BN > kv_end) || (causal && j * BN + BN > q0);
-      if (need_mask) {
-        const int lim = causal ? min(S - key0, qi - key0 + 1) : (S - key0);  // keys [0, lim) valid
-#pragma unroll
-        for (int c = 0; c < HC; ++c) sv[c] = c < lim ? sv[c] : __float_as_uint(-INFINITY);
-      }
-      float pm[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) pm[i] = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < HC; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sv[c]));
-      const float mloc = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                               fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
-      red_max[j & 1][wg][r] = mloc;
-      named_bar_sync(1, 256);  // both warpgroups of this tile
-      const float mx = fmaxf(mloc, red_max[j & 1][wg ^ 1][r]) * scale_log2;
-      float alpha = 1.f;
-      if (mx > m_run + kRescaleThreshold || m_run == -INFINITY) {
-        alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mx);
-        m_run = mx;
-        l_run *= alpha;
-      }
-      const float msub = (m_run == -INFINITY) ? 0.f : m_run;
-      // P_j (bf16) overwrites this warpgroup's first 32 columns of its own S region
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[HC / 2];
-#pragma unroll
-      for (int c2 = 0; c2 < HC / 2; ++c2) {
-        // p = 2^(s*scale_log2 - m); half the pairs on the SFU, half on the FMA pipe
-        const float x0 = fmaf(__uint_as_float(sv[2 * c2]), scale_log2, -msub);
-        const float x1 = fmaf(__uint_as_float(sv[2 * c2 + 1]), scale_log2, -msub);
-        // (exp2_poly on the FMA pipe for half the pairs measured slower here: 459 vs 404 us)
-        const float p0 = fast_exp2(x0);
-        const float p1 = fast_exp2(x1);
-        ls[c2 & 3] += p0 + p1;
-        pk[c2] = pack_bf16x2(p0, p1);
-      }
-#pragma unroll
-      for (int c = 0; c < HC / 2; c += 16) tmem_st_x16(tS[b] + lane_off + c0 + c, pk + c);
-      l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-      // rescale this warpgroup's half of O in TMEM when the running max moved
-      const bool corr = (j > 0) && (alpha != 1.f);
-      if (__any_sync(0xffffffffu, corr)) {
-        mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+    int tc = 0;
+    for (int ii = 0;; ++ii) {
+        mbar_wait(&item_full[ii & 7], (ii >> 3) & 1);
+        const int it = item_ring[ii & 7];
+        if (it < 0) break;
+      const AttnItem a = attn_item(it, S, n_q, n_kv, n_seqs, causal);
+      const int ob = ii & 1;
+      const int qi = a.q0 + r;  // query position inside the sequence
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < a.nt; ++j, ++tc) {
+        const int b = tc & 1;
+        mbar_wait(&s_full[b], (tc >> 1) & 1);
         tc_fence_after();
+        uint32_t sv[HC];
 #pragma unroll
-        for (int c = 0; c < HD; c += 32) {
-          uint32_t ov[32];
-          tmem_ld_x32(tO + lane_off + wg * HD + c, ov);
-          tmem_ld_wait();
+        for (int c = 0; c < HC; c += 32) tmem_ld_x32(tS[b] + lane_off + c0 + c, sv + c);
+        tmem_ld_wait();
+        // mask (only tiles touching the diagonal / sequence end; branch-free
+        // select) + partial row max with 8 independent chains (raw scores)
+        const int key0 = j * BN + c0;
+        const bool need_mask = (j * BN + BN > a.kv_end) || (causal && j * BN + BN > a.q0);
+        if (need_mask) {
+          const int lim = causal ? min(S - key0, qi - key0 + 1) : (S - key0);  // keys [0, lim) valid
 #pragma unroll
-          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-          tmem_st_x32(tO + lane_off + wg * HD + c, ov);
+          for (int c = 0; c < HC; ++c) sv[c] = c < lim ? sv[c] : __float_as_uint(-INFINITY);
+        }
+        float pm[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pm[i] = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < HC; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sv[c]));
+        const float mloc = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                 fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+        red_max[b][wg][r] = mloc;
+        named_bar_sync(1, 256);  // both warpgroups of this tile
+        const float mx = fmaxf(mloc, red_max[b][wg ^ 1][r]) * scale_log2;
+        float alpha = 1.f;
+        if (mx > m_run + kRescaleThreshold || m_run == -INFINITY) {
+          alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mx);
+          m_run = mx;
+          l_run *= alpha;
+        }
+        const float msub = (m_run == -INFINITY) ? 0.f : m_run;
+        // P_j (bf16) overwrites this warpgroup's first 32 columns of its own S region
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[HC / 2];
+#pragma unroll
+        for (int c2 = 0; c2 < HC / 2; ++c2) {
+          const float x0 = fmaf(__uint_as_float(sv[2 * c2]), scale_log2, -msub);
+          const float x1 = fmaf(__uint_as_float(sv[2 * c2 + 1]), scale_log2, -msub);
+          // (a degree-3 FMA-pipe exp2 for 1/8..3/8 of the pairs measured 3-12 % slower)
+          const float p0 = fast_exp2(x0);
+          const float p1 = fast_exp2(x1);
+          ls[c2 & 3] += p0 + p1;
+          pk[c2] = pack_bf16x2(p0, p1);
+        }
+#pragma unroll
+        for (int c = 0; c < HC / 2; c += 16) tmem_st_x16(tS[b] + lane_off + c0 + c, pk + c);
+        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        // rescale this warpgroup's half of O in TMEM when the running max moved
+        const bool corr = (j > 0) && (alpha != 1.f);
+        if (__any_sync(0xffffffffu, corr)) {
+          mbar_wait(&o_done[(tc - 1) & 1], ((tc - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < HD; c += 32) {
+            uint32_t ov[32];
+            tmem_ld_x32(tOb[ob] + lane_off + wg * HD + c, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st_x32(tOb[ob] + lane_off + wg * HD + c, ov);
+          }
+          tmem_st_wait();
         }
         tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[b]);
       }
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&p_full[b]);
-    }
-    // epilogue: combine the two partial row sums, normalise this half of O
-    red_max[nt & 1][wg][r] = l_run;  // parity nt&1 is no longer read by the loop
-    mbar_wait(&o_final, 0);
-    tc_fence_after();
-    named_bar_sync(1, 256);
-    const float l_tot = red_max[nt & 1][0][r] + red_max[nt & 1][1][r];
-    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
-    __nv_bfloat16* orow = out + (int64_t)(tok0 + qi) * ldo + (int64_t)head * D + wg * HD;
+      // item epilogue: combine the two partial row sums, normalise this half of O
+      red_l[wg][r] = l_run;
+      mbar_wait(&o_final[ob], (ii >> 1) & 1);
+      tc_fence_after();
+      named_bar_sync(1, 256);
+      const float l_tot = red_l[0][r] + red_l[1][r];
+      const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
+      __nv_bfloat16* orow = out + (int64_t)(a.tok0 + qi) * ldo + (int64_t)a.head * D + wg * HD;
 #pragma unroll
-    for (int c = 0; c < HD; c += 32) {
-      uint32_t ov[32];
-      tmem_ld_x32(tO + lane_off + wg * HD + c, ov);
-      tmem_ld_wait();
-      if (qi < S) {
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t ov[32];
+        tmem_ld_x32(tOb[ob] + lane_off + wg * HD + c, ov);
+        tmem_ld_wait();
+        if (qi < S) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint32_t pk[4];
+          for (int i = 0; i < 32; i += 8) {
+            uint32_t pk[4];
 #pragma unroll
-          for (int k2 = 0; k2 < 4; ++k2)
-            pk[k2] = pack_bf16x2(__uint_as_float(ov[i + 2 * k2]) * inv, __uint_as_float(ov[i + 2 * k2 + 1]) * inv);
-          *reinterpret_cast<uint4*>(orow + c + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            for (int k2 = 0; k2 < 4; ++k2)
+              pk[k2] = pack_bf16x2(__uint_as_float(ov[i + 2 * k2]) * inv, __uint_as_float(ov[i + 2 * k2 + 1]) * inv);
+            *reinterpret_cast<uint4*>(orow + c + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&o_free[ob]);  // the MMA may overwrite this O buffer (item ii + 2)
     }
   }
   tc_fence_before();
@@ -340,9 +420,10 @@ static int launch(const void* q, int64_t ldq, const void* k, int64_t ldk, const 
     if (configure_smem((const void*)attn_tc_kernel<D>, Smem<D>::kTotal)) return HAP_ERR_LAUNCH;
     configured = 1;
   }
-  dim3 grid((unsigned)((S + BM - 1) / BM), (unsigned)n_q, (unsigned)n_seqs);
+  const int64_t n_items = ((S + BM - 1) / BM) * n_q * n_seqs;
+  const unsigned grid = (unsigned)(n_items < kNumSMs ? n_items : kNumSMs);
   { if (hap::launch_k(attn_tc_kernel<D>, dim3(grid), dim3(kThreads), Smem<D>::kTotal, st, mq, mk, mv, reinterpret_cast<__nv_bfloat16*>(out), ldo,
-                                                              (int)S, (int)n_q, (int)n_kv,
+                                                              (int)S, (int)n_q, (int)n_kv, (int)n_seqs,
                                                               scale * 1.4426950408889634f, causal) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
