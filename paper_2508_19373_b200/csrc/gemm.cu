@@ -648,7 +648,7 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cfg.numAttrs = (pdl_enabled() || (pdl_mode() == 2 && p.seg == nullptr)) ? 2 : 1;
   if (cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<kPair>, tmA, tmB, p) != cudaSuccess) return HAP_ERR_LAUNCH;
   HAP_CHECK_LAUNCH();
   return HAP_OK;

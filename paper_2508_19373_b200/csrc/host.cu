@@ -43,14 +43,15 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uin
 // 679 us vs 668 us without (scripts: 3 x 15 windows of 50 replays); the waiting
 // dependents' smem/TMEM reservations cost more than the launch gaps they hide.
 // HAP_PDL=1 turns it on for experiments.
-bool pdl_enabled() {
+int pdl_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HAP_PDL");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = e ? atoi(e) : 0;
   }
-  return v == 1;
+  return v;
 }
+bool pdl_enabled() { return pdl_mode() == 1; }
 
 int configure_smem(const void* kernel, int bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess ? 0 : -1;

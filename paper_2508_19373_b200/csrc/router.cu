@@ -220,6 +220,138 @@ __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* _
   finish_token<NE>(acc, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
 }
 
+// Large-T variant for NE <= 16 (Mixtral, tiny): CTA = 64 tokens x 8 h-ranges,
+// lane owns tokens (t0 + lane, t0 + lane + 32) of its warp's range.  Token rows
+// arrive by TMA (64-element x 64-row boxes, 128B swizzle, a 2-stage ring per
+// warp) instead of per-lane row-strided loads, and each 64-element chunk of the
+// router rows is converted to fp32 in smem once per warp, so a lane's inner
+// step is 2 swizzled 16-byte x loads + broadcast fp32 router loads + 2*NE*8
+// FMAs.  Every (token, expert, range) chain and the ordered sum of the range
+// partials are exactly those of router_kernel: logits are bit-identical.
+constexpr int kTB = 64;       // tokens per CTA
+constexpr int kCH = 64;       // elements per chunk (128 B rows)
+constexpr int kXStages = 2;
+constexpr int kXStageBytes = kTB * kCH * 2;  // 8 KB per warp-stage
+
+template <int NE>
+__global__ void __launch_bounds__(kThreads, 1)
+    router_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __nv_bfloat16* __restrict__ w, int T, int h,
+                      int n_rows_w, int E, int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx,
+                      float* __restrict__ topk_w, float* __restrict__ shared_gate, float* __restrict__ logits_out) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t bars[kRanges][kXStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* xs = dsm + warp * kXStages * kXStageBytes;
+  float* ws = reinterpret_cast<float*>(dsm + kRanges * kXStages * kXStageBytes) + warp * NE * kCH;
+  uint64_t* bar = bars[warp];
+  const int tb0 = blockIdx.x * kTB;
+  const int hr = h / kRanges, j0 = warp * hr, nch = hr / kCH;
+  if (lane == 0) {
+    for (int s2 = 0; s2 < kXStages; ++s2) mbar_init(&bar[s2], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  auto issue = [&](int c, int stage) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bar[stage], kXStageBytes);
+      tma_load_2d(xs + stage * kXStageBytes, &tmX, &bar[stage], j0 + c * kCH, tb0, kEvictFirst);
+    }
+  };
+  for (int c = 0; c < kXStages && c < nch; ++c) issue(c, c);
+
+  float acc[2][NE];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[i][e] = 0.f;
+  const int sw = lane & 7;  // 128B swizzle phase of rows lane and lane + 32
+  // router chunk c -> fp32 smem: lane handles items (lane, lane + 32) of the NE x 8 vectors;
+  // the next chunk's vectors are loaded into registers while the current one is consumed
+  constexpr int kWItems = (NE * (kCH / 8) + 31) / 32;
+  uint4 wreg[kWItems];
+  auto load_w = [&](int c) {
+#pragma unroll
+    for (int k2 = 0; k2 < kWItems; ++k2) {
+      const int it = lane + 32 * k2, e = it / (kCH / 8), v = it % (kCH / 8);
+      wreg[k2] = (it < NE * (kCH / 8) && e < n_rows_w)
+                     ? __ldg(reinterpret_cast<const uint4*>(w + (int64_t)e * h + j0 + c * kCH + v * 8))
+                     : make_uint4(0, 0, 0, 0);
+    }
+  };
+  auto store_w = [&]() {
+#pragma unroll
+    for (int k2 = 0; k2 < kWItems; ++k2) {
+      const int it = lane + 32 * k2, e = it / (kCH / 8), v = it % (kCH / 8);
+      if (it < NE * (kCH / 8)) {
+        const float2 a0 = unpack_bf16x2(wreg[k2].x), a1 = unpack_bf16x2(wreg[k2].y), a2 = unpack_bf16x2(wreg[k2].z),
+                     a3 = unpack_bf16x2(wreg[k2].w);
+        reinterpret_cast<float4*>(ws + e * kCH + v * 8)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
+        reinterpret_cast<float4*>(ws + e * kCH + v * 8)[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
+      }
+    }
+  };
+  load_w(0);
+  store_w();
+  for (int c = 0; c < nch; ++c) {
+    const int stage = c % kXStages;
+    if (c + 1 < nch) load_w(c + 1);
+    __syncwarp();  // router chunk c visible to every lane
+    mbar_wait(&bar[stage], (c / kXStages) & 1);
+    const uint8_t* xst = xs + stage * kXStageBytes;
+#pragma unroll 2
+    for (int v = 0; v < kCH / 8; ++v) {
+      float xf[2][8];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(xst + (lane + 32 * i) * 128 + ((v ^ sw) << 4));
+        const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = unpack_bf16x2(xw[q]);
+          xf[i][2 * q] = f.x;
+          xf[i][2 * q + 1] = f.y;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const float4 w0 = reinterpret_cast<const float4*>(ws + e * kCH + v * 8)[0];
+        const float4 w1 = reinterpret_cast<const float4*>(ws + e * kCH + v * 8)[1];
+        const float wf[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          acc[0][e] = __fmaf_rn(xf[0][q], wf[q], acc[0][e]);
+          acc[1][e] = __fmaf_rn(xf[1][q], wf[q], acc[1][e]);
+        }
+      }
+    }
+    __syncwarp();  // stage and router chunk consumed by every lane
+    if (c + kXStages < nch) issue(c + kXStages, stage);
+    if (c + 1 < nch) store_w();
+  }
+  __syncthreads();  // the partial table below overlays other warps' stages
+  float* part = reinterpret_cast<float*>(dsm);  // [kRanges][NE][kTB + 1]
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int e = 0; e < NE; ++e) part[(warp * NE + e) * (kTB + 1) + lane + 32 * i] = acc[i][e];
+  __syncthreads();
+  if (threadIdx.x >= kTB) return;
+  const int tl = threadIdx.x, t = tb0 + tl;
+  if (t >= T) return;
+  float tot[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    float s2 = part[e * (kTB + 1) + tl];
+#pragma unroll
+    for (int pp = 1; pp < kRanges; ++pp) s2 = __fadd_rn(s2, part[(pp * NE + e) * (kTB + 1) + tl]);
+    tot[e] = s2;
+  }
+  finish_token<NE>(tot, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
+}
+
 template <int NE>
 static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E, int64_t k, int renorm,
                   int has_shared, int32_t* idx, float* tw, float* sg, float* logits, cudaStream_t st) {
@@ -242,6 +374,24 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
         (int)(E + has_shared), (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
     HAP_CHECK_LAUNCH();
     return HAP_OK;
+  }
+  if constexpr (NE <= 16) {
+    if (h % (kRanges * kCH) == 0) {
+    constexpr int smem_tma = kRanges * kXStages * kXStageBytes + kRanges * NE * kCH * 4 + 1024;
+    static int configured_tma = 0;
+    if (!configured_tma) {
+      if (configure_smem((const void*)router_tma_kernel<NE>, smem_tma)) return HAP_ERR_LAUNCH;
+      configured_tma = 1;
+    }
+    CUtensorMap tmX;
+    if (!encode_tmap_2d_bf16(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, kCH, kTB, true))
+      return HAP_ERR_DRIVER;
+    { if (hap::launch_k(router_tma_kernel<NE>, dim3((unsigned)((T + kTB - 1) / kTB)), dim3(kThreads), smem_tma, st,
+          tmX, reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared), (int)E, (int)k,
+          renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
+    HAP_CHECK_LAUNCH();
+    return HAP_OK;
+    }
   }
   const int grid = (int)((T + 31) / 32);
   { if (hap::launch_k(router_kernel<NE>, dim3(grid), dim3(kThreads), smem, st, 
