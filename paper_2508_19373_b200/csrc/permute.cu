@@ -26,7 +26,7 @@ namespace permute {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kRowsPerBlock = 4096;
+constexpr int kRowsPerBlock = 512;  // 64 blocks at R = 32768 (latency-bound otherwise)
 constexpr int kMaxExperts = 512;
 
 struct Workspace {
