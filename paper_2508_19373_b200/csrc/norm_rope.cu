@@ -56,6 +56,61 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const uint4* __restri
   }
 }
 
+// Wide rows (h >= 2048): 128 threads per row, VPT 16-byte vectors per thread,
+// fp32 sum of squares reduced warp-then-block in a fixed order.  ~40 registers,
+// so 16 rows per SM are in flight (the warp-per-row kernel needs the whole row
+// in a lane's registers and is latency-bound at 1 CTA per SM).
+constexpr int kRowThreads = 128;
+template <int VPT>
+__global__ void __launch_bounds__(kRowThreads) rmsnorm_row_kernel(const uint4* __restrict__ x, int T, int hv, int ldxv,
+                                                                  const uint4* __restrict__ w, float eps,
+                                                                  uint4* __restrict__ out, int ldov) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[kRowThreads / 32];
+  const int row = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint4 v[VPT];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = tid + kRowThreads * i;
+    v[i] = c < hv ? __ldg(x + (int64_t)row * ldxv + c) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const uint32_t u[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16x2(u[j]);
+      ss = fmaf(f.x, f.x, ss);
+      ss = fmaf(f.y, f.y, ss);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) red[warp] = ss;
+  __syncthreads();
+  const float tot = (red[0] + red[1]) + (red[2] + red[3]);
+  const float inv = rsqrtf(tot / (float)(hv * 8) + eps);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = tid + kRowThreads * i;
+    if (c >= hv) break;
+    const uint4 wv = __ldg(w + c);
+    const uint32_t u[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+    const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16x2(u[j]);
+      const float2 g = unpack_bf16x2(ww[j]);
+      o[j] = pack_bf16x2(f.x * inv * g.x, f.y * inv * g.y);
+    }
+    out[(int64_t)row * ldov + c] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // One warp per (token, head) for the q and k heads; lane owns rotation pairs
 // (i, i + d/2) for i = lane, lane + 32 (d = 128) or i = lane (d = 64).
 __global__ void __launch_bounds__(kThreads) rope_kernel(__nv_bfloat16* __restrict__ qkv, int T, int64_t ld,
@@ -103,6 +158,21 @@ extern "C" int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, con
   const uint4* xv = reinterpret_cast<const uint4*>(x);
   const uint4* wv = reinterpret_cast<const uint4*>(w);
   uint4* ov = reinterpret_cast<uint4*>(out);
+  if (hv >= 2 * kRowThreads && hv <= 8 * kRowThreads) {
+    const int vpt = (hv + kRowThreads - 1) / kRowThreads;
+#define HAP_ROW_CASE(V)                                                                                          \
+  if (vpt <= V) {                                                                                               \
+    { if (hap::launch_k(rmsnorm_row_kernel<V>, dim3((unsigned)T), dim3(kRowThreads), 0, st, xv, (int)T, hv,    \
+                        (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8)) != cudaSuccess) return HAP_ERR_LAUNCH; } \
+    HAP_CHECK_LAUNCH();                                                                                         \
+    return HAP_OK;                                                                                              \
+  }
+    HAP_ROW_CASE(2)
+    HAP_ROW_CASE(4)
+    HAP_ROW_CASE(6)
+    HAP_ROW_CASE(8)
+#undef HAP_ROW_CASE
+  }
 #define HAP_NORM_CASE(V) \
   if (vpl <= V) { { if (hap::launch_k(rmsnorm_kernel<V>, dim3(grid), dim3(kThreads), 0, st, xv, (int)T, hv, (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8)) != cudaSuccess) return HAP_ERR_LAUNCH; } HAP_CHECK_LAUNCH(); return HAP_OK; }
   HAP_NORM_CASE(2)
