@@ -246,24 +246,49 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
   }
 }
 
-__global__ void decode_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_ml, int n_splits,
-                                    int n_q, int D, __nv_bfloat16* __restrict__ out, int64_t ldo) {
+// Warp per (sequence, query head): lanes hold the split statistics (m, l),
+// the max and the weighted denominator are warp reductions, and every lane
+// accumulates D/32 output columns over the splits with all partial loads of a
+// split in flight at once.  Splits with m = -inf (past the sequence) weigh 0.
+constexpr int kMergeWarps = 4;
+__global__ void __launch_bounds__(kMergeWarps * 32) decode_merge_kernel(const float* __restrict__ ws_o,
+                                                                        const float* __restrict__ ws_ml, int n_splits,
+                                                                        int n_q, int B, int D,
+                                                                        __nv_bfloat16* __restrict__ out, int64_t ldo) {
   pdl_trigger();
   pdl_wait();
-  const int hq = blockIdx.x, b = blockIdx.y;
-  const int64_t base = ((int64_t)b * n_q + hq) * n_splits;
+  const int lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kMergeWarps + (threadIdx.x >> 5);
+  if (item >= B * n_q) return;
+  const int b = item / n_q, hq = item - b * n_q;
+  const int64_t base = (int64_t)item * n_splits;  // == (b * n_q + hq) * n_splits
   float M = -INFINITY;
-  for (int s = 0; s < n_splits; ++s) M = fmaxf(M, ws_ml[(base + s) * 2]);
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    float num = 0.f, den = 0.f;
-    for (int s = 0; s < n_splits; ++s) {
-      const float m = ws_ml[(base + s) * 2];
+  for (int s2 = lane; s2 < n_splits; s2 += 32) M = fmaxf(M, ws_ml[(base + s2) * 2]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float den = 0.f;
+  for (int s2 = lane; s2 < n_splits; s2 += 32) {
+    const float m = ws_ml[(base + s2) * 2];
+    if (m != -INFINITY) den = fmaf(exp2f(m - M), ws_ml[(base + s2) * 2 + 1], den);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+  const float inv = den > 0.f ? 1.f / den : 0.f;
+  for (int d0 = lane * 4; d0 < D; d0 += 128) {
+    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int s2 = 0; s2 < n_splits; ++s2) {
+      const float m = ws_ml[(base + s2) * 2];  // same address in every lane
       if (m == -INFINITY) continue;
-      const float w = exp2f(m - M);
-      num = fmaf(w, ws_o[(base + s) * D + d], num);
-      den = fmaf(w, ws_ml[(base + s) * 2 + 1], den);
+      const float wgt = exp2f(m - M);
+      const float4 o4 = *reinterpret_cast<const float4*>(ws_o + (base + s2) * D + d0);
+      num.x = fmaf(wgt, o4.x, num.x);
+      num.y = fmaf(wgt, o4.y, num.y);
+      num.z = fmaf(wgt, o4.z, num.z);
+      num.w = fmaf(wgt, o4.w, num.w);
     }
-    out[(int64_t)b * ldo + (int64_t)hq * D + d] = __float2bfloat16_rn(den > 0.f ? num / den : 0.f);
+    __nv_bfloat16* orow = out + (int64_t)b * ldo + (int64_t)hq * D + d0;
+    *reinterpret_cast<uint2*>(orow) = make_uint2(pack_bf16x2(num.x * inv, num.y * inv), pack_bf16x2(num.z * inv, num.w * inv));
   }
 }
 
@@ -443,7 +468,7 @@ extern "C" int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, vo
   const int rc = head_dim == 128 ? launch_decode<128>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st)
                                  : launch_decode<64>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st);
   if (rc != HAP_OK) return rc;
-  { if (hap::launch_k(decode_merge_kernel, dim3(dim3((unsigned)n_q_heads, (unsigned)B)), dim3(128), 0, st, ws_o, ws_ml, ns, (int)n_q_heads, (int)head_dim,
+  { if (hap::launch_k(decode_merge_kernel, dim3((unsigned)((B * n_q_heads + kMergeWarps - 1) / kMergeWarps)), dim3(kMergeWarps * 32), 0, st, ws_o, ws_ml, ns, (int)n_q_heads, (int)B, (int)head_dim,
                                                                               reinterpret_cast<__nv_bfloat16*>(out), ldo) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;

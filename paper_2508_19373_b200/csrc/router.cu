@@ -24,6 +24,7 @@ namespace router {
 constexpr int kRanges = 8;              // == warps per CTA; fixed by the parity contract
 constexpr int kThreads = kRanges * 32;
 constexpr int kPrefetch = 4;
+constexpr int kSmallPrefetch = 16;  // router rows stream from L2: 16 x 16 B in flight per thread
 constexpr int kSmallT = 1024;         // <= this many tokens: one CTA per token
 
 // Softmax over the E routed logits, top-k on logits (strict '>' keeps the lower
@@ -109,16 +110,16 @@ __global__ void __launch_bounds__(kRanges * NE) router_small_kernel(const __nv_b
     const uint4* wr = reinterpret_cast<const uint4*>(w + (int64_t)e * h + p * hr);
     const uint4* xr = xs + p * (hr / 8);
     const int nv = hr / 8;
-    uint4 wb[kPrefetch];
+    uint4 wb[kSmallPrefetch];
 #pragma unroll
-    for (int i = 0; i < kPrefetch; ++i) wb[i] = i < nv ? __ldg(wr + i) : make_uint4(0, 0, 0, 0);
-    for (int v0 = 0; v0 < nv; v0 += kPrefetch) {
+    for (int i = 0; i < kSmallPrefetch; ++i) wb[i] = i < nv ? __ldg(wr + i) : make_uint4(0, 0, 0, 0);
+    for (int v0 = 0; v0 < nv; v0 += kSmallPrefetch) {
 #pragma unroll
-      for (int i = 0; i < kPrefetch; ++i) {
+      for (int i = 0; i < kSmallPrefetch; ++i) {
         const int v = v0 + i;
         if (v >= nv) break;
         const uint4 wv = wb[i];
-        if (v + kPrefetch < nv) wb[i] = __ldg(wr + v + kPrefetch);
+        if (v + kSmallPrefetch < nv) wb[i] = __ldg(wr + v + kSmallPrefetch);
         const uint4 xv = xr[v];
         const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
         const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
