@@ -117,6 +117,32 @@ int hap_gemm_qkv_rope_ex(const void* A, int64_t M, int64_t lda, int64_t K, const
                          int64_t head_dim, float theta, void* workspace, size_t ws_bytes, void* stream);
 
 /*
+ * EP combine over peer memory: hap_grouped_gemm_bf16 with HAP_EPI_STORE whose
+ * output rows are scattered per segment: row r of segment s (rows
+ * [seg[s], seg[s+1]) of A) is stored at
+ *     (bf16*)seg_dst[s] + (r - seg[s] + seg_dst_row0[s]) * ldc
+ * seg_dst (device int64[n_segs]) holds device addresses — in the executor the
+ * peer-mapped (CUDA IPC) output buffers of the ranks the rows came from, so the
+ * down-projection epilogue writes each expert output straight back to its
+ * source rank over NVLink (the combine all-to-all of strategies.py:334-338,
+ * fused into the GEMM).  No bias / residual / split-K.
+ */
+int hap_grouped_gemm_bf16_scatter(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                                  int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
+                                  const int32_t* seg_group, const int64_t* seg_dst, const int32_t* seg_dst_row0,
+                                  int64_t ldc, void* stream);
+
+/*
+ * EP dispatch over peer memory: rows [seg[s], seg[s+1]) of src (bf16 [*, h],
+ * contiguous) are copied to (bf16*)dst_base[s] + (dst_row0[s] + i) * ldd,
+ * dst_base holding (peer-mapped) device addresses (the dispatch all-to-all of
+ * strategies.py:334-338 as direct NVLink stores).  rows_max bounds seg[n_segs]
+ * (grid sizing only); seg, dst_base, dst_row0 are device arrays.
+ */
+int hap_peer_copy_rows(const void* src, int64_t rows_max, int64_t h, const int32_t* seg, int64_t n_segs,
+                       const int64_t* dst_base, const int64_t* dst_row0, int64_t ldd, void* stream);
+
+/*
  * Router: logits[t,e] = x[t,:] . w[e,:] in fp32 with a FIXED reduction
  * order — h is cut into 8 equal contiguous ranges; in range p the partial is
  * the sequential chain acc = fma(x[t,j], w[e,j], acc) (bf16*bf16 products are

@@ -58,6 +58,15 @@ SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
          c_int64, c_int64, c_float, c_void_p, c_size_t, c_void_p],
     ),
+    "hap_grouped_gemm_bf16_scatter": (
+        ctypes.c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+         c_void_p, c_void_p, c_int64, c_void_p],
+    ),
+    "hap_peer_copy_rows": (
+        ctypes.c_int,
+        [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p],
+    ),
     "hap_router_topk": (
         ctypes.c_int,
         [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int32, c_int32, c_void_p, c_void_p,

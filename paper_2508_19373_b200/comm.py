@@ -60,6 +60,10 @@ class Comm:
     def _g(self, kind):
         return self.groups[kind][1]
 
+    def barrier(self, kind: str) -> None:
+        if self.size(kind) > 1:
+            dist.barrier(group=self._g(kind))
+
     # All ops are no-ops on singleton groups.
     def all_reduce(self, t: torch.Tensor, kind: str) -> torch.Tensor:
         if self.size(kind) > 1:

@@ -70,6 +70,11 @@ struct Params {
   // epilogue — deterministic, no atomics.
   int32_t ksplit;
   float* part;
+  // scatter epilogue (EP combine over peer memory): row r of segment s is
+  // stored at seg_dst[s] + (r - seg[s] + seg_dst_row0[s]) * ldc, seg_dst[s]
+  // being a (possibly peer-mapped) device address; NULL = C
+  const int64_t* seg_dst;
+  const int32_t* seg_dst_row0;
 };
 
 constexpr int kEpiRope = 2;     // internal epilogue id (hap_gemm_qkv_rope)
@@ -78,7 +83,7 @@ constexpr size_t kSplitWorkspaceBytes = (size_t)32 << 20;
 constexpr int64_t kRasterL2Bytes = 48ll << 20;  // A rows of one raster group kept L2-resident across n-blocks
 
 struct TileCoord {
-  int32_t g, m0, m_end, n_blk;
+  int32_t g, s, m0, m_end, n_blk;  // weight group, segment, rows [m0, m_end), n block
 };
 
 // Map a linear tile index to (segment's weight group, row range, n block).
@@ -104,6 +109,7 @@ __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, 
   const int r = local - grp * group_m * n_blocks;
   TileCoord c;
   c.g = seg_group[g];
+  c.s = g;
   c.m0 = seg[g] + (g0 + r % gsz) * TM;
   c.m_end = seg[g + 1];
   c.n_blk = r / gsz;
@@ -300,7 +306,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = c.m0 + (int)crank * BM + q * 32 + lane;
       const bool row_ok = row < c.m_end;
       const uint32_t t_row = tmem_base + acc * kAccCols + ((uint32_t)(q * 32) << 16);
-      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+      __nv_bfloat16* crow =
+          p.seg_dst ? reinterpret_cast<__nv_bfloat16*>(p.seg_dst[c.s]) +
+                          (int64_t)(row - seg_s[c.s] + p.seg_dst_row0[c.s]) * p.ldc
+                    : p.C + (int64_t)row * p.ldc;
       bool do_epi = true;
       if (ksplit > 1) {
         // tcgen05.ld is warp-collective: every lane loads, stores are predicated
@@ -755,6 +764,36 @@ extern "C" int hap_grouped_gemm_bf16_ex(const void* A, int64_t a_rows, int64_t l
   }
 
   return hap::gemm::launch(p, A, a_rows, lda, K, B, n_groups, N, n_segs, workspace, ws_bytes, stream);
+}
+
+extern "C" int hap_grouped_gemm_bf16_scatter(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                                             int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
+                                             const int32_t* seg_group, const int64_t* seg_dst,
+                                             const int32_t* seg_dst_row0, int64_t ldc, void* stream) {
+  using namespace hap::gemm;
+  if (!A || !B || !seg || !seg_dst || !seg_dst_row0 || a_rows < 0 || K <= 0 || N <= 0 || n_groups <= 0)
+    return HAP_ERR_INVALID_ARG;
+  if (n_segs <= 0 || n_segs > kMaxSegs) return HAP_ERR_INVALID_ARG;
+  if (!seg_group && n_segs != n_groups) return HAP_ERR_INVALID_ARG;
+  if (a_rows > INT32_MAX || N * n_groups > INT32_MAX || K > INT32_MAX) return HAP_ERR_UNSUPPORTED;
+  if (K % 8 || lda % 8 || ldc % 8 || N % 8 || lda < K || ldc < N) return HAP_ERR_MISALIGNED;
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return HAP_ERR_MISALIGNED;
+  if (a_rows == 0) return HAP_OK;
+  Params p{};
+  p.a_rows = (int32_t)a_rows;
+  p.K = (int32_t)K;
+  p.N = (int32_t)N;
+  p.n_segs = (int32_t)n_segs;
+  p.seg = seg;
+  p.seg_group = seg_group;
+  p.epi = HAP_EPI_STORE;
+  p.BN = pick_bn(N);
+  p.out_cols = (int32_t)N;
+  p.ldc = ldc;
+  p.seg_dst = seg_dst;
+  p.seg_dst_row0 = seg_dst_row0;
+  // no split-K workspace: the slice reduce writes through C only
+  return hap::gemm::launch(p, A, a_rows, lda, K, B, n_groups, N, n_segs, nullptr, 0, stream);
 }
 
 extern "C" int hap_grouped_gemm_bf16(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,

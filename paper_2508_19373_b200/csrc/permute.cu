@@ -213,6 +213,40 @@ __global__ void __launch_bounds__(kThreads) combine_kernel(const uint4* __restri
   }
 }
 
+// EP dispatch over peer memory: rows [seg[s], seg[s+1]) of src go to
+// dst_base[s] + (dst_row0[s] + i) * ldd (dst_base[s] may be a peer-mapped
+// address, so the stores travel over NVLink).  One warp per row, 16-byte
+// vectors, 4 in flight per lane.
+__global__ void __launch_bounds__(kThreads) peer_copy_kernel(const uint4* __restrict__ src, int hv, int n_segs,
+                                                             const int32_t* __restrict__ seg,
+                                                             const int64_t* __restrict__ dst_base,
+                                                             const int64_t* __restrict__ dst_row0, int64_t lddv) {
+  pdl_trigger();
+  pdl_wait();
+  const int warp_global = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_warps = (gridDim.x * kThreads) >> 5;
+  const int R = seg[n_segs];
+  for (int r = warp_global; r < R; r += n_warps) {
+    int lo = 0, hi = n_segs - 1;  // segment of row r: last s with seg[s] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (seg[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const uint4* in = src + (int64_t)r * hv;
+    uint4* out = reinterpret_cast<uint4*>(dst_base[lo]) + (dst_row0[lo] + (r - seg[lo])) * lddv;
+    int i = lane;
+    for (; i + 96 < hv; i += 128) {
+      const uint4 a = __ldg(in + i), b = __ldg(in + i + 32), c = __ldg(in + i + 64), d = __ldg(in + i + 96);
+      out[i] = a;
+      out[i + 32] = b;
+      out[i + 64] = c;
+      out[i + 96] = d;
+    }
+    for (; i < hv; i += 32) out[i] = __ldg(in + i);
+  }
+}
+
 }  // namespace permute
 }  // namespace hap
 
@@ -279,6 +313,20 @@ extern "C" int hap_moe_combine(const void* y, const int32_t* dst_of_row, const f
                                             (int)(h / 8), reinterpret_cast<const uint4*>(residual), (int)res_row0,
                                             (int)res_rows, reinterpret_cast<const uint4*>(shared_y), shared_gate,
                                             reinterpret_cast<uint4*>(out)) != cudaSuccess) return HAP_ERR_LAUNCH; }
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
+}
+
+extern "C" int hap_peer_copy_rows(const void* src, int64_t rows_max, int64_t h, const int32_t* seg, int64_t n_segs,
+                                  const int64_t* dst_base, const int64_t* dst_row0, int64_t ldd, void* stream) {
+  if (!src || !seg || !dst_base || !dst_row0 || rows_max < 0 || h <= 0 || n_segs <= 0) return HAP_ERR_INVALID_ARG;
+  if (h % 8 || ldd % 8 || ldd < h || (reinterpret_cast<uintptr_t>(src) & 15)) return HAP_ERR_MISALIGNED;
+  if (rows_max == 0) return HAP_OK;
+  int grid = (int)((rows_max * 32 + kThreads - 1) / kThreads);
+  if (grid > 148 * 16) grid = 148 * 16;
+  { if (hap::launch_k(peer_copy_kernel, dim3(grid), dim3(kThreads), 0, reinterpret_cast<cudaStream_t>(stream),
+                      reinterpret_cast<const uint4*>(src), (int)(h / 8), (int)n_segs, seg, dst_base, dst_row0,
+                      ldd / 8) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }

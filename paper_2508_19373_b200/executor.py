@@ -38,6 +38,14 @@ from .weights import RankWeights, pack_rank_weights, synthetic_weights
 BF16 = torch.bfloat16
 
 
+def _ep_peer_default() -> bool:
+    """EP dispatch/combine through peer-mapped buffers (HAP_EP_PEER=1) instead of
+    NCCL all-to-alls; opt-in until measured on a multi-GPU box."""
+    import os
+
+    return os.environ.get("HAP_EP_PEER", "0") == "1"
+
+
 class CudaOps:
     """The product compute backend: every method launches a kernel of
     libhap_kernels.so through the C-ABI (ops.py).  Construction fails loudly
@@ -61,6 +69,8 @@ class CudaOps:
     router_topk = staticmethod(K.router_topk)
     moe_permute = staticmethod(K.moe_permute)
     moe_combine = staticmethod(K.moe_combine)
+    grouped_gemm_scatter = staticmethod(K.grouped_gemm_scatter)
+    peer_copy_rows = staticmethod(K.peer_copy_rows)
     permute_workspace_bytes = staticmethod(K.permute_workspace_bytes)
     attn_decode_workspace_bytes = staticmethod(K.attn_decode_workspace_bytes)
 
@@ -105,6 +115,7 @@ class HapMoEBlock:
         self.last_routing = None  # (topk_idx, dst_of_row, seg) of the last expert call, for parity tests
         self.capture = None       # set to {} to keep references to intermediates (tests only)
         self.timers = None        # set to {} to record CUDA events around the expert GEMMs (bench)
+        self.ep_peer = _ep_peer_default()
 
     @classmethod
     def from_rank_weights(cls, cfg: BlockConfig, deg: PlanDegrees, rank: int, w: RankWeights, *, device=None,
@@ -120,6 +131,7 @@ class HapMoEBlock:
         blk.last_routing = None
         blk.capture = None
         blk.timers = None
+        blk.ep_peer = _ep_peer_default()
         return blk
 
     @classmethod
@@ -359,6 +371,8 @@ class HapMoEBlock:
             Y = torch.empty(R, h, device=dev, dtype=BF16)
             with self._timed("down"):
                 ops.grouped_gemm(H, w.w2, E, seg, Y)
+        elif self.ep_peer:
+            Y = self._ep_experts_peer(x_perm, seg)
         else:
             Y = self._ep_experts(x_perm, seg)
         ys = None
@@ -400,6 +414,79 @@ class HapMoEBlock:
                 ops.grouped_gemm(H, w.w2, El, seg_r, Y_r, seg_group=grp)
         Y = torch.empty(x_perm.shape[0], h, device=dev, dtype=BF16)
         comm.all_to_all(Y, Y_r, send, recv, "a2a_group")
+        return Y
+
+
+    # ------------------------------------------------ EP over peer memory --
+    def _peer_buffers(self, recv_rows: int, y_rows: int):
+        """Symmetric receive / expert-output buffers on the EP group, (re)allocated
+        collectively when a call needs more rows (every rank derives the same
+        sizes from the same count matrix, so the decision is identical)."""
+        from .peer import PeerBuffer
+
+        bufs = getattr(self, "_peer", None)
+        if bufs is not None and bufs[0].rows >= recv_rows and bufs[1].rows >= y_rows:
+            return bufs
+        grow = lambda need, cur: max(need, int(cur * 1.25)) if cur else need  # noqa: E731
+        rr = grow(recv_rows, bufs[0].rows if bufs else 0)
+        yr = grow(y_rows, bufs[1].rows if bufs else 0)
+        ranks = self.comm.groups["a2a_group"][0]
+        g = self.comm._g("a2a_group")
+        h = self.cfg.hidden
+        self._peer = (PeerBuffer(max(rr, 1), h, BF16, self.device, g, ranks),
+                      PeerBuffer(max(yr, 1), h, BF16, self.device, g, ranks))
+        return self._peer
+
+    def _ep_experts_peer(self, x_perm, seg):
+        """EP dispatch -> local grouped GEMMs -> combine with both all-to-alls done
+        as direct stores into peer-mapped buffers: hap_peer_copy_rows writes each
+        rank's rows into the owning rank's receive buffer, and the down GEMM's
+        scatter epilogue writes every expert output back into its source rank's
+        output buffer.  Same row layouts as _ep_experts (received rows in
+        (source rank, local expert) blocks), so the results are identical."""
+        w, ops, comm = self.w, self.ops, self.comm
+        dev = self.device
+        ep, El, h = self.deg.e_ep, w.n_experts_local, self.cfg.hidden
+        E = ep * El
+        me = comm.index("a2a_group")
+        counts = (seg[1:] - seg[:-1]).contiguous()
+        allc = torch.empty(ep * E, device=dev, dtype=torch.int32)
+        comm.all_gather(allc, counts, "a2a_group")
+        C = allc.view(ep, E).cpu().to(torch.int64)          # C[s][e]: rows of source s for global expert e
+        # receive layout at destination d: blocks (s, j) in lexicographic order
+        blk = C.view(ep, ep, El).permute(1, 0, 2)            # [d][s][j]
+        off = torch.zeros(ep, ep * El + 1, dtype=torch.int64)
+        off[:, 1:] = torch.cumsum(blk.reshape(ep, ep * El), 1)
+        n_recv_all = off[:, -1]
+        src_prefix = torch.zeros(ep, E + 1, dtype=torch.int64)
+        src_prefix[:, 1:] = torch.cumsum(C, 1)               # each source's x_perm segment offsets
+        recv_buf, y_buf = self._peer_buffers(int(n_recv_all.max()), int(src_prefix[:, -1].max()))
+        # dispatch: my rows of global expert e go to rank e // El at block (me, e % El)
+        e_ids = torch.arange(E)
+        d_of_e = e_ids // El
+        dst_base = torch.tensor([recv_buf.ptrs[int(d)] for d in d_of_e], dtype=torch.int64)
+        dst_row0 = off[d_of_e, me * El + e_ids % El]
+        ops.peer_copy_rows(x_perm, seg, dst_base.to(dev), dst_row0.to(dev), h)
+        torch.cuda.current_stream().synchronize()
+        comm.barrier("a2a_group")                            # every rank's rows have landed
+        n_recv = int(n_recv_all[me])
+        Y = y_buf.local[:x_perm.shape[0]]
+        if n_recv:
+            seg_r = off[me].to(torch.int32).to(dev)
+            grp = torch.arange(El, dtype=torch.int32).repeat(ep).to(dev)
+            H = torch.empty(n_recv, w.inter_local, device=dev, dtype=BF16)
+            x_recv = recv_buf.local[:n_recv]
+            with self._timed("gate_up"):
+                ops.grouped_gemm(x_recv, w.w13, El, seg_r, H, swiglu_half=w.hw, seg_group=grp)
+            # combine: block (s, j) goes back to source s at its segment of expert me*El + j
+            s_ids = torch.arange(ep).repeat_interleave(El)
+            j_ids = torch.arange(El).repeat(ep)
+            seg_dst = torch.tensor([y_buf.ptrs[int(s)] for s in s_ids], dtype=torch.int64).to(dev)
+            seg_dst_row0 = src_prefix[s_ids, me * El + j_ids].to(torch.int32).to(dev)
+            with self._timed("down"):
+                ops.grouped_gemm_scatter(H, w.w2, El, seg_r, grp, seg_dst, seg_dst_row0, h)
+        torch.cuda.current_stream().synchronize()
+        comm.barrier("a2a_group")                            # every expert output is back at its source
         return Y
 
 

@@ -117,6 +117,44 @@ def grouped_gemm(a: torch.Tensor, b: torch.Tensor, n_groups: int, seg: Optional[
     return out
 
 
+def grouped_gemm_scatter(a: torch.Tensor, b: torch.Tensor, n_groups: int, seg: torch.Tensor,
+                         seg_group: Optional[torch.Tensor], seg_dst: torch.Tensor, seg_dst_row0: torch.Tensor,
+                         ldc: int) -> None:
+    """Grouped GEMM (store epilogue) whose rows of segment s land at
+    seg_dst[s] + (r - seg[s] + seg_dst_row0[s]) * ldc (device addresses, e.g.
+    peer-mapped buffers): the EP combine fused into the down projection."""
+    lib = _lib.load()
+    _need(a, "a", BF16); _need(b, "b", BF16); _rowmajor(a, "a")
+    _need(seg, "seg", torch.int32); _need(seg_dst, "seg_dst", torch.int64); _need(seg_dst_row0, "seg_dst_row0", torch.int32)
+    K = a.shape[1]
+    b2 = b.reshape(-1, b.shape[-1])
+    N = b2.shape[0] // n_groups
+    n_segs = seg.numel() - 1
+    if seg_dst.numel() != n_segs or seg_dst_row0.numel() != n_segs:
+        raise ValueError("seg_dst / seg_dst_row0 need one entry per segment")
+    if seg_group is not None:
+        _need(seg_group, "seg_group", torch.int32)
+    st = lib.hap_grouped_gemm_bf16_scatter(a.data_ptr(), a.shape[0], a.stride(0), K, b2.data_ptr(), n_groups, N,
+                                           seg.data_ptr(), n_segs, _ptr(seg_group), seg_dst.data_ptr(),
+                                           seg_dst_row0.data_ptr(), ldc, _stream())
+    check(st, "hap_grouped_gemm_bf16_scatter")
+    _count(1 if a.shape[0] else 0)
+
+
+def peer_copy_rows(src: torch.Tensor, seg: torch.Tensor, dst_base: torch.Tensor, dst_row0: torch.Tensor,
+                   ldd: int) -> None:
+    """Copy the row segments of src to (peer) addresses dst_base[s] + (dst_row0[s] + i) * ldd."""
+    lib = _lib.load()
+    _need(src, "src", BF16); _rowmajor(src, "src")
+    if src.stride(0) != src.shape[1]:
+        raise ValueError("src must be contiguous")
+    _need(seg, "seg", torch.int32); _need(dst_base, "dst_base", torch.int64); _need(dst_row0, "dst_row0", torch.int64)
+    st = lib.hap_peer_copy_rows(src.data_ptr(), src.shape[0], src.shape[1], seg.data_ptr(), seg.numel() - 1,
+                                dst_base.data_ptr(), dst_row0.data_ptr(), ldd, _stream())
+    check(st, "hap_peer_copy_rows")
+    _count(1 if src.shape[0] else 0)
+
+
 def gemm(a: torch.Tensor, w: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None, residual=None,
          swiglu_half: int = 0) -> torch.Tensor:
     """Dense a @ w^T (nn.Linear layout) on the tcgen05 kernel."""
