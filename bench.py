@@ -507,6 +507,8 @@ def main():
             "clocks": clocks, "peaks": peaks,
         }
         print(json.dumps(line), flush=True)
+    for b in blocks.values():
+        b.close()
     barrier()
     import torch.distributed as dist
 

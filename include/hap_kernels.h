@@ -46,6 +46,11 @@ typedef enum {
 #define HAP_EPI_SWIGLU 1 /* C = silu(acc[:, gate]) * acc[:, up] per tile        */
 
 const char* hap_status_string(int status);
+
+/* Enable peer access from the current device to peer_device (NVLink P2P) so
+ * kernels can store through CUDA-IPC mappings of that device's buffers.
+ * Idempotent; HAP_ERR_UNSUPPORTED when the pair has no P2P path. */
+int hap_enable_peer_access(int peer_device);
 int hap_abi_version(void);
 
 /* Largest SwiGLU tile half-width (multiple of 8, <= 128) dividing `inter_dim`;

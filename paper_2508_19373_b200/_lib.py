@@ -36,6 +36,7 @@ HAP_EPI_SWIGLU = 1
 SIGNATURES = {
     "hap_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "hap_abi_version": (ctypes.c_int, []),
+    "hap_enable_peer_access": (ctypes.c_int, [ctypes.c_int]),
     "hap_swiglu_half_width": (c_int64, [c_int64]),
     "hap_grouped_gemm_bf16": (
         ctypes.c_int,

@@ -59,6 +59,23 @@ int configure_smem(const void* kernel, int bytes) {
 
 }  // namespace hap
 
+// Peer mappings of CUDA-IPC buffers are opened by the owner's device guard;
+// kernels on this device write through them only with peer access enabled
+// from the current device (NVLink P2P).  Idempotent.
+extern "C" int hap_enable_peer_access(int peer_device) {
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return HAP_ERR_LAUNCH;
+  if (peer_device == cur) return HAP_OK;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, cur, peer_device) != cudaSuccess || !can) return HAP_ERR_UNSUPPORTED;
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free error state
+    return HAP_OK;
+  }
+  return e == cudaSuccess ? HAP_OK : HAP_ERR_LAUNCH;
+}
+
 extern "C" const char* hap_status_string(int status) {
   switch (status) {
     case HAP_OK: return "ok";

@@ -417,6 +417,12 @@ class HapMoEBlock:
         return Y
 
 
+    def close(self) -> None:
+        """Release peer mappings (every rank, before a barrier and shutdown)."""
+        for b in getattr(self, "_peer", None) or ():
+            b.close()
+        self._peer = None
+
     # ------------------------------------------------ EP over peer memory --
     def _peer_buffers(self, recv_rows: int, y_rows: int):
         """Symmetric receive / expert-output buffers on the EP group, (re)allocated

@@ -34,6 +34,12 @@ class PeerBuffer:
         self.views = []
         for r, f, a in objs:
             self.views.append(self.local if r == me else f(*a))
+        from . import _lib
+
+        lib = _lib.load()
+        for v in self.views:  # stores from this device go straight over NVLink
+            if v.device != self.local.device:
+                _lib.check(lib.hap_enable_peer_access(v.device.index), "hap_enable_peer_access")
         self.ptrs = [v.data_ptr() for v in self.views]  # group order
 
     def __len__(self):

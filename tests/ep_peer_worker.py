@@ -38,8 +38,7 @@ def main(rank, world, port, cfg_kw, plan, out_path):
         outs = [blk.forward(x[s0 * S:s1 * S].contiguous(), "prefill", B, S) for _ in range(2)]
         torch.cuda.synchronize()
         res[peer] = [o.cpu() for o in outs]
-        for b in getattr(blk, "_peer", None) or ():
-            b.close()
+        blk.close()
         dist.barrier()
     # the peer path must reproduce the all-to-all path exactly (same rows, same GEMMs), twice in a row
     ok = all(torch.equal(a, b) for a, b in zip(res[False], res[True])) and torch.equal(res[True][0], res[True][1])
