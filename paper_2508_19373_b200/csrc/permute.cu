@@ -45,7 +45,8 @@ static size_t ws_bytes(int64_t R, int64_t E, int64_t* nb_out) {
 
 __global__ void __launch_bounds__(kThreads) rank_kernel(const int32_t* __restrict__ eid, int R, int E,
                                                         int32_t* __restrict__ local_rank,
-                                                        int32_t* __restrict__ block_counts) {
+                                                        int32_t* __restrict__ block_counts,
+                                                        int32_t* __restrict__ block_base, int32_t* __restrict__ seg) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ int32_t sm[];
@@ -85,6 +86,16 @@ __global__ void __launch_bounds__(kThreads) rank_kernel(const int32_t* __restric
     __syncthreads();
   }
   for (int i = threadIdx.x; i < E; i += kThreads) block_counts[(int64_t)blockIdx.x * E + i] = running[i];
+  if (gridDim.x == 1 && threadIdx.x == 0) {
+    // a single block (decode-sized R): the scan is the prefix of its own counts
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      seg[e] = acc;
+      block_base[e] = acc;
+      acc += running[e];
+    }
+    seg[E] = acc;
+  }
 }
 
 __global__ void scan_kernel(const int32_t* __restrict__ block_counts, int NB, int E, int32_t* __restrict__ block_base,
@@ -282,8 +293,10 @@ extern "C" int hap_moe_permute(const int32_t* expert_of_row, int64_t R, int64_t 
     return HAP_OK;
   }
   const int smem = (int)((1 + kWarps) * E * sizeof(int32_t));
-  { if (hap::launch_k(rank_kernel, dim3((int)nb), dim3(kThreads), smem, st, expert_of_row, (int)R, E, local_rank, block_counts) != cudaSuccess) return HAP_ERR_LAUNCH; }
-  { if (hap::launch_k(scan_kernel, dim3(1), dim3(256), 0, st, block_counts, (int)nb, E, block_base, seg) != cudaSuccess) return HAP_ERR_LAUNCH; }
+  { if (hap::launch_k(rank_kernel, dim3((int)nb), dim3(kThreads), smem, st, expert_of_row, (int)R, E, local_rank, block_counts, block_base, seg) != cudaSuccess) return HAP_ERR_LAUNCH; }
+  if (nb > 1) {  // one block computes the prefix itself
+    { if (hap::launch_k(scan_kernel, dim3(1), dim3(256), 0, st, block_counts, (int)nb, E, block_base, seg) != cudaSuccess) return HAP_ERR_LAUNCH; }
+  }
   const int64_t warps_needed = R;
   int grid = (int)((warps_needed * 32 + kThreads - 1) / kThreads);
   if (grid > 148 * 16) grid = 148 * 16;

@@ -224,7 +224,7 @@ def moe_permute(expert_of_row: torch.Tensor, n_experts: int, x: Optional[torch.T
                              dst_of_row.data_ptr(), seg.data_ptr(), workspace.data_ptr(),
                              workspace.numel() * workspace.element_size(), _stream())
     check(st, "hap_moe_permute")
-    _count(3 if R else 0)
+    _count((3 if R > 512 else 2) if R else 0)  # rank (+ scan when > 1 block of 512 rows) + scatter
 
 
 def moe_combine(y: torch.Tensor, dst_of_row: torch.Tensor, topk_w: torch.Tensor, T: int, k: int,
