@@ -225,7 +225,7 @@ def bench_decode(block, cfg, steps, warmup):
     loop keeps the contract's K)."""
     x, cache, pos = make_decode_state(block, cfg)
     steps, warmup = max(steps, DECODE_MIN_STEPS), max(warmup, 20)
-    if block.lay.n == 1 and block.deg.e_ep == 1:
+    if block.graph_capturable():
         g, _ = block.capture_graph(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos)
         return time_loop(g.replay, steps, warmup), "cuda_graph"
     return time_loop(lambda: block.forward(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos), steps,

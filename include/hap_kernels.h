@@ -148,6 +148,26 @@ int hap_peer_copy_rows(const void* src, int64_t rows_max, int64_t h, const int32
                        const int64_t* dst_base, const int64_t* dst_row0, int64_t ldd, void* stream);
 
 /*
+ * One-shot all-reduce (sum) of n bf16 elements over peer-mapped memory for
+ * decode-size messages.  Each rank owns a symmetric region data (2 * n_max
+ * bf16, double-buffered by call parity) and sig (hap_peer_allreduce_sig_bytes
+ * int32 flags, zeroed once on every rank before the first call), and a local
+ * epoch array (n_ctas int32, zeroed once).  All arrays of addresses are device
+ * int64[n_ranks]: in_ptrs / out_ptrs / epoch_ptrs are read at the entries of
+ * the ranks this launch plays (rank0 .. rank0 + ranks_in_launch - 1; a
+ * multi-GPU rank plays itself, ranks_in_launch = 1), data_ptrs / sig_ptrs hold
+ * every rank's (peer-mapped) region.  Sum in rank order in fp32, one bf16
+ * rounding: every rank gets identical bytes.  in == out is allowed.  No host
+ * synchronisation (CUDA-graph capturable); every rank must use the same n_ctas.
+ * Replaces: the AllReduce rows of comm_volume (strategies.py:314-322, 341-342)
+ * on the decode path.
+ */
+size_t hap_peer_allreduce_sig_bytes(int32_t n_ranks, int32_t n_ctas);
+int hap_peer_allreduce_bf16(const int64_t* in_ptrs, const int64_t* out_ptrs, const int64_t* epoch_ptrs,
+                            const int64_t* data_ptrs, const int64_t* sig_ptrs, int64_t n, int64_t n_max,
+                            int32_t n_ranks, int32_t rank0, int32_t ranks_in_launch, int32_t n_ctas, void* stream);
+
+/*
  * Router: logits[t,e] = x[t,:] . w[e,:] in fp32 with a FIXED reduction
  * order — h is cut into 8 equal contiguous ranges; in range p the partial is
  * the sequential chain acc = fma(x[t,j], w[e,j], acc) (bf16*bf16 products are

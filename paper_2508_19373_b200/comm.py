@@ -60,12 +60,30 @@ class Comm:
     def _g(self, kind):
         return self.groups[kind][1]
 
+    def enable_peer_allreduce(self, kinds, n_max: int = 1 << 20) -> None:
+        """Route all-reduces of bf16 tensors up to n_max elements on these groups
+        through the one-shot peer-memory kernel (peer.PeerAllReduce)."""
+        from .peer import PeerAllReduce
+
+        if not hasattr(self, "peer_ar"):
+            self.peer_ar = {}
+        for kind in kinds:
+            if self.size(kind) > 1 and kind not in self.peer_ar:
+                self.peer_ar[kind] = PeerAllReduce(n_max, torch.device("cuda", torch.cuda.current_device()),
+                                                   self._g(kind), self.groups[kind][0])
+
+    def uses_peer_allreduce(self, kind: str) -> bool:
+        return kind in getattr(self, "peer_ar", {})
+
     def barrier(self, kind: str) -> None:
         if self.size(kind) > 1:
             dist.barrier(group=self._g(kind))
 
     # All ops are no-ops on singleton groups.
     def all_reduce(self, t: torch.Tensor, kind: str) -> torch.Tensor:
+        par = getattr(self, "peer_ar", {}).get(kind)
+        if par is not None and par.fits(t):
+            return par(t)
         if self.size(kind) > 1:
             if self.staged and t.is_cuda:
                 h = t.cpu()

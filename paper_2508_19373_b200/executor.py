@@ -38,6 +38,16 @@ from .weights import RankWeights, pack_rank_weights, synthetic_weights
 BF16 = torch.bfloat16
 
 
+def _maybe_peer_allreduce(comm) -> None:
+    """HAP_PEER_AR=1: decode-size all-reduces of this block's groups go through the
+    one-shot peer-memory kernel (graph capturable); opt-in until measured on a
+    multi-GPU box."""
+    import os
+
+    if comm is not None and comm.lay.n > 1 and os.environ.get("HAP_PEER_AR", "0") == "1":
+        comm.enable_peer_allreduce(["attn_tp_group", "exp_tp_group"])
+
+
 def _ep_peer_default() -> bool:
     """EP dispatch/combine through peer-mapped buffers (HAP_EP_PEER=1) instead of
     NCCL all-to-alls; opt-in until measured on a multi-GPU box."""
@@ -112,6 +122,7 @@ class HapMoEBlock:
         self.w: RankWeights = pack_rank_weights(cfg, full, self.lay)
         del full
         self.comm = comm if comm is not None else (Comm(self.lay) if self.lay.n > 1 else None)
+        _maybe_peer_allreduce(self.comm)
         self.last_routing = None  # (topk_idx, dst_of_row, seg) of the last expert call, for parity tests
         self.capture = None       # set to {} to keep references to intermediates (tests only)
         self.timers = None        # set to {} to record CUDA events around the expert GEMMs (bench)
@@ -128,6 +139,7 @@ class HapMoEBlock:
         blk.device = torch.device(device) if device is not None else w.w13.device
         blk.w = w
         blk.comm = comm if comm is not None else (Comm(blk.lay) if blk.lay.n > 1 else None)
+        _maybe_peer_allreduce(blk.comm)
         blk.last_routing = None
         blk.capture = None
         blk.timers = None
@@ -255,8 +267,8 @@ class HapMoEBlock:
         (graph, out_static).  Replaying the graph re-runs every kernel of the
         block with no host work (decode is launch-bound otherwise).  Only for
         plans without host synchronisation (no EP count exchange) on one GPU."""
-        if self.deg.e_ep > 1 or self.lay.n > 1:
-            raise RuntimeError("graph capture is supported for single-device, non-EP plans")
+        if not self.graph_capturable():
+            raise RuntimeError("graph capture needs one device, or a non-EP plan on peer all-reduces (HAP_PEER_AR=1)")
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
@@ -333,6 +345,9 @@ class HapMoEBlock:
         y = self._experts(hn_s, residual, res_row0=lay.e_tp_rank * c, res_rows=c)
 
         # ---------------- back to the attention layout
+        if self._peer_allreduce_back(y):
+            # pure TP: RS + AG over one group == one all-reduce, done one-shot over peer memory
+            return self.comm.all_reduce(y, "attn_tp_group")[:T_real]
         if self.deg.e_tp > 1:
             chunk = torch.empty(c, h, device=dev, dtype=BF16)
             self.comm.reduce_scatter(chunk, y, "exp_tp_group")
@@ -344,6 +359,23 @@ class HapMoEBlock:
         else:
             out = chunk
         return out[:T_real]
+
+    def _peer_allreduce_back(self, y) -> bool:
+        c = self.comm
+        return (c is not None and self.deg.e_tp > 1 and self.deg.a_tp == self.deg.e_tp
+                and c.groups["exp_tp_group"][0] == c.groups["attn_tp_group"][0]
+                and c.uses_peer_allreduce("attn_tp_group") and c.peer_ar["attn_tp_group"].fits(y))
+
+    def graph_capturable(self) -> bool:
+        """True when a forward issues no host synchronisation and no NCCL call:
+        one device, or a non-EP plan whose collectives all run through the
+        one-shot peer all-reduce (HAP_PEER_AR=1)."""
+        if self.lay.n == 1:
+            return True
+        c = self.comm
+        return (self.deg.e_ep == 1 and self.lay.n_shards == self.deg.a_dp and c is not None
+                and all(c.size(k) == 1 or c.uses_peer_allreduce(k) for k in ("attn_tp_group", "exp_tp_group"))
+                and c.size("gather_group") == 1)
 
     def _experts(self, hn_s, residual, res_row0, res_rows):
         cfg, w, lay, ops = self.cfg, self.w, self.lay, self.ops
@@ -422,6 +454,8 @@ class HapMoEBlock:
         for b in getattr(self, "_peer", None) or ():
             b.close()
         self._peer = None
+        for par in getattr(self.comm, "peer_ar", {}).values():
+            par.close()
 
     # ------------------------------------------------ EP over peer memory --
     def _peer_buffers(self, recv_rows: int, y_rows: int):

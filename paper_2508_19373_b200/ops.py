@@ -155,6 +155,21 @@ def peer_copy_rows(src: torch.Tensor, seg: torch.Tensor, dst_base: torch.Tensor,
     _count(1 if src.shape[0] else 0)
 
 
+def peer_allreduce(in_ptrs: torch.Tensor, out_ptrs: torch.Tensor, epoch_ptrs: torch.Tensor, data_ptrs: torch.Tensor,
+                   sig_ptrs: torch.Tensor, n: int, n_max: int, n_ranks: int, rank0: int, ranks_in_launch: int,
+                   n_ctas: int) -> None:
+    """One-shot all-reduce over peer-mapped memory (tables of device addresses, see hap_kernels.h)."""
+    lib = _lib.load()
+    for t, name in ((in_ptrs, "in_ptrs"), (out_ptrs, "out_ptrs"), (epoch_ptrs, "epoch_ptrs"),
+                    (data_ptrs, "data_ptrs"), (sig_ptrs, "sig_ptrs")):
+        _need(t, name, torch.int64)
+    st = lib.hap_peer_allreduce_bf16(in_ptrs.data_ptr(), out_ptrs.data_ptr(), epoch_ptrs.data_ptr(),
+                                     data_ptrs.data_ptr(), sig_ptrs.data_ptr(), n, n_max, n_ranks, rank0,
+                                     ranks_in_launch, n_ctas, _stream())
+    check(st, "hap_peer_allreduce_bf16")
+    _count(1 if n else 0)
+
+
 def gemm(a: torch.Tensor, w: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None, residual=None,
          swiglu_half: int = 0) -> torch.Tensor:
     """Dense a @ w^T (nn.Linear layout) on the tcgen05 kernel."""

@@ -49,3 +49,48 @@ class PeerBuffer:
         """Drop the peer mappings (call on every rank before a barrier, ahead of shutdown)."""
         self.views = [self.local]
         self.ptrs = []
+
+
+class PeerAllReduce:
+    """One-shot all-reduce over a process group through peer-mapped memory
+    (hap_peer_allreduce_bf16): symmetric data (2 x n_max bf16) and flag regions,
+    a local epoch per CTA, and device tables of addresses.  The per-call input
+    address is written into the table by a fill kernel, so the call is
+    CUDA-graph capturable (no host synchronisation, no NCCL)."""
+
+    def __init__(self, n_max: int, device, group, group_ranks: List[int], n_ctas: int = 32):
+        from . import _lib
+
+        if n_max % 8:
+            raise ValueError("n_max must be a multiple of 8")
+        self.n_max, self.n_ctas = n_max, n_ctas
+        self.n = len(group_ranks)
+        self.me = group_ranks.index(dist.get_rank())
+        sig_elems = int(_lib.load().hap_peer_allreduce_sig_bytes(self.n, n_ctas)) // 4
+        self.data = PeerBuffer(2, n_max, torch.bfloat16, device, group, group_ranks)
+        self.sig = PeerBuffer(1, sig_elems, torch.int32, device, group, group_ranks)
+        self.sig.local.zero_()
+        self.epoch = torch.zeros(n_ctas, dtype=torch.int32, device=device)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # every rank's flags are zero before anyone publishes
+        dev = self.epoch.device
+        self.data_tab = torch.tensor(self.data.ptrs, dtype=torch.int64, device=dev)
+        self.sig_tab = torch.tensor(self.sig.ptrs, dtype=torch.int64, device=dev)
+        self.epoch_tab = torch.zeros(self.n, dtype=torch.int64, device=dev)
+        self.epoch_tab[self.me] = self.epoch.data_ptr()
+        self.io_tab = torch.zeros(self.n, dtype=torch.int64, device=dev)
+
+    def fits(self, t: torch.Tensor) -> bool:
+        return t.dtype == torch.bfloat16 and t.is_contiguous() and t.numel() % 8 == 0 and t.numel() <= self.n_max
+
+    def __call__(self, t: torch.Tensor) -> torch.Tensor:
+        from . import ops
+
+        self.io_tab[self.me].fill_(t.data_ptr())
+        ops.peer_allreduce(self.io_tab, self.io_tab, self.epoch_tab, self.data_tab, self.sig_tab, t.numel(),
+                           self.n_max, self.n, self.me, 1, self.n_ctas)
+        return t
+
+    def close(self) -> None:
+        self.data.close()
+        self.sig.close()
