@@ -456,26 +456,15 @@ def main():
     x_loc = local_slice(x_global, blk, PREFILL_BATCH, PREFILL_SEQ)
     x_host = x_loc.cpu().pin_memory()
     out_host = torch.empty_like(x_host).pin_memory()
-    x_dev = torch.empty_like(x_loc)
-    n_loc = x_loc.shape[0] // PREFILL_SEQ
 
-    if world == 1:
-        # streamed host I/O: sequence chunks, H2D/D2H overlapped with compute (HapMoEBlock.forward_host)
-        # every step copies its input from pinned host memory and its output back;
-        # forward_host double-buffers across steps (H2D of step i+1 and D2H of
-        # step i-1 overlap step i's forward), the way a serving loop streams batches
-        def e2e_step():
-            blk.forward_host(x_host, out_host, n_loc, PREFILL_SEQ)
-        e2e_finish = blk.host_sync
-        api = ("paper_2508_19373_b200.executor.HapMoEBlock.forward_host (pinned host in/out every step; "
-               "H2D(i+1) and D2H(i-1) overlap forward(i); the timed region ends after the last D2H)")
-    else:
-        def e2e_step():
-            x_dev.copy_(x_host, non_blocking=True)
-            o = blk.forward(x_dev, "prefill", PREFILL_BATCH, PREFILL_SEQ)
-            out_host.copy_(o, non_blocking=True)
-        api = "paper_2508_19373_b200.executor.HapMoEBlock.forward (H2D -> block -> D2H)"
-        e2e_finish = None
+    # every step copies its input from pinned host memory and its output back;
+    # forward_host double-buffers across steps (H2D of step i+1 and D2H of
+    # step i-1 overlap step i's forward), the way a serving loop streams batches
+    def e2e_step():
+        blk.forward_host(x_host, out_host, PREFILL_BATCH, PREFILL_SEQ)
+    e2e_finish = blk.host_sync
+    api = ("paper_2508_19373_b200.executor.HapMoEBlock.forward_host (pinned host in/out every step; "
+           "H2D(i+1) and D2H(i-1) overlap forward(i); the timed region ends after the last D2H)")
 
     e2e_ms = time_loop(e2e_step, args.steps, args.warmup, finish=e2e_finish)
     h2d = x_host.numel() * 2 * world

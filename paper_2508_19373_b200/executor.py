@@ -211,16 +211,18 @@ class HapMoEBlock:
         ``host_sync()`` + a stream synchronisation.  With n_chunks > 1 the batch
         is additionally split into sequence chunks inside the call (sequences
         are independent in the block, so the output equals one forward over the
-        whole batch).  Single-device plans only."""
-        if self.lay.n > 1:
-            raise RuntimeError("forward_host streams batches on one device; use forward() under a multi-GPU plan")
+        whole batch; single-device plans).  Under a multi-GPU plan, ``batch`` is
+        the global batch and x_host this rank's replica rows, as for forward()."""
+        if self.lay.n > 1 and n_chunks != 1:
+            raise RuntimeError("sequence chunking is single-device; under a multi-GPU plan use n_chunks=1")
         if not (x_host.is_pinned() and out_host.is_pinned()):
             raise ValueError("host buffers must be pinned for asynchronous copies")
         n_chunks = max(1, min(n_chunks, batch))
         while batch % n_chunks:
             n_chunks -= 1
+        # forward() takes the global batch; x_host holds this rank's replica rows
         bc = batch // n_chunks
-        rows = bc * seq_len
+        rows = x_host.shape[0] // n_chunks
         st = getattr(self, "_host", None)
         if st is None or st["rows"] != rows or st["n_chunks"] != n_chunks:
             st = {"rows": rows, "n_chunks": n_chunks, "i": 0,
