@@ -290,6 +290,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int HC = BN / 2;    // key columns per warpgroup
     constexpr int HD = D / 2;     // O columns per warpgroup
     const int c0 = wg * HC;
+    // item epilogue: combine the two partial row sums, normalise this half of O,
+    // store, release the O buffer to the MMA (item ii + 2 reuses it)
+    auto epilogue = [&](int eii, const AttnItem& ea, float el) {
+      const int ob = eii & 1;
+      const int qi = ea.q0 + r;
+      red_l[wg][r] = el;
+      mbar_wait(&o_final[ob], (eii >> 1) & 1);
+      tc_fence_after();
+      named_bar_sync(1, 256);
+      const float l_tot = red_l[0][r] + red_l[1][r];
+      const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
+      __nv_bfloat16* orow = out + (int64_t)(ea.tok0 + qi) * ldo + (int64_t)ea.head * D + wg * HD;
+#pragma unroll
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t ov[32];
+        tmem_ld_x32(tOb[ob] + lane_off + wg * HD + c, ov);
+        tmem_ld_wait();
+        if (qi < S) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2)
+              pk[k2] = pack_bf16x2(__uint_as_float(ov[i + 2 * k2]) * inv, __uint_as_float(ov[i + 2 * k2 + 1]) * inv);
+            *reinterpret_cast<uint4*>(orow + c + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&o_free[ob]);
+    };
+    int pend_ii = -1;
+    AttnItem pend_a{};
+    float pend_l = 0.f;
     int tc = 0;
     for (int ii = 0;; ++ii) {
         mbar_wait(&item_full[ii & 7], (ii >> 3) & 1);
@@ -369,33 +403,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&p_full[b]);
       }
-      // item epilogue: combine the two partial row sums, normalise this half of O
-      red_l[wg][r] = l_run;
-      mbar_wait(&o_final[ob], (ii >> 1) & 1);
-      tc_fence_after();
-      named_bar_sync(1, 256);
-      const float l_tot = red_l[0][r] + red_l[1][r];
-      const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
-      __nv_bfloat16* orow = out + (int64_t)(a.tok0 + qi) * ldo + (int64_t)a.head * D + wg * HD;
-#pragma unroll
-      for (int c = 0; c < HD; c += 32) {
-        uint32_t ov[32];
-        tmem_ld_x32(tOb[ob] + lane_off + wg * HD + c, ov);
-        tmem_ld_wait();
-        if (qi < S) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int k2 = 0; k2 < 4; ++k2)
-              pk[k2] = pack_bf16x2(__uint_as_float(ov[i + 2 * k2]) * inv, __uint_as_float(ov[i + 2 * k2 + 1]) * inv);
-            *reinterpret_cast<uint4*>(orow + c + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&o_free[ob]);  // the MMA may overwrite this O buffer (item ii + 2)
+      // the epilogue of the previous item runs now, one item late: its last PV
+      // (issued behind this item's S_0) finished long ago, so the softmax warps
+      // never idle on o_final; O is double-buffered, so this item's PVs are
+      // unaffected
+      if (pend_ii >= 0) epilogue(pend_ii, pend_a, pend_l);
+      pend_ii = ii;
+      pend_a = a;
+      pend_l = l_run;
     }
+    if (pend_ii >= 0) epilogue(pend_ii, pend_a, pend_l);
   }
   tc_fence_before();
   __syncthreads();
