@@ -229,18 +229,18 @@ __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* _
 // step is 2 swizzled 16-byte x loads + broadcast fp32 router loads + 2*NE*8
 // FMAs.  Every (token, expert, range) chain and the ordered sum of the range
 // partials are exactly those of router_kernel: logits are bit-identical.
-constexpr int kTB = 64;       // tokens per CTA
 constexpr int kCH = 64;       // elements per chunk (128 B rows)
 constexpr int kXStages = 2;
-constexpr int kXStageBytes = kTB * kCH * 2;  // 8 KB per warp-stage
 
-template <int NE>
+template <int NE, int TPL>
 __global__ void __launch_bounds__(kThreads, 1)
     router_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __nv_bfloat16* __restrict__ w, int T, int h,
                       int n_rows_w, int E, int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx,
                       float* __restrict__ topk_w, float* __restrict__ shared_gate, float* __restrict__ logits_out) {
   pdl_trigger();
   pdl_wait();
+  constexpr int kTB = 32 * TPL;                   // tokens per CTA
+  constexpr int kXStageBytes = kTB * kCH * 2;     // per warp-stage
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t bars[kRanges][kXStages];
@@ -263,9 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   for (int c = 0; c < kXStages && c < nch; ++c) issue(c, c);
 
-  float acc[2][NE];
+  float acc[TPL][NE];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < TPL; ++i)
 #pragma unroll
     for (int e = 0; e < NE; ++e) acc[i][e] = 0.f;
   const int sw = lane & 7;  // 128B swizzle phase of rows lane and lane + 32
@@ -304,9 +304,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint8_t* xst = xs + stage * kXStageBytes;
 #pragma unroll 2
     for (int v = 0; v < kCH / 8; ++v) {
-      float xf[2][8];
+      float xf[TPL][8];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < TPL; ++i) {
         const uint4 xv = *reinterpret_cast<const uint4*>(xst + (lane + 32 * i) * 128 + ((v ^ sw) << 4));
         const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
@@ -323,8 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float wf[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          acc[0][e] = __fmaf_rn(xf[0][q], wf[q], acc[0][e]);
-          acc[1][e] = __fmaf_rn(xf[1][q], wf[q], acc[1][e]);
+#pragma unroll
+          for (int i = 0; i < TPL; ++i) acc[i][e] = __fmaf_rn(xf[i][q], wf[q], acc[i][e]);
         }
       }
     }
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();  // the partial table below overlays other warps' stages
   float* part = reinterpret_cast<float*>(dsm);  // [kRanges][NE][kTB + 1]
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < TPL; ++i)
 #pragma unroll
     for (int e = 0; e < NE; ++e) part[(warp * NE + e) * (kTB + 1) + lane + 32 * i] = acc[i][e];
   __syncthreads();
@@ -376,22 +376,26 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
     HAP_CHECK_LAUNCH();
     return HAP_OK;
   }
-  if constexpr (NE <= 16) {
+  {
+    // TMA-staged variant: 2 tokens per lane while 2*NE accumulators fit, else 1
+    constexpr int TPL = NE <= 16 ? 2 : 1;
+    constexpr int kTB = 32 * TPL;
+    constexpr int smem_tma = kRanges * kXStages * kTB * kCH * 2 + kRanges * NE * kCH * 4 + 1024;
+    static_assert(smem_tma <= 227 * 1024, "router smem");
     if (h % (kRanges * kCH) == 0) {
-    constexpr int smem_tma = kRanges * kXStages * kXStageBytes + kRanges * NE * kCH * 4 + 1024;
-    static int configured_tma = 0;
-    if (!configured_tma) {
-      if (configure_smem((const void*)router_tma_kernel<NE>, smem_tma)) return HAP_ERR_LAUNCH;
-      configured_tma = 1;
-    }
-    CUtensorMap tmX;
-    if (!encode_tmap_2d_bf16(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, kCH, kTB, true))
-      return HAP_ERR_DRIVER;
-    { if (hap::launch_k(router_tma_kernel<NE>, dim3((unsigned)((T + kTB - 1) / kTB)), dim3(kThreads), smem_tma, st,
-          tmX, reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared), (int)E, (int)k,
-          renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
-    HAP_CHECK_LAUNCH();
-    return HAP_OK;
+      static int configured_tma = 0;
+      if (!configured_tma) {
+        if (configure_smem((const void*)router_tma_kernel<NE, TPL>, smem_tma)) return HAP_ERR_LAUNCH;
+        configured_tma = 1;
+      }
+      CUtensorMap tmX;
+      if (!encode_tmap_2d_bf16(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, kCH, kTB, true))
+        return HAP_ERR_DRIVER;
+      { if (hap::launch_k(router_tma_kernel<NE, TPL>, dim3((unsigned)((T + kTB - 1) / kTB)), dim3(kThreads), smem_tma,
+                          st, tmX, reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared),
+                          (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
+      HAP_CHECK_LAUNCH();
+      return HAP_OK;
     }
   }
   const int grid = (int)((T + 31) / 32);
