@@ -81,6 +81,61 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const uint8_t* __rest
   }
 }
 
+// Fast path (group_size % 32 == 0, n % 32 == 0, 16-byte aligned codes): a
+// thread expands 16 packed bytes (32 elements of one group) per step — one
+// 16-byte load, one scale/zero pair, 4 x 16-byte bf16 stores (or 16 x 16-byte
+// fp64 stores) — with two steps in flight, so the kernel streams at HBM rate
+// instead of issuing 4-byte loads one at a time.
+template <bool kBf16>
+__global__ void __launch_bounds__(kThreads) dequant32_kernel(const uint4* __restrict__ codes,
+                                                             const double* __restrict__ scales,
+                                                             const double* __restrict__ zeros, int64_t group_size,
+                                                             int64_t n32, void* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t v0 = (int64_t)blockIdx.x * kThreads + threadIdx.x; v0 < n32; v0 += 2 * stride) {
+    uint4 pk[2];
+    double sc[2], zp[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t v = v0 + u * stride;
+      if (v < n32) {
+        pk[u] = __ldcs(codes + v);
+        const int64_t g = v * 32 / group_size;
+        sc[u] = __ldg(scales + g);
+        zp[u] = __ldg(zeros + g);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t v = v0 + u * stride;
+      if (v >= n32) break;
+      const uint32_t words[4] = {pk[u].x, pk[u].y, pk[u].z, pk[u].w};
+#pragma unroll
+      for (int wq = 0; wq < 4; ++wq) {
+        double val[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          val[i] = __dadd_rn(__dmul_rn((double)((words[wq] >> (4 * i)) & 0xF), sc[u]), zp[u]);
+        if (kBf16) {
+          uint32_t w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            __nv_bfloat162 p2 = __floats2bfloat162_rn((float)val[2 * i], (float)val[2 * i + 1]);
+            w[i] = *reinterpret_cast<uint32_t*>(&p2);
+          }
+          __stcs(reinterpret_cast<uint4*>(out) + v * 4 + wq, make_uint4(w[0], w[1], w[2], w[3]));
+        } else {
+          double2* o = reinterpret_cast<double2*>(out) + (v * 32 + wq * 8) / 2;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) __stcs(o + i, make_double2(val[2 * i], val[2 * i + 1]));
+        }
+      }
+    }
+  }
+}
+
 }  // namespace quant
 }  // namespace hap
 
@@ -90,6 +145,19 @@ extern "C" int hap_int4_dequant(const uint8_t* codes, const double* scales, cons
   if (!codes || !scales || !zero_points || !out || group_size < 1 || n < 0) return HAP_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(codes) & 3) || (reinterpret_cast<uintptr_t>(out) & 15)) return HAP_ERR_MISALIGNED;
   if (n == 0) return HAP_OK;
+  if (group_size % 32 == 0 && n % 32 == 0 && (reinterpret_cast<uintptr_t>(codes) & 15) == 0) {
+    const int64_t n32 = n / 32;
+    int64_t g32 = (n32 + 2 * kThreads - 1) / (2 * kThreads);
+    if (g32 > 148 * 16) g32 = 148 * 16;
+    cudaStream_t st32 = reinterpret_cast<cudaStream_t>(stream);
+    const uint4* c4 = reinterpret_cast<const uint4*>(codes);
+    if (out_bf16)
+      { if (hap::launch_k(dequant32_kernel<true>, dim3((int)g32), dim3(kThreads), 0, st32, c4, scales, zero_points, group_size, n32, out) != cudaSuccess) return HAP_ERR_LAUNCH; }
+    else
+      { if (hap::launch_k(dequant32_kernel<false>, dim3((int)g32), dim3(kThreads), 0, st32, c4, scales, zero_points, group_size, n32, out) != cudaSuccess) return HAP_ERR_LAUNCH; }
+    HAP_CHECK_LAUNCH();
+    return HAP_OK;
+  }
   const int64_t n8 = (n + 7) / 8;
   int64_t grid = (n8 + kThreads - 1) / kThreads;
   if (grid > 148 * 32) grid = 148 * 32;
