@@ -396,6 +396,25 @@ def main():
     total_launches = K.LAUNCHES[0] - launches0
     clocks = sampler.stop()
 
+    # -- whole-block roofline per plan: the reference's FLOP model (arch.py:145-178)
+    # with the causal half of the score/value term removed, over N GPUs at the
+    # measured dense bf16 peak
+    from paper_2508_19373_b200.config import import_moeplan
+
+    mpl = import_moeplan()
+    spec = cfg.to_model_spec()
+    T_pf = PREFILL_BATCH * PREFILL_SEQ
+    f_attn = mpl.attention_flops(spec, T_pf, PREFILL_SEQ)
+    f_useful = f_attn - 2 * T_pf * PREFILL_SEQ * cfg.hidden + mpl.expert_flops(spec, T_pf)
+    roof_ms = f_useful / (world * peaks["bf16_tflops"] * 1e12) * 1e3
+    for r in results.values():
+        r["roofline_ms"] = roof_ms
+        r["frac_of_roofline"] = roof_ms / r["prefill_ms"]
+    roofline_block = {"flops_per_step": f_useful, "peak_tflops_per_gpu": peaks["bf16_tflops"], "n_gpus": world,
+                      "ms": roof_ms, "frac": roof_ms / results["hap"]["prefill_ms"],
+                      "convention": "attention_flops + expert_flops (reference arch.py:145-178), causal score/value "
+                                    "term halved; measured burst bf16 peak"}
+
     # -- roofline of the dominant kernel (expert gate/up grouped GEMM), live CUDA events
     blk = get_block(hap_p)
     blk.timers = {}
@@ -489,7 +508,7 @@ def main():
                        "planner": f"moeplan solve_ilp (reference ILP) on {plan_src}",
                        "planner_ms": plan_ms,
                        "l2": "no flush: every step streams > L2 (2.8 GB expert weights + 128 MB activations)"},
-            "plans": results, "decode": decode, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "plans": results, "decode": decode, "roofline": roofline, "roofline_block": roofline_block, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": TIMED_LAUNCHES.get(f"prefill:{hap_p.degrees.label()}"),
             "gpu_launches_note": "kernels of libhap_kernels.so launched in the headline timed region (this rank)",
             "gpu_launches_all_bench_loops": total_launches,
