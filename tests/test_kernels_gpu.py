@@ -319,7 +319,9 @@ def test_rope(d):
 
 
 # ------------------------------------------------------------- attention --
-@pytest.mark.parametrize("d,nq,nkv,S,B", [(128, 8, 2, 200, 2), (64, 8, 2, 128, 4), (128, 4, 4, 1000, 1)])
+@pytest.mark.parametrize("d,nq,nkv,S,B", [(128, 8, 2, 200, 2), (64, 8, 2, 128, 4), (128, 4, 4, 1000, 1),
+                                           (128, 16, 2, 2048, 2),   # G = 8, 512 items: dynamic scheduler
+                                           (64, 8, 1, 777, 3)])     # G = 8, d = 64, ragged tail tiles
 def test_attn_prefill(d, nq, nkv, S, B):
     T = B * S
     qkv = bf16((T, (nq + 2 * nkv) * d), seed=18)
@@ -337,7 +339,8 @@ def test_attn_prefill(d, nq, nkv, S, B):
     assert rel_err(np32(out), np.concatenate(ref)) < 2e-2
 
 
-@pytest.mark.parametrize("d,nq,nkv", [(128, 32, 8), (64, 8, 2), (128, 28, 4), (128, 16, 16)])
+@pytest.mark.parametrize("d,nq,nkv", [(128, 32, 8), (64, 8, 2), (128, 28, 4), (128, 16, 16), (128, 16, 2),
+                                      (64, 8, 8)])
 def test_attn_decode(d, nq, nkv):
     B, Lmax = 5, 700
     qkv = bf16((B, (nq + 2 * nkv) * d), seed=19)
@@ -383,3 +386,26 @@ def test_attn_decode_many_items_per_warp():
         vv = vcn[b, :, :p + 1].transpose(1, 0, 2)
         ref = O.attention(a[b, :nq * d].reshape(1, nq, d), kk, vv, causal=True).reshape(-1)
         assert rel_err(np32(out[b]), ref) < 2e-2
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_attn_prefill_large_scores_and_noncausal(causal):
+    """Scores spanning ~+-40 (q, k ~ N(0, 4^2)): the running max moves by more than
+    the lazy-rescale threshold inside a row, so the O rescale in TMEM is exercised;
+    non-causal mode covers the unmasked path."""
+    nq, nkv, d, S, B = 8, 2, 128, 384, 2
+    T = B * S
+    qkv = bf16((T, (nq + 2 * nkv) * d), seed=77)
+    qkv[:, :(nq + nkv) * d] *= 4
+    out = torch.empty(T, nq * d, device=dev, dtype=torch.bfloat16)
+    K().attn_prefill(qkv, nq, nkv, d, B, S, out, causal=causal)
+    torch.cuda.synchronize()
+    a = np32(qkv)
+    ref = []
+    for s0 in range(B):
+        blk = a[s0 * S:(s0 + 1) * S]
+        q = blk[:, :nq * d].reshape(S, nq, d)
+        k = blk[:, nq * d:(nq + nkv) * d].reshape(S, nkv, d)
+        v = blk[:, (nq + nkv) * d:].reshape(S, nkv, d)
+        ref.append(O.attention(q, k, v, causal=causal).reshape(S, -1))
+    assert rel_err(np32(out), np.concatenate(ref)) < 2e-2
