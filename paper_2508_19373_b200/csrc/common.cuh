@@ -286,6 +286,8 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 // ------------------------------------------------------------- host side --
 // cuTensorMapEncodeTiled fetched through the runtime so the library does not
 // link libcuda directly.
+bool encode_tmap_2d_bf16_sw(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                            uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
 bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                          uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, bool swizzle128);
 

@@ -229,27 +229,29 @@ __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* _
 // step is 2 swizzled 16-byte x loads + broadcast fp32 router loads + 2*NE*8
 // FMAs.  Every (token, expert, range) chain and the ordered sum of the range
 // partials are exactly those of router_kernel: logits are bit-identical.
-constexpr int kCH = 64;       // elements per chunk (128 B rows)
 constexpr int kXStages = 2;
 
-template <int NE, int TPL>
-__global__ void __launch_bounds__(kThreads, 1)
+// CH = elements per chunk: 32 (64-byte rows, 64B swizzle, ~72 KB smem -> 2 CTAs
+// per SM) for NE <= 16; 64 (128-byte rows, 128B swizzle) for the wide routers
+// whose fp32 router chunks dominate the smem.
+template <int NE, int TPL, int CH>
+__global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
     router_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __nv_bfloat16* __restrict__ w, int T, int h,
                       int n_rows_w, int E, int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx,
                       float* __restrict__ topk_w, float* __restrict__ shared_gate, float* __restrict__ logits_out) {
   pdl_trigger();
   pdl_wait();
   constexpr int kTB = 32 * TPL;                   // tokens per CTA
-  constexpr int kXStageBytes = kTB * kCH * 2;     // per warp-stage
+  constexpr int kXStageBytes = kTB * CH * 2;     // per warp-stage
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t bars[kRanges][kXStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* xs = dsm + warp * kXStages * kXStageBytes;
-  float* ws = reinterpret_cast<float*>(dsm + kRanges * kXStages * kXStageBytes) + warp * NE * kCH;
+  float* ws = reinterpret_cast<float*>(dsm + kRanges * kXStages * kXStageBytes) + warp * NE * CH;
   uint64_t* bar = bars[warp];
   const int tb0 = blockIdx.x * kTB;
-  const int hr = h / kRanges, j0 = warp * hr, nch = hr / kCH;
+  const int hr = h / kRanges, j0 = warp * hr, nch = hr / CH;
   if (lane == 0) {
     for (int s2 = 0; s2 < kXStages; ++s2) mbar_init(&bar[s2], 1);
     fence_barrier_init();
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto issue = [&](int c, int stage) {
     if (lane == 0) {
       mbar_arrive_expect_tx(&bar[stage], kXStageBytes);
-      tma_load_2d(xs + stage * kXStageBytes, &tmX, &bar[stage], j0 + c * kCH, tb0, kEvictFirst);
+      tma_load_2d(xs + stage * kXStageBytes, &tmX, &bar[stage], j0 + c * CH, tb0, kEvictFirst);
     }
   };
   for (int c = 0; c < kXStages && c < nch; ++c) issue(c, c);
@@ -268,29 +270,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int i = 0; i < TPL; ++i)
 #pragma unroll
     for (int e = 0; e < NE; ++e) acc[i][e] = 0.f;
-  const int sw = lane & 7;  // 128B swizzle phase of rows lane and lane + 32
+  // swizzle phase of rows lane and lane + 32: 16-byte chunk c of row r sits at
+  // c ^ (r & 7) (128B rows) or c ^ ((r >> 1) & 3) (64B rows)
+  const int sw = CH == 64 ? (lane & 7) : ((lane >> 1) & 3);
   // router chunk c -> fp32 smem: lane handles items (lane, lane + 32) of the NE x 8 vectors;
   // the next chunk's vectors are loaded into registers while the current one is consumed
-  constexpr int kWItems = (NE * (kCH / 8) + 31) / 32;
+  constexpr int kWItems = (NE * (CH / 8) + 31) / 32;
   uint4 wreg[kWItems];
   auto load_w = [&](int c) {
 #pragma unroll
     for (int k2 = 0; k2 < kWItems; ++k2) {
-      const int it = lane + 32 * k2, e = it / (kCH / 8), v = it % (kCH / 8);
-      wreg[k2] = (it < NE * (kCH / 8) && e < n_rows_w)
-                     ? __ldg(reinterpret_cast<const uint4*>(w + (int64_t)e * h + j0 + c * kCH + v * 8))
+      const int it = lane + 32 * k2, e = it / (CH / 8), v = it % (CH / 8);
+      wreg[k2] = (it < NE * (CH / 8) && e < n_rows_w)
+                     ? __ldg(reinterpret_cast<const uint4*>(w + (int64_t)e * h + j0 + c * CH + v * 8))
                      : make_uint4(0, 0, 0, 0);
     }
   };
   auto store_w = [&]() {
 #pragma unroll
     for (int k2 = 0; k2 < kWItems; ++k2) {
-      const int it = lane + 32 * k2, e = it / (kCH / 8), v = it % (kCH / 8);
-      if (it < NE * (kCH / 8)) {
+      const int it = lane + 32 * k2, e = it / (CH / 8), v = it % (CH / 8);
+      if (it < NE * (CH / 8)) {
         const float2 a0 = unpack_bf16x2(wreg[k2].x), a1 = unpack_bf16x2(wreg[k2].y), a2 = unpack_bf16x2(wreg[k2].z),
                      a3 = unpack_bf16x2(wreg[k2].w);
-        reinterpret_cast<float4*>(ws + e * kCH + v * 8)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
-        reinterpret_cast<float4*>(ws + e * kCH + v * 8)[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
+        reinterpret_cast<float4*>(ws + e * CH + v * 8)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
+        reinterpret_cast<float4*>(ws + e * CH + v * 8)[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
       }
     }
   };
@@ -303,11 +307,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(&bar[stage], (c / kXStages) & 1);
     const uint8_t* xst = xs + stage * kXStageBytes;
 #pragma unroll 2
-    for (int v = 0; v < kCH / 8; ++v) {
+    for (int v = 0; v < CH / 8; ++v) {
       float xf[TPL][8];
 #pragma unroll
       for (int i = 0; i < TPL; ++i) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(xst + (lane + 32 * i) * 128 + ((v ^ sw) << 4));
+        const uint4 xv = *reinterpret_cast<const uint4*>(xst + (lane + 32 * i) * (CH * 2) + ((v ^ sw) << 4));
         const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -318,8 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
-        const float4 w0 = reinterpret_cast<const float4*>(ws + e * kCH + v * 8)[0];
-        const float4 w1 = reinterpret_cast<const float4*>(ws + e * kCH + v * 8)[1];
+        const float4 w0 = reinterpret_cast<const float4*>(ws + e * CH + v * 8)[0];
+        const float4 w1 = reinterpret_cast<const float4*>(ws + e * CH + v * 8)[1];
         const float wf[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -379,19 +383,20 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
   {
     // TMA-staged variant: 2 tokens per lane while 2*NE accumulators fit, else 1
     constexpr int TPL = NE <= 16 ? 2 : 1;
+    constexpr int CH = NE <= 16 ? 32 : 64;
     constexpr int kTB = 32 * TPL;
-    constexpr int smem_tma = kRanges * kXStages * kTB * kCH * 2 + kRanges * NE * kCH * 4 + 1024;
+    constexpr int smem_tma = kRanges * kXStages * kTB * CH * 2 + kRanges * NE * CH * 4 + 1024;
     static_assert(smem_tma <= 227 * 1024, "router smem");
-    if (h % (kRanges * kCH) == 0) {
+    if (h % (kRanges * CH) == 0) {
       static int configured_tma = 0;
       if (!configured_tma) {
-        if (configure_smem((const void*)router_tma_kernel<NE, TPL>, smem_tma)) return HAP_ERR_LAUNCH;
+        if (configure_smem((const void*)router_tma_kernel<NE, TPL, CH>, smem_tma)) return HAP_ERR_LAUNCH;
         configured_tma = 1;
       }
       CUtensorMap tmX;
-      if (!encode_tmap_2d_bf16(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, kCH, kTB, true))
+      if (!encode_tmap_2d_bf16_sw(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, CH, kTB, CH * 2))
         return HAP_ERR_DRIVER;
-      { if (hap::launch_k(router_tma_kernel<NE, TPL>, dim3((unsigned)((T + kTB - 1) / kTB)), dim3(kThreads), smem_tma,
+      { if (hap::launch_k(router_tma_kernel<NE, TPL, CH>, dim3((unsigned)((T + kTB - 1) / kTB)), dim3(kThreads), smem_tma,
                           st, tmX, reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared),
                           (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
       HAP_CHECK_LAUNCH();
