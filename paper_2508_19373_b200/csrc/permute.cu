@@ -160,6 +160,97 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const int32_t* __rest
   }
 }
 
+// Large-T combine: one warp per token row; the k slot rows / weights are read
+// once per token and every lane streams its 16-byte column chunks of the k
+// expert outputs (+ shared output, + residual) with 4 chunks in flight, so a
+// warp keeps several KB of loads outstanding instead of one dependent pair per
+// 256-column item.  Same accumulation order as combine_kernel (slot order,
+// then shared, then residual; fp32; one bf16 rounding): bit-identical.
+constexpr int kCombineU = 4;
+__global__ void __launch_bounds__(kThreads) combine_row_kernel(const uint4* __restrict__ y, const int32_t* __restrict__ dst,
+                                                               const float* __restrict__ tw, int T, int k, int hv,
+                                                               const uint4* __restrict__ resid, int res_row0,
+                                                               int res_rows, const uint4* __restrict__ shared_y,
+                                                               const float* __restrict__ shared_gate,
+                                                               uint4* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int warp_global = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_warps = (gridDim.x * kThreads) >> 5;
+  for (int t = warp_global; t < T; t += n_warps) {
+    const int my_row = lane < k ? dst[(int64_t)t * k + lane] : -1;
+    const float my_w = lane < k ? tw[(int64_t)t * k + lane] : 0.f;
+    const float sg = shared_y ? shared_gate[t] : 0.f;
+    const bool has_res = resid && t >= res_row0 && t < res_row0 + res_rows;
+    for (int c0 = lane; c0 < hv; c0 += 32 * kCombineU) {
+      float acc[kCombineU][8];
+#pragma unroll
+      for (int u = 0; u < kCombineU; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        const int row = __shfl_sync(0xffffffffu, my_row, j);
+        const float wj = __shfl_sync(0xffffffffu, my_w, j);
+        if (row < 0) continue;
+        uint4 v[kCombineU];
+#pragma unroll
+        for (int u = 0; u < kCombineU; ++u) {
+          const int c = c0 + 32 * u;
+          v[u] = c < hv ? __ldg(y + (int64_t)row * hv + c) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kCombineU; ++u) {
+          const uint32_t vw[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = unpack_bf16x2(vw[i]);
+            acc[u][2 * i] = fmaf(wj, f.x, acc[u][2 * i]);
+            acc[u][2 * i + 1] = fmaf(wj, f.y, acc[u][2 * i + 1]);
+          }
+        }
+      }
+      if (shared_y) {
+#pragma unroll
+        for (int u = 0; u < kCombineU; ++u) {
+          const int c = c0 + 32 * u;
+          if (c >= hv) continue;
+          const uint4 v = __ldg(shared_y + (int64_t)t * hv + c);
+          const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = unpack_bf16x2(vw[i]);
+            acc[u][2 * i] = fmaf(sg, f.x, acc[u][2 * i]);
+            acc[u][2 * i + 1] = fmaf(sg, f.y, acc[u][2 * i + 1]);
+          }
+        }
+      }
+      if (has_res) {
+#pragma unroll
+        for (int u = 0; u < kCombineU; ++u) {
+          const int c = c0 + 32 * u;
+          if (c >= hv) continue;
+          const uint4 v = __ldg(resid + (int64_t)(t - res_row0) * hv + c);
+          const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = unpack_bf16x2(vw[i]);
+            acc[u][2 * i] += f.x;
+            acc[u][2 * i + 1] += f.y;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kCombineU; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < hv)
+          out[(int64_t)t * hv + c] = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
+                                                pack_bf16x2(acc[u][4], acc[u][5]), pack_bf16x2(acc[u][6], acc[u][7]));
+      }
+    }
+  }
+}
+
 // One warp per (token, 256-column chunk): lane owns columns chunk*256 + lane*8
 // .. +8.  Slot rows/weights are loaded once per warp (lane j holds slot j) and
 // broadcast with shuffles, so small-T (decode) calls still fill the GPU.
@@ -319,6 +410,16 @@ extern "C" int hap_moe_combine(const void* y, const int32_t* dst_of_row, const f
     return HAP_ERR_MISALIGNED;
   if (T == 0) return HAP_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (T >= 148 * kWarps) {  // enough tokens to fill the GPU with one warp per row
+    int grid_r = (int)((T + kWarps - 1) / kWarps);
+    if (grid_r > 148 * 16) grid_r = 148 * 16;
+    { if (hap::launch_k(combine_row_kernel, dim3(grid_r), dim3(kThreads), 0, st, reinterpret_cast<const uint4*>(y),
+                        dst_of_row, topk_w, (int)T, (int)k, (int)(h / 8), reinterpret_cast<const uint4*>(residual),
+                        (int)res_row0, (int)res_rows, reinterpret_cast<const uint4*>(shared_y), shared_gate,
+                        reinterpret_cast<uint4*>(out)) != cudaSuccess) return HAP_ERR_LAUNCH; }
+    HAP_CHECK_LAUNCH();
+    return HAP_OK;
+  }
   const int64_t items = T * ((h / 8 + 31) / 32);
   int grid = (int)((items * 32 + kThreads - 1) / kThreads);
   if (grid > 148 * 16) grid = 148 * 16;

@@ -291,6 +291,37 @@ def test_combine_with_shared_and_residual_window():
     assert rel_err(np32(out), ref) < 1e-2
 
 
+def test_combine_row_kernel_matches_chunk_kernel():
+    """Large-T combine (warp per token row) vs the numpy sum and bit-identical to
+    the chunked small-T kernel on the same tokens; dropped slots (dst = -1)."""
+    ops = K()
+    T, k, h = 4000, 2, 4096
+    R = T * k
+    y = bf16((R, h), seed=23)
+    perm = torch.randperm(R, device=dev).to(torch.int32)
+    perm[::97] = -1
+    tw = torch.rand(T, k, device=dev)
+    res = bf16((1000, h), seed=24)
+    ys = bf16((T, h), seed=25)
+    sg = torch.rand(T, device=dev)
+    out = torch.empty(T, h, device=dev, dtype=torch.bfloat16)
+    ops.moe_combine(y, perm, tw, T, k, out, residual=res, shared_y=ys, shared_gate=sg, res_row0=100, res_rows=1000)
+    sub = torch.empty(300, h, device=dev, dtype=torch.bfloat16)
+    ops.moe_combine(y, perm[:300 * k].contiguous(), tw[:300].contiguous(), 300, k, sub, residual=res,
+                    shared_y=ys[:300].contiguous(), shared_gate=sg[:300].contiguous(), res_row0=100, res_rows=1000)
+    torch.cuda.synchronize()
+    assert torch.equal(sub, out[:300])
+    p = perm.cpu().numpy().reshape(T, k)
+    yy = np32(y)
+    ref = np32(ys) * sg.cpu().numpy()[:, None]
+    twn = tw.cpu().numpy()
+    for j in range(k):
+        ok = p[:, j] >= 0
+        ref[ok] += twn[ok, j][:, None] * yy[p[ok, j]]
+    ref[100:1100] += np32(res)
+    assert rel_err(np32(out), ref) < 1e-2
+
+
 # ------------------------------------------------------------ norm / rope --
 def test_rmsnorm():
     x = bf16((333, 4096), seed=16)
