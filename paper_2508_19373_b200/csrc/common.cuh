@@ -92,6 +92,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Latency-critical wait: try_wait without a suspend-time hint (the hardware
+// default), for the MMA issuer and softmax waits on the attention critical path.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "HAP_SPIN_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra HAP_SPIN_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
 // 2^x on the SFU (ftz; inputs here are <= 0 or small positive).
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;

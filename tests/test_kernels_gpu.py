@@ -352,7 +352,8 @@ def test_rope(d):
 # ------------------------------------------------------------- attention --
 @pytest.mark.parametrize("d,nq,nkv,S,B", [(128, 8, 2, 200, 2), (64, 8, 2, 128, 4), (128, 4, 4, 1000, 1),
                                            (128, 16, 2, 2048, 2),   # G = 8, 512 items: dynamic scheduler
-                                           (64, 8, 1, 777, 3)])     # G = 8, d = 64, ragged tail tiles
+                                           (64, 8, 1, 777, 3),      # G = 8, d = 64, ragged tail tiles
+                                           (128, 6, 2, 300, 2)])    # G = 3: q-tile pairs + a lone tile
 def test_attn_prefill(d, nq, nkv, S, B):
     T = B * S
     qkv = bf16((T, (nq + 2 * nkv) * d), seed=18)
