@@ -127,6 +127,15 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// 1D bulk copy global -> shared (16-byte aligned, size a multiple of 16),
+// completion counted on bar.
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // 2-CTA (cta_group::2) variant: executed by both CTAs of a pair; each loads its
 // own half into its own smem and the transaction bytes land on the LEADER
 // CTA's barrier (peer bit of the shared::cluster address cleared).

@@ -16,6 +16,8 @@
 // Models: router term 2*T*h*E of expert_flops (reference arch.py:177); HF
 // semantics of MixtralTopKRouter / Qwen2MoeTopKRouter (softmax -> top-k ->
 // optional renorm).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hap {
@@ -86,7 +88,7 @@ __device__ __forceinline__ void finish_token(const float (&acc)[NE], int t, int 
 // Small-T variant (decode): one CTA per token; thread (p, e) runs exactly the
 // sequential fma chain the large kernel's lane runs for (token, expert e,
 // range p), so the logits are bit-identical between the two variants.
-template <int NE>
+template <int NE, bool kStage>
 __global__ void __launch_bounds__(kRanges * NE) router_small_kernel(const __nv_bfloat16* __restrict__ x,
                                                                     const __nv_bfloat16* __restrict__ w, int T,
                                                                     int h, int n_rows_w, int E, int top_k,
@@ -97,29 +99,44 @@ __global__ void __launch_bounds__(kRanges * NE) router_small_kernel(const __nv_b
                                                                     float* __restrict__ logits_out) {
   pdl_trigger();
   pdl_wait();
-  extern __shared__ uint4 xs[];  // token row, h/8 vectors
+  extern __shared__ uint4 xs[];  // token row (h/8 vectors), then (kStage) the router rows
   __shared__ float part[kRanges][NE];
+  __shared__ __align__(8) uint64_t bar;
   const int t = blockIdx.x;
   const uint4* xrow = reinterpret_cast<const uint4*>(x + (int64_t)t * h);
-  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) xs[i] = __ldg(xrow + i);
-  __syncthreads();
   const int p = threadIdx.x / NE, e = threadIdx.x % NE;
   const int hr = h / kRanges;
+  const int nv = hr / 8;
+  // kStage: the token row and every (router row, h-range) segment arrive by 1D
+  // bulk copies in one round trip; segments sit nv+1 vectors apart so the 64
+  // threads' reads fall in different banks.  (The streaming variant needs
+  // ~4 dependent L2/DRAM round trips per thread: 15 us for Mixtral decode.)
+  uint4* ws = xs + h / 8;
+  if (kStage) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&bar, (uint32_t)(h * 2) + (uint32_t)n_rows_w * (uint32_t)(h * 2));
+      bulk_load(xs, xrow, (uint32_t)(h * 2), &bar);
+      for (int r = 0; r < n_rows_w * kRanges; ++r)
+        bulk_load(ws + r * (nv + 1), w + (int64_t)r * hr, (uint32_t)(hr * 2), &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
+    for (int i = threadIdx.x; i < h / 8; i += blockDim.x) xs[i] = __ldg(xrow + i);
+    __syncthreads();
+  }
   float acc = 0.f;
   if (e < n_rows_w) {
-    const uint4* wr = reinterpret_cast<const uint4*>(w + (int64_t)e * h + p * hr);
-    const uint4* xr = xs + p * (hr / 8);
-    const int nv = hr / 8;
-    uint4 wb[kSmallPrefetch];
-#pragma unroll
-    for (int i = 0; i < kSmallPrefetch; ++i) wb[i] = i < nv ? __ldg(wr + i) : make_uint4(0, 0, 0, 0);
-    for (int v0 = 0; v0 < nv; v0 += kSmallPrefetch) {
-#pragma unroll
-      for (int i = 0; i < kSmallPrefetch; ++i) {
-        const int v = v0 + i;
-        if (v >= nv) break;
-        const uint4 wv = wb[i];
-        if (v + kSmallPrefetch < nv) wb[i] = __ldg(wr + v + kSmallPrefetch);
+    const uint4* xr = xs + p * nv;
+    if (kStage) {
+      const uint4* wr = ws + (e * kRanges + p) * (nv + 1);
+#pragma unroll 4
+      for (int v = 0; v < nv; ++v) {
+        const uint4 wv = wr[v];
         const uint4 xv = xr[v];
         const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
         const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
@@ -129,6 +146,30 @@ __global__ void __launch_bounds__(kRanges * NE) router_small_kernel(const __nv_b
           const float2 fw = unpack_bf16x2(ww[q]);
           acc = __fmaf_rn(fx.x, fw.x, acc);
           acc = __fmaf_rn(fx.y, fw.y, acc);
+        }
+      }
+    } else {
+      const uint4* wr = reinterpret_cast<const uint4*>(w + (int64_t)e * h + p * hr);
+      uint4 wb[kSmallPrefetch];
+#pragma unroll
+      for (int i = 0; i < kSmallPrefetch; ++i) wb[i] = i < nv ? __ldg(wr + i) : make_uint4(0, 0, 0, 0);
+      for (int v0 = 0; v0 < nv; v0 += kSmallPrefetch) {
+#pragma unroll
+        for (int i = 0; i < kSmallPrefetch; ++i) {
+          const int v = v0 + i;
+          if (v >= nv) break;
+          const uint4 wv = wb[i];
+          if (v + kSmallPrefetch < nv) wb[i] = __ldg(wr + v + kSmallPrefetch);
+          const uint4 xv = xr[v];
+          const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+          const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 fx = unpack_bf16x2(xw[q]);
+            const float2 fw = unpack_bf16x2(ww[q]);
+            acc = __fmaf_rn(fx.x, fw.x, acc);
+            acc = __fmaf_rn(fx.y, fw.y, acc);
+          }
         }
       }
     }
@@ -368,13 +409,24 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
   }
   if (T <= kSmallT) {
     const int xs_bytes = (int)(h / 8) * 16;
+    const int ws_bytes = (int)((E + has_shared) * kRanges) * (int)(h / kRanges / 8 + 1) * 16;
+    constexpr int kStageLimit = 200 * 1024;
     static int configured_small = 0;
     if (!configured_small) {
-      if (configure_smem((const void*)router_small_kernel<NE>, 64 * 1024)) return HAP_ERR_LAUNCH;
+      if (configure_smem((const void*)router_small_kernel<NE, false>, 64 * 1024) ||
+          configure_smem((const void*)router_small_kernel<NE, true>, kStageLimit))
+        return HAP_ERR_LAUNCH;
       configured_small = 1;
     }
     if (xs_bytes > 64 * 1024) return HAP_ERR_UNSUPPORTED;
-    { if (hap::launch_k(router_small_kernel<NE>, dim3((int)T), dim3(kRanges * NE), xs_bytes, st, 
+    static const bool allow_stage = [] {
+      const char* e = getenv("HAP_ROUTER_STAGE");  // A/B experiments only
+      return e ? atoi(e) != 0 : true;
+    }();
+    const bool stage = allow_stage && xs_bytes + ws_bytes <= kStageLimit && (reinterpret_cast<uintptr_t>(w) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    auto kern = stage ? router_small_kernel<NE, true> : router_small_kernel<NE, false>;
+    { if (hap::launch_k(kern, dim3((int)T), dim3(kRanges * NE), stage ? xs_bytes + ws_bytes : xs_bytes, st,
         reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h,
         (int)(E + has_shared), (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
     HAP_CHECK_LAUNCH();
