@@ -428,6 +428,7 @@ def main():
     torch.cuda.synchronize()
     gu = [s.elapsed_time(e) for s, e in blk.timers["gate_up"]]
     dn = [s.elapsed_time(e) for s, e in blk.timers["down"]]
+    phase_ms = {k: statistics.mean(s.elapsed_time(e) for s, e in v) for k, v in blk.timers.items()}
     blk.timers = None
     gu_ms = max_over_ranks(statistics.mean(gu))
     dn_ms = max_over_ranks(statistics.mean(dn))
@@ -454,6 +455,35 @@ def main():
                 "algorithmic_flops_per_launch": gu_flops, "launch_ms": gu_ms,
                 "down_proj": {"launch_ms": dn_ms, "achieved": dn_flops / (dn_ms / 1e3) / 1e12},
                 "expert_gemms_share_of_step": (gu_ms + dn_ms) / results["hap"]["prefill_ms"]}
+
+    # -- every kernel phase of the prefill step against its roofline (N=1: the
+    # algorithmic work per launch below is for the whole, unsharded block)
+    kernels = None
+    if world == 1:
+        T, h, d = PREFILL_BATCH * PREFILL_SEQ, cfg.hidden, cfg.head_dim
+        nq, nkv, E, k = cfg.n_q_heads, cfg.n_kv_heads, cfg.n_experts, cfg.top_k
+        work = {  # phase: (algorithmic work per launch, bound)
+            "norm": (2.0 * T * h * 2, "hbm"),
+            "qkv": (2.0 * T * h * (nq + 2 * nkv) * d, "tensor"),
+            "attn": (4.0 * T * PREFILL_SEQ * nq * d / 2, "tensor"),  # arch.py:161, causal half
+            "o_proj": (2.0 * T * nq * d * h, "tensor"),
+            "router": (T * h * 2.0 + E * h * 2.0 + T * k * 8.0, "hbm"),
+            "permute": (T * h * 2.0 + T * k * h * 2.0 + T * k * 4.0, "hbm"),
+            "gate_up": (gu_flops, "tensor"),
+            "down": (dn_flops, "tensor"),
+            "combine": (T * k * h * 2.0 + 2.0 * T * h * 2, "hbm"),
+        }
+        kernels = {}
+        for name, (wk, bound) in work.items():
+            if name not in phase_ms:
+                continue
+            ms = phase_ms[name]
+            if bound == "tensor":
+                ach, peak, unit = wk / (ms / 1e3) / 1e12, peaks["bf16_tflops_sustained"], "TFLOP/s"
+            else:
+                ach, peak, unit = wk / (ms / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"
+            kernels[name] = {"ms": ms, "bound": bound, "work": wk, "achieved": ach, "peak": peak, "unit": unit,
+                             "frac": ach / peak}
 
     # -- decode HBM roofline (whole step)
     decode = None
@@ -508,7 +538,8 @@ def main():
                        "planner": f"moeplan solve_ilp (reference ILP) on {plan_src}",
                        "planner_ms": plan_ms,
                        "l2": "no flush: every step streams > L2 (2.8 GB expert weights + 128 MB activations)"},
-            "plans": results, "decode": decode, "roofline": roofline, "roofline_block": roofline_block, "cpu_baseline": cpu, "e2e": e2e,
+            "plans": results, "decode": decode, "roofline": roofline, "roofline_block": roofline_block,
+            "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": TIMED_LAUNCHES.get(f"prefill:{hap_p.degrees.label()}"),
             "gpu_launches_note": "kernels of libhap_kernels.so launched in the headline timed region (this rank)",
             "gpu_launches_all_bench_loops": total_launches,

@@ -125,7 +125,7 @@ class HapMoEBlock:
         _maybe_peer_allreduce(self.comm)
         self.last_routing = None  # (topk_idx, dst_of_row, seg) of the last expert call, for parity tests
         self.capture = None       # set to {} to keep references to intermediates (tests only)
-        self.timers = None        # set to {} to record CUDA events around the expert GEMMs (bench)
+        self.timers = None        # set to {} to record CUDA events around each kernel phase (bench)
         self.ep_peer = _ep_peer_default()
 
     @classmethod
@@ -297,7 +297,8 @@ class HapMoEBlock:
             x = x_local.contiguous()
 
         # ---------------- attention module
-        xn = ops.rmsnorm(x, w.ln1, cfg.rms_eps)
+        with self._timed("norm"):
+            xn = ops.rmsnorm(x, w.ln1, cfg.rms_eps)
         nq, nkv = w.n_q_local, w.n_kv_local
         if decode:
             if rows == n_seq and positions.dtype == torch.int32 and positions.is_contiguous():
@@ -308,7 +309,8 @@ class HapMoEBlock:
         else:
             pos = self._prefill_positions(bpr, S, rows)
         # QKV projection with RoPE fused into the GEMM epilogue
-        qkv = ops.gemm_qkv_rope(xn, w.wqkv, pos, nq + nkv, d, cfg.rope_theta, bias=w.bqkv)
+        with self._timed("qkv"):
+            qkv = ops.gemm_qkv_rope(xn, w.wqkv, pos, nq + nkv, d, cfg.rope_theta, bias=w.bqkv)
         attn = torch.zeros(rows, nq * d, device=dev, dtype=BF16) if rows != T_real else \
             torch.empty(rows, nq * d, device=dev, dtype=BF16)
         if decode:
@@ -320,10 +322,13 @@ class HapMoEBlock:
         elif n_seq:
             if kv_cache is not None:  # keep this prefill's k/v for the decode steps that follow
                 ops.kv_cache_fill(qkv, nq, nkv, d, n_seq, S, kv_cache.k, kv_cache.v)
-            ops.attn_prefill(qkv, nq, nkv, d, n_seq, S, attn)
-        h1 = ops.gemm(attn, w.wo, residual=x if lay.a_tp_rank == 0 else None)
+            with self._timed("attn"):
+                ops.attn_prefill(qkv, nq, nkv, d, n_seq, S, attn)
+        with self._timed("o_proj"):
+            h1 = ops.gemm(attn, w.wo, residual=x if lay.a_tp_rank == 0 else None)
         self._coll("all_reduce", h1, "attn_tp_group")
-        hn = ops.rmsnorm(h1, w.ln2, cfg.rms_eps)
+        with self._timed("norm"):
+            hn = ops.rmsnorm(h1, w.ln2, cfg.rms_eps)
 
         # ---------------- boundary: attention layout -> expert shard
         S_e, a_dp = lay.n_shards, self.deg.a_dp
@@ -387,13 +392,15 @@ class HapMoEBlock:
         idx = torch.empty(T, k, device=dev, dtype=torch.int32)
         tw = torch.empty(T, k, device=dev, dtype=torch.float32)
         sg = torch.empty(T, device=dev, dtype=torch.float32) if cfg.n_shared else None
-        ops.router_topk(hn_s, w.router, E, k, cfg.norm_topk_prob, bool(cfg.n_shared), idx, tw, sg)
+        with self._timed("router"):
+            ops.router_topk(hn_s, w.router, E, k, cfg.norm_topk_prob, bool(cfg.n_shared), idx, tw, sg)
         R = T * k
         x_perm = torch.empty(R, h, device=dev, dtype=BF16)
         dst = torch.empty(R, device=dev, dtype=torch.int32)
         seg = torch.empty(E + 1, device=dev, dtype=torch.int32)
         ws = torch.empty(max(ops.permute_workspace_bytes(R, E), 16), device=dev, dtype=torch.uint8)
-        ops.moe_permute(idx.view(-1), E, hn_s, k, x_perm, dst, seg, ws)
+        with self._timed("permute"):
+            ops.moe_permute(idx.view(-1), E, hn_s, k, x_perm, dst, seg, ws)
         self.last_routing = (idx, dst, seg)
         if self.capture is not None:
             self.capture.update(topk_w=tw, shared_gate=sg)
@@ -414,8 +421,9 @@ class HapMoEBlock:
             hs = ops.gemm(hn_s, w.ws13, swiglu_half=w.hw_s)
             ys = ops.gemm(hs, w.ws2)
         out = torch.empty(T, h, device=dev, dtype=BF16)
-        ops.moe_combine(Y, dst, tw, T, k, out, residual=residual, shared_y=ys, shared_gate=sg,
-                        res_row0=res_row0, res_rows=res_rows)
+        with self._timed("combine"):
+            ops.moe_combine(Y, dst, tw, T, k, out, residual=residual, shared_y=ys, shared_gate=sg,
+                            res_row0=res_row0, res_rows=res_rows)
         return out
 
     def _ep_experts(self, x_perm, seg):
