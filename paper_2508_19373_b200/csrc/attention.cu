@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
   constexpr int kStageBytes = 2 * H * kHalfBytes;  // K + V of one chunk
   constexpr int NT = D / 8;                        // O n-tiles
   extern __shared__ uint8_t dsm_raw[];
-  uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* dsm = smem_align1024(dsm_raw);
   __shared__ __align__(8) uint64_t bars[kDecWarps][kDecStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = dsm + warp * kDecStages * kStageBytes;

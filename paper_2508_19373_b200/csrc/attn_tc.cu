@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait();
   using SM = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* sQ = smem;                  // [2][kQ]
   uint8_t* sK = sQ + 2 * SM::kQ;       // [2][kK]
   uint8_t* sV = sK + 2 * SM::kK;       // [2][kV]
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kTile = PairSmem<D>::kTile;
   constexpr int kKS = PairSmem<D>::kKS, kVS = PairSmem<D>::kVS;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* sQ = smem;            // [tile][kTile]
   uint8_t* sK = sQ + 2 * kTile;  // [stage][kTile]
   uint8_t* sV = sK + kKS * kTile;  // [stage][kTile]

@@ -32,6 +32,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Round a dynamic shared-memory base up to 1024 B by pointer arithmetic on the
+// shared array itself: a uintptr_t round trip hides the address space from the
+// compiler, which then emits generic LD/ST (slower, through the generic path)
+// for every C++ access through the result.
+__device__ __forceinline__ uint8_t* smem_align1024(uint8_t* base) {
+  return base + ((1024u - (smem_u32(base) & 1023u)) & 1023u);
+}
+
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t l;
   asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kBBytes = Geo<kPair>::kBBytes;
   constexpr int TM = BM * kPair;  // rows per tile
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* smA = smem;
   uint8_t* smB = smem + kStages * kABytes;
   const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0;

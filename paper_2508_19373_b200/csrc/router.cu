@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
   constexpr int kTB = 32 * TPL;                   // tokens per CTA
   constexpr int kXStageBytes = kTB * CH * 2;     // per warp-stage
   extern __shared__ uint8_t dsm_raw[];
-  uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* dsm = smem_align1024(dsm_raw);
   __shared__ __align__(8) uint64_t bars[kRanges][kXStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* xs = dsm + warp * kXStages * kXStageBytes;
