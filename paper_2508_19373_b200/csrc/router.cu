@@ -262,34 +262,48 @@ __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* _
   finish_token<NE>(acc, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
 }
 
-// Large-T variant for NE <= 16 (Mixtral, tiny): CTA = 64 tokens x 8 h-ranges,
-// lane owns tokens (t0 + lane, t0 + lane + 32) of its warp's range.  Token rows
-// arrive by TMA (64-element x 64-row boxes, 128B swizzle, a 2-stage ring per
-// warp) instead of per-lane row-strided loads, and each 64-element chunk of the
-// router rows is converted to fp32 in smem once per warp, so a lane's inner
-// step is 2 swizzled 16-byte x loads + broadcast fp32 router loads + 2*NE*8
-// FMAs.  Every (token, expert, range) chain and the ordered sum of the range
-// partials are exactly those of router_kernel: logits are bit-identical.
+// Large-T variant: CTA = 32*TPL tokens x 8 h-ranges, lane owns tokens
+// (t0 + lane [, t0 + lane + 32]) of its warp's range.  Each warp streams its
+// range in CH-element chunks through a 2-stage TMA ring: the token rows
+// (CH x 32*TPL box, swizzled) and the router rows of that chunk (CH x NE box,
+// bf16, OOB rows zero-filled) land on one barrier per stage.  A lane's inner
+// step is TPL swizzled 16-byte x loads, then per expert one broadcast 16-byte
+// router load (8 bf16) feeding 8*TPL FMAs.  Every (token, expert, range) chain
+// and the ordered sum of the range partials are exactly those of
+// router_kernel: logits are bit-identical.
 constexpr int kXStages = 2;
 
-// CH = elements per chunk: 32 (64-byte rows, 64B swizzle, ~72 KB smem -> 2 CTAs
-// per SM) for NE <= 16; 64 (128-byte rows, 128B swizzle) for the wide routers
-// whose fp32 router chunks dominate the smem.
+template <int NE, int TPL, int CH>
+struct RouterTmaGeo {
+  static constexpr int kTB = 32 * TPL;                       // tokens per CTA
+  static constexpr int kXBytes = kTB * CH * 2;               // token box per warp-stage
+  static constexpr int kWBytes = NE * CH * 2;                // router box per warp-stage
+  static constexpr int kStageBytes = kXBytes + kWBytes;
+  // narrow routers (NE <= 16) re-expand each router chunk to fp32 once per warp:
+  // 2 broadcast fp32 loads per 8 FMAs beat 1 bf16 load + 8 unpacks when the
+  // loop is issue-bound; wide routers are smem-bandwidth-bound and keep bf16
+  static constexpr bool kF32W = NE <= 16;
+  static constexpr int kWF32Bytes = kF32W ? NE * CH * 4 : 0;  // per warp
+  static constexpr int kRing = kRanges * (kXStages * kStageBytes + kWF32Bytes);
+  static constexpr int kPart = kRanges * NE * (kTB + 1) * 4;  // partial table (overlays the rings)
+  static constexpr int kSmem = (kRing > kPart ? kRing : kPart) + 1024;
+};
+
 template <int NE, int TPL, int CH>
 __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
-    router_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __nv_bfloat16* __restrict__ w, int T, int h,
-                      int n_rows_w, int E, int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx,
+    router_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int T,
+                      int h, int E, int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx,
                       float* __restrict__ topk_w, float* __restrict__ shared_gate, float* __restrict__ logits_out) {
   pdl_trigger();
   pdl_wait();
-  constexpr int kTB = 32 * TPL;                   // tokens per CTA
-  constexpr int kXStageBytes = kTB * CH * 2;     // per warp-stage
+  using G = RouterTmaGeo<NE, TPL, CH>;
+  constexpr int kTB = G::kTB;
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* dsm = smem_align1024(dsm_raw);
   __shared__ __align__(8) uint64_t bars[kRanges][kXStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* xs = dsm + warp * kXStages * kXStageBytes;
-  float* ws = reinterpret_cast<float*>(dsm + kRanges * kXStages * kXStageBytes) + warp * NE * CH;
+  uint8_t* ring = dsm + warp * (kXStages * G::kStageBytes + G::kWF32Bytes);
+  float* wf32 = reinterpret_cast<float*>(ring + kXStages * G::kStageBytes);  // [NE][CH] (kF32W)
   uint64_t* bar = bars[warp];
   const int tb0 = blockIdx.x * kTB;
   const int hr = h / kRanges, j0 = warp * hr, nch = hr / CH;
@@ -300,8 +314,10 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
   __syncwarp();
   auto issue = [&](int c, int stage) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(&bar[stage], kXStageBytes);
-      tma_load_2d(xs + stage * kXStageBytes, &tmX, &bar[stage], j0 + c * CH, tb0, kEvictFirst);
+      uint8_t* st = ring + stage * G::kStageBytes;
+      mbar_arrive_expect_tx(&bar[stage], G::kStageBytes);
+      tma_load_2d(st, &tmX, &bar[stage], j0 + c * CH, tb0, kEvictFirst);
+      tma_load_2d(st + G::kXBytes, &tmW, &bar[stage], j0 + c * CH, 0, kEvictLast);
     }
   };
   for (int c = 0; c < kXStages && c < nch; ++c) issue(c, c);
@@ -314,40 +330,23 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
   // swizzle phase of rows lane and lane + 32: 16-byte chunk c of row r sits at
   // c ^ (r & 7) (128B rows) or c ^ ((r >> 1) & 3) (64B rows)
   const int sw = CH == 64 ? (lane & 7) : ((lane >> 1) & 3);
-  // router chunk c -> fp32 smem: lane handles items (lane, lane + 32) of the NE x 8 vectors;
-  // the next chunk's vectors are loaded into registers while the current one is consumed
-  constexpr int kWItems = (NE * (CH / 8) + 31) / 32;
-  uint4 wreg[kWItems];
-  auto load_w = [&](int c) {
-#pragma unroll
-    for (int k2 = 0; k2 < kWItems; ++k2) {
-      const int it = lane + 32 * k2, e = it / (CH / 8), v = it % (CH / 8);
-      wreg[k2] = (it < NE * (CH / 8) && e < n_rows_w)
-                     ? __ldg(reinterpret_cast<const uint4*>(w + (int64_t)e * h + j0 + c * CH + v * 8))
-                     : make_uint4(0, 0, 0, 0);
-    }
-  };
-  auto store_w = [&]() {
-#pragma unroll
-    for (int k2 = 0; k2 < kWItems; ++k2) {
-      const int it = lane + 32 * k2, e = it / (CH / 8), v = it % (CH / 8);
-      if (it < NE * (CH / 8)) {
-        const float2 a0 = unpack_bf16x2(wreg[k2].x), a1 = unpack_bf16x2(wreg[k2].y), a2 = unpack_bf16x2(wreg[k2].z),
-                     a3 = unpack_bf16x2(wreg[k2].w);
-        reinterpret_cast<float4*>(ws + e * CH + v * 8)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
-        reinterpret_cast<float4*>(ws + e * CH + v * 8)[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
-      }
-    }
-  };
-  load_w(0);
-  store_w();
   for (int c = 0; c < nch; ++c) {
     const int stage = c % kXStages;
-    if (c + 1 < nch) load_w(c + 1);
-    __syncwarp();  // router chunk c visible to every lane
     mbar_wait(&bar[stage], (c / kXStages) & 1);
-    const uint8_t* xst = xs + stage * kXStageBytes;
-#pragma unroll 2
+    const uint8_t* xst = ring + stage * G::kStageBytes;
+    const uint4* wst = reinterpret_cast<const uint4*>(xst + G::kXBytes);  // [NE][CH/8] 16-byte vectors
+    if (G::kF32W) {
+#pragma unroll
+      for (int it = lane; it < NE * CH / 8; it += 32) {
+        const uint4 wv = wst[it];
+        const float2 a0 = unpack_bf16x2(wv.x), a1 = unpack_bf16x2(wv.y), a2 = unpack_bf16x2(wv.z),
+                     a3 = unpack_bf16x2(wv.w);
+        reinterpret_cast<float4*>(wf32 + it * 8)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
+        reinterpret_cast<float4*>(wf32 + it * 8)[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
+      }
+      __syncwarp();
+    }
+#pragma unroll(G::kF32W ? 2 : 1)
     for (int v = 0; v < CH / 8; ++v) {
       float xf[TPL][8];
 #pragma unroll
@@ -363,19 +362,30 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
       }
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
-        const float4 w0 = reinterpret_cast<const float4*>(ws + e * CH + v * 8)[0];
-        const float4 w1 = reinterpret_cast<const float4*>(ws + e * CH + v * 8)[1];
-        const float wf[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        float wf[8];  // same address in every lane: broadcast loads
+        if (G::kF32W) {
+          const float4 w0 = reinterpret_cast<const float4*>(wf32 + e * CH + v * 8)[0];
+          const float4 w1 = reinterpret_cast<const float4*>(wf32 + e * CH + v * 8)[1];
+          wf[0] = w0.x; wf[1] = w0.y; wf[2] = w0.z; wf[3] = w0.w;
+          wf[4] = w1.x; wf[5] = w1.y; wf[6] = w1.z; wf[7] = w1.w;
+        } else {
+          const uint4 wv = wst[e * (CH / 8) + v];
+          const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = unpack_bf16x2(ww[q]);
+            wf[2 * q] = f.x;
+            wf[2 * q + 1] = f.y;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
 #pragma unroll
           for (int i = 0; i < TPL; ++i) acc[i][e] = __fmaf_rn(xf[i][q], wf[q], acc[i][e]);
-        }
       }
     }
-    __syncwarp();  // stage and router chunk consumed by every lane
+    __syncwarp();  // stage consumed by every lane
     if (c + kXStages < nch) issue(c + kXStages, stage);
-    if (c + 1 < nch) store_w();
   }
   __syncthreads();  // the partial table below overlays other warps' stages
   float* part = reinterpret_cast<float*>(dsm);  // [kRanges][NE][kTB + 1]
@@ -433,24 +443,24 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
     return HAP_OK;
   }
   {
-    // TMA-staged variant: 2 tokens per lane while 2*NE accumulators fit, else 1
-    constexpr int TPL = NE <= 16 ? 2 : 1;
-    constexpr int CH = NE <= 16 ? 32 : 64;
-    constexpr int kTB = 32 * TPL;
-    constexpr int smem_tma = kRanges * kXStages * kTB * CH * 2 + kRanges * NE * CH * 4 + 1024;
-    static_assert(smem_tma <= 227 * 1024, "router smem");
+    // TMA-staged variant: 2 tokens per lane, 32-element chunks
+    constexpr int TPL = 2;
+    constexpr int CH = 32;
+    using G = RouterTmaGeo<NE, TPL, CH>;
+    static_assert(G::kSmem <= 227 * 1024, "router smem");
     if (h % (kRanges * CH) == 0) {
       static int configured_tma = 0;
       if (!configured_tma) {
-        if (configure_smem((const void*)router_tma_kernel<NE, TPL, CH>, smem_tma)) return HAP_ERR_LAUNCH;
+        if (configure_smem((const void*)router_tma_kernel<NE, TPL, CH>, G::kSmem)) return HAP_ERR_LAUNCH;
         configured_tma = 1;
       }
-      CUtensorMap tmX;
-      if (!encode_tmap_2d_bf16_sw(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, CH, kTB, CH * 2))
+      CUtensorMap tmX, tmW;
+      if (!encode_tmap_2d_bf16_sw(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, CH, G::kTB, CH * 2) ||
+          !encode_tmap_2d_bf16_sw(&tmW, w, (uint64_t)h, (uint64_t)(E + has_shared), (uint64_t)h * 2, CH, NE, 0))
         return HAP_ERR_DRIVER;
-      { if (hap::launch_k(router_tma_kernel<NE, TPL, CH>, dim3((unsigned)((T + kTB - 1) / kTB)), dim3(kThreads), smem_tma,
-                          st, tmX, reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared),
-                          (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
+      { if (hap::launch_k(router_tma_kernel<NE, TPL, CH>, dim3((unsigned)((T + G::kTB - 1) / G::kTB)), dim3(kThreads),
+                          G::kSmem, st, tmX, tmW, (int)T, (int)h, (int)E, (int)k, renorm, has_shared, idx, tw, sg,
+                          logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
       HAP_CHECK_LAUNCH();
       return HAP_OK;
     }
