@@ -196,7 +196,9 @@ def test_grouped_gemm_segment_groups():
                                                    (1, 3584, 64, 8, False, True),       # small-T kernel
                                                    (3000, 4096, 8, 2, True, False),     # large-T kernel
                                                    (2100, 3584, 64, 8, False, True),
-                                                   (1500, 2048, 60, 4, False, True)])
+                                                   (1500, 2048, 60, 4, False, True),
+                                                   (1200, 1024, 16, 2, True, False),    # large-T, fp32 router chunks
+                                                   (1100, 2048, 24, 4, False, True)])   # large-T, bf16 chunks, NE 32
 def test_router_bit_exact(T, h, E, k, renorm, shared):
     x = bf16((T, h), seed=10)
     w = bf16((E + int(shared), h), 0.02, seed=11)
