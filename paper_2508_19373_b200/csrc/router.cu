@@ -266,25 +266,38 @@ __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* _
 // (t0 + lane [, t0 + lane + 32]) of its warp's range.  Each warp streams its
 // range in CH-element chunks through a 2-stage TMA ring: the token rows
 // (CH x 32*TPL box, swizzled) and the router rows of that chunk (CH x NE box,
-// bf16, OOB rows zero-filled) land on one barrier per stage.  A lane's inner
-// step is TPL swizzled 16-byte x loads, then per expert one broadcast 16-byte
-// router load (8 bf16) feeding 8*TPL FMAs.  Every (token, expert, range) chain
-// and the ordered sum of the range partials are exactly those of
-// router_kernel: logits are bit-identical.
+// bf16, OOB rows zero-filled) land on one barrier per stage.  Each warp then
+// re-expands its router chunk to fp32 transposed to [j][e], so one broadcast
+// 16-byte load yields the weights of experts e..e+3 at element j, and the
+// chains (token, e) and (token, e+1) advance together in one packed FFMA2
+// (fma.rn.f32x2: two independent fma.rn.f32, rounding unchanged).  Every
+// (token, expert, range) chain and the ordered sum of the range partials are
+// exactly those of router_kernel: logits are bit-identical.
 constexpr int kXStages = 2;
+
+__device__ __forceinline__ uint64_t f2dup(float a) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ void ffma2(uint64_t& acc, uint64_t a, uint64_t b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ float2 f2split(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
 
 template <int NE, int TPL, int CH>
 struct RouterTmaGeo {
+  static_assert(NE % 4 == 0, "expert quads");
   static constexpr int kTB = 32 * TPL;                       // tokens per CTA
   static constexpr int kXBytes = kTB * CH * 2;               // token box per warp-stage
   static constexpr int kWBytes = NE * CH * 2;                // router box per warp-stage
   static constexpr int kStageBytes = kXBytes + kWBytes;
-  // narrow routers (NE <= 16) re-expand each router chunk to fp32 once per warp:
-  // 2 broadcast fp32 loads per 8 FMAs beat 1 bf16 load + 8 unpacks when the
-  // loop is issue-bound; wide routers are smem-bandwidth-bound and keep bf16
-  static constexpr bool kF32W = NE <= 16;
-  static constexpr int kWF32Bytes = kF32W ? NE * CH * 4 : 0;  // per warp
-  static constexpr int kRing = kRanges * (kXStages * kStageBytes + kWF32Bytes);
+  static constexpr int kWT = CH * NE * 4;                    // fp32 [j][e] router chunk per warp
+  static constexpr int kRing = kRanges * (kXStages * kStageBytes + kWT);
   static constexpr int kPart = kRanges * NE * (kTB + 1) * 4;  // partial table (overlays the rings)
   static constexpr int kSmem = (kRing > kPart ? kRing : kPart) + 1024;
 };
@@ -302,8 +315,8 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
   uint8_t* dsm = smem_align1024(dsm_raw);
   __shared__ __align__(8) uint64_t bars[kRanges][kXStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = dsm + warp * (kXStages * G::kStageBytes + G::kWF32Bytes);
-  float* wf32 = reinterpret_cast<float*>(ring + kXStages * G::kStageBytes);  // [NE][CH] (kF32W)
+  uint8_t* ring = dsm + warp * (kXStages * G::kStageBytes + G::kWT);
+  float* wT = reinterpret_cast<float*>(ring + kXStages * G::kStageBytes);  // [CH][NE]
   uint64_t* bar = bars[warp];
   const int tb0 = blockIdx.x * kTB;
   const int hr = h / kRanges, j0 = warp * hr, nch = hr / CH;
@@ -322,11 +335,11 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
   };
   for (int c = 0; c < kXStages && c < nch; ++c) issue(c, c);
 
-  float acc[TPL][NE];
+  uint64_t acc2[TPL][NE / 2];  // chains (token i, e) and (token i, e+1) as one fp32 pair
 #pragma unroll
   for (int i = 0; i < TPL; ++i)
 #pragma unroll
-    for (int e = 0; e < NE; ++e) acc[i][e] = 0.f;
+    for (int e = 0; e < NE / 2; ++e) acc2[i][e] = 0ull;
   // swizzle phase of rows lane and lane + 32: 16-byte chunk c of row r sits at
   // c ^ (r & 7) (128B rows) or c ^ ((r >> 1) & 3) (64B rows)
   const int sw = CH == 64 ? (lane & 7) : ((lane >> 1) & 3);
@@ -335,18 +348,20 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
     mbar_wait(&bar[stage], (c / kXStages) & 1);
     const uint8_t* xst = ring + stage * G::kStageBytes;
     const uint4* wst = reinterpret_cast<const uint4*>(xst + G::kXBytes);  // [NE][CH/8] 16-byte vectors
-    if (G::kF32W) {
 #pragma unroll
-      for (int it = lane; it < NE * CH / 8; it += 32) {
-        const uint4 wv = wst[it];
-        const float2 a0 = unpack_bf16x2(wv.x), a1 = unpack_bf16x2(wv.y), a2 = unpack_bf16x2(wv.z),
-                     a3 = unpack_bf16x2(wv.w);
-        reinterpret_cast<float4*>(wf32 + it * 8)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
-        reinterpret_cast<float4*>(wf32 + it * 8)[1] = make_float4(a2.x, a2.y, a3.x, a3.y);
+    for (int it = lane; it < NE * CH / 8; it += 32) {
+      const int e = it / (CH / 8), v = it % (CH / 8);
+      const uint4 wv = wst[it];
+      const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = unpack_bf16x2(ww[q]);
+        wT[(8 * v + 2 * q) * NE + e] = f.x;
+        wT[(8 * v + 2 * q + 1) * NE + e] = f.y;
       }
-      __syncwarp();
     }
-#pragma unroll(G::kF32W ? 2 : 1)
+    __syncwarp();
+#pragma unroll 2
     for (int v = 0; v < CH / 8; ++v) {
       float xf[TPL][8];
 #pragma unroll
@@ -361,30 +376,23 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
         }
       }
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        float wf[8];  // same address in every lane: broadcast loads
-        if (G::kF32W) {
-          const float4 w0 = reinterpret_cast<const float4*>(wf32 + e * CH + v * 8)[0];
-          const float4 w1 = reinterpret_cast<const float4*>(wf32 + e * CH + v * 8)[1];
-          wf[0] = w0.x; wf[1] = w0.y; wf[2] = w0.z; wf[3] = w0.w;
-          wf[4] = w1.x; wf[5] = w1.y; wf[6] = w1.z; wf[7] = w1.w;
-        } else {
-          const uint4 wv = wst[e * (CH / 8) + v];
-          const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+      for (int q = 0; q < 8; ++q) {
+        uint64_t xd[TPL];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f = unpack_bf16x2(ww[q]);
-            wf[2 * q] = f.x;
-            wf[2 * q + 1] = f.y;
+        for (int i = 0; i < TPL; ++i) xd[i] = f2dup(xf[i][q]);
+        const ulonglong2* wrow = reinterpret_cast<const ulonglong2*>(wT + (8 * v + q) * NE);
+#pragma unroll
+        for (int e4 = 0; e4 < NE / 4; ++e4) {
+          const ulonglong2 w4 = wrow[e4];  // same address in every lane: broadcast
+#pragma unroll
+          for (int i = 0; i < TPL; ++i) {
+            ffma2(acc2[i][2 * e4], xd[i], w4.x);
+            ffma2(acc2[i][2 * e4 + 1], xd[i], w4.y);
           }
         }
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-#pragma unroll
-          for (int i = 0; i < TPL; ++i) acc[i][e] = __fmaf_rn(xf[i][q], wf[q], acc[i][e]);
       }
     }
-    __syncwarp();  // stage consumed by every lane
+    __syncwarp();  // stage and router chunk consumed by every lane
     if (c + kXStages < nch) issue(c + kXStages, stage);
   }
   __syncthreads();  // the partial table below overlays other warps' stages
@@ -392,7 +400,11 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
 #pragma unroll
   for (int i = 0; i < TPL; ++i)
 #pragma unroll
-    for (int e = 0; e < NE; ++e) part[(warp * NE + e) * (kTB + 1) + lane + 32 * i] = acc[i][e];
+    for (int e2 = 0; e2 < NE / 2; ++e2) {
+      const float2 f = f2split(acc2[i][e2]);
+      part[(warp * NE + 2 * e2) * (kTB + 1) + lane + 32 * i] = f.x;
+      part[(warp * NE + 2 * e2 + 1) * (kTB + 1) + lane + 32 * i] = f.y;
+    }
   __syncthreads();
   if (threadIdx.x >= kTB) return;
   const int tl = threadIdx.x, t = tb0 + tl;
@@ -448,18 +460,20 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
     constexpr int CH = 32;
     using G = RouterTmaGeo<NE, TPL, CH>;
     static_assert(G::kSmem <= 227 * 1024, "router smem");
+    auto kern = router_tma_kernel<NE, TPL, CH>;
+    const int smem_tma = G::kSmem;
     if (h % (kRanges * CH) == 0) {
       static int configured_tma = 0;
       if (!configured_tma) {
-        if (configure_smem((const void*)router_tma_kernel<NE, TPL, CH>, G::kSmem)) return HAP_ERR_LAUNCH;
+        if (configure_smem((const void*)kern, smem_tma)) return HAP_ERR_LAUNCH;
         configured_tma = 1;
       }
       CUtensorMap tmX, tmW;
       if (!encode_tmap_2d_bf16_sw(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, CH, G::kTB, CH * 2) ||
           !encode_tmap_2d_bf16_sw(&tmW, w, (uint64_t)h, (uint64_t)(E + has_shared), (uint64_t)h * 2, CH, NE, 0))
         return HAP_ERR_DRIVER;
-      { if (hap::launch_k(router_tma_kernel<NE, TPL, CH>, dim3((unsigned)((T + G::kTB - 1) / G::kTB)), dim3(kThreads),
-                          G::kSmem, st, tmX, tmW, (int)T, (int)h, (int)E, (int)k, renorm, has_shared, idx, tw, sg,
+      { if (hap::launch_k(kern, dim3((unsigned)((T + G::kTB - 1) / G::kTB)), dim3(kThreads),
+                          smem_tma, st, tmX, tmW, (int)T, (int)h, (int)E, (int)k, renorm, has_shared, idx, tw, sg,
                           logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
       HAP_CHECK_LAUNCH();
       return HAP_OK;
