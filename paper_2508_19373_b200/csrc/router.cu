@@ -275,19 +275,6 @@ __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* _
 // exactly those of router_kernel: logits are bit-identical.
 constexpr int kXStages = 2;
 
-__device__ __forceinline__ uint64_t f2dup(float a) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
-  return r;
-}
-__device__ __forceinline__ void ffma2(uint64_t& acc, uint64_t a, uint64_t b) {
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
-}
-__device__ __forceinline__ float2 f2split(uint64_t v) {
-  float2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-  return r;
-}
 
 template <int NE, int TPL, int CH>
 struct RouterTmaGeo {
