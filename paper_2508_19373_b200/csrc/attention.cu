@@ -262,6 +262,52 @@ __global__ void __launch_bounds__(kMergeWarps * 32) decode_merge_kernel(const fl
   if (item >= B * n_q) return;
   const int b = item / n_q, hq = item - b * n_q;
   const int64_t base = (int64_t)item * n_splits;  // == (b * n_q + hq) * n_splits
+  if (n_splits <= 32 && D == 128) {
+    // one split per lane: the (m, l) pairs and the first 8 partial rows are
+    // all requested before any reduction, so the merge costs ~2 memory round
+    // trips instead of one per dependent pass
+    constexpr int kPre = 8;
+    const int d0 = lane * 4;
+    float4 pre[kPre];
+#pragma unroll
+    for (int s2 = 0; s2 < kPre; ++s2)
+      pre[s2] = s2 < n_splits ? *reinterpret_cast<const float4*>(ws_o + (base + s2) * D + d0)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float m = lane < n_splits ? ws_ml[(base + lane) * 2] : -INFINITY;
+    const float l = lane < n_splits ? ws_ml[(base + lane) * 2 + 1] : 0.f;
+    float M = m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float wgt = m != -INFINITY ? exp2f(m - M) : 0.f;
+    float den = wgt * l;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int s2 = 0; s2 < kPre; ++s2) {
+      const float w2 = __shfl_sync(0xffffffffu, wgt, s2);
+      if (s2 < n_splits) {
+        num.x = fmaf(w2, pre[s2].x, num.x);
+        num.y = fmaf(w2, pre[s2].y, num.y);
+        num.z = fmaf(w2, pre[s2].z, num.z);
+        num.w = fmaf(w2, pre[s2].w, num.w);
+      }
+    }
+#pragma unroll 4
+    for (int s2 = kPre; s2 < n_splits; ++s2) {
+      const float w2 = __shfl_sync(0xffffffffu, wgt, s2);
+      const float4 o4 = *reinterpret_cast<const float4*>(ws_o + (base + s2) * D + d0);
+      num.x = fmaf(w2, o4.x, num.x);
+      num.y = fmaf(w2, o4.y, num.y);
+      num.z = fmaf(w2, o4.z, num.z);
+      num.w = fmaf(w2, o4.w, num.w);
+    }
+    __nv_bfloat16* orow = out + (int64_t)b * ldo + (int64_t)hq * D + d0;
+    *reinterpret_cast<uint2*>(orow) =
+        make_uint2(pack_bf16x2(num.x * inv, num.y * inv), pack_bf16x2(num.z * inv, num.w * inv));
+    return;
+  }
   float M = -INFINITY;
   for (int s2 = lane; s2 < n_splits; s2 += 32) M = fmaxf(M, ws_ml[(base + s2) * 2]);
 #pragma unroll
