@@ -481,6 +481,28 @@ static int pick_bn(int64_t N) {
 // order, then the same epilogue math as the TMEM path (bias, residual, SwiGLU,
 // RoPE with inv_freq = 1/theta^(2i/d)), one bf16 rounding.
 __device__ __forceinline__ void sum_slices8(const float* part, int64_t slice, int ks, int64_t off, float (&f)[8]) {
+  if (ks <= 4) {
+    // every slice's load in flight before the first add (one memory round
+    // trip instead of ks); the sum order is unchanged
+    float4 a[4], b[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (s < ks) {
+        a[s] = __ldcg(reinterpret_cast<const float4*>(part + s * slice + off));
+        b[s] = __ldcg(reinterpret_cast<const float4*>(part + s * slice + off + 4));
+      }
+    }
+    f[0] = a[0].x; f[1] = a[0].y; f[2] = a[0].z; f[3] = a[0].w;
+    f[4] = b[0].x; f[5] = b[0].y; f[6] = b[0].z; f[7] = b[0].w;
+#pragma unroll
+    for (int s = 1; s < 4; ++s) {
+      if (s < ks) {
+        f[0] += a[s].x; f[1] += a[s].y; f[2] += a[s].z; f[3] += a[s].w;
+        f[4] += b[s].x; f[5] += b[s].y; f[6] += b[s].z; f[7] += b[s].w;
+      }
+    }
+    return;
+  }
   float4 a = __ldcg(reinterpret_cast<const float4*>(part + off));
   float4 b = __ldcg(reinterpret_cast<const float4*>(part + off + 4));
   f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
