@@ -484,6 +484,8 @@ def main():
                 ach, peak, unit = wk / (ms / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"
             kernels[name] = {"ms": ms, "bound": bound, "work": wk, "achieved": ach, "peak": peak, "unit": unit,
                              "frac": ach / peak}
+            if bound == "hbm":  # the north star's ~8 TB/s denominator beside the measured copy peak
+                kernels[name]["frac_of_8TBps"] = ach / 8000.0
 
     # -- decode HBM roofline (whole step)
     decode = None
