@@ -232,7 +232,10 @@ int hap_rope_qk(void* qkv, int64_t T, int64_t ld, int64_t n_q_heads, int64_t n_k
  * Causal (or full) GQA prefill attention on tcgen05/TMEM, bf16 in/out, fp32
  * softmax.  Token (s, i) = row s*seq_len + i.  q/k/v/out addressed by leading
  * dims (multiples of 8, 16-byte aligned bases); head h of a row starts at
- * column h*head_dim.  head_dim in {64, 128}.
+ * column h*head_dim.  head_dim in {64, 128}.  The persistent kernel hands out
+ * work through a per-device ticket counter that it re-zeroes on exit, so calls
+ * on one device must not overlap in time (issue them on one stream, or order
+ * the streams).
  * Replaces: score+value term 4*n*kv_len*h of attention_flops (arch.py:161).
  */
 int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
