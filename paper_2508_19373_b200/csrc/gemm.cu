@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
         for (int kb = kb0; kb < kb1; ++kb) {
           const bool pre = u == tile0 && kb - kb0 < npre;  // B already in flight
-          if (!pre) mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (!pre) mbar_wait_spin(&empty_bar[stage], phase ^ 1);
           if (kPair == 1) {
             if (!pre) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
             tma_load_2d(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, kEvictNormal);
@@ -269,11 +269,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        mbar_wait_spin(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+          mbar_wait_spin(&full_bar[stage], phase);
           tc_fence_after();
           const uint64_t da = make_sdesc_sw128(smem_u32(smA + stage * kABytes));
           const uint64_t db = make_sdesc_sw128(smem_u32(smB + stage * kBBytes));
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tfull_bar[acc], acc_phase);
+      mbar_wait_spin(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = c.m0 + (int)crank * BM + q * 32 + lane;
       const bool row_ok = row < c.m_end;
