@@ -422,6 +422,26 @@ def test_attn_decode_many_items_per_warp():
         assert rel_err(np32(out[b]), ref) < 2e-2
 
 
+@pytest.mark.parametrize("nq,nkv,S,B", [(6, 2, 300, 2), (4, 4, 640, 1)])
+def test_attn_prefill_noncausal_qtile_pairs(nq, nkv, S, B):
+    """Odd GQA group (q-tile pairing, incl. a lone last tile) without the causal mask."""
+    d = 128
+    T = B * S
+    qkv = bf16((T, (nq + 2 * nkv) * d), seed=31)
+    out = torch.empty(T, nq * d, device=dev, dtype=torch.bfloat16)
+    K().attn_prefill(qkv, nq, nkv, d, B, S, out, causal=False)
+    torch.cuda.synchronize()
+    a = np32(qkv)
+    ref = []
+    for s0 in range(B):
+        blk = a[s0 * S:(s0 + 1) * S]
+        q = blk[:, :nq * d].reshape(S, nq, d)
+        k = blk[:, nq * d:(nq + nkv) * d].reshape(S, nkv, d)
+        v = blk[:, (nq + nkv) * d:].reshape(S, nkv, d)
+        ref.append(O.attention(q, k, v, causal=False).reshape(S, -1))
+    assert rel_err(np32(out), np.concatenate(ref)) < 2e-2
+
+
 @pytest.mark.parametrize("causal", [True, False])
 def test_attn_prefill_large_scores_and_noncausal(causal):
     """Scores spanning ~+-40 (q, k ~ N(0, 4^2)): the running max moves by more than
