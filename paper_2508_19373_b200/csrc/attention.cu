@@ -250,6 +250,76 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
 // the max and the weighted denominator are warp reductions, and every lane
 // accumulates D/32 output columns over the splits with all partial loads of a
 // split in flight at once.  Splits with m = -inf (past the sequence) weigh 0.
+// Many splits (small batches: few (sequence, kv head) items, so the key range
+// is cut finely): one CTA of 8 warps per (sequence, q head); warp w folds splits
+// w, w+8, ... and the 8 partial rows are summed in warp order (deterministic).
+constexpr int kWideMergeWarps = 8;
+__global__ void __launch_bounds__(kWideMergeWarps * 32) decode_merge_wide_kernel(
+    const float* __restrict__ ws_o, const float* __restrict__ ws_ml, int n_splits, int n_q, int D,
+    __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[kWideMergeWarps];
+  __shared__ float num_s[kWideMergeWarps][128];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int item = blockIdx.x;
+  const int b = item / n_q, hq = item - b * n_q;
+  const int64_t base = (int64_t)item * n_splits;
+  float M = -INFINITY;
+  for (int s2 = tid; s2 < n_splits; s2 += blockDim.x) M = fmaxf(M, ws_ml[(base + s2) * 2]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  if (lane == 0) red[warp] = M;
+  __syncthreads();
+  M = red[0];
+#pragma unroll
+  for (int w = 1; w < kWideMergeWarps; ++w) M = fmaxf(M, red[w]);
+  __syncthreads();
+  float den = 0.f;
+  for (int s2 = tid; s2 < n_splits; s2 += blockDim.x) {
+    const float m = ws_ml[(base + s2) * 2];
+    if (m != -INFINITY) den = fmaf(exp2f(m - M), ws_ml[(base + s2) * 2 + 1], den);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+  if (lane == 0) red[warp] = den;
+  __syncthreads();
+  den = 0.f;
+#pragma unroll
+  for (int w = 0; w < kWideMergeWarps; ++w) den += red[w];
+  const float inv = den > 0.f ? 1.f / den : 0.f;
+  for (int db = 0; db < D; db += 128) {  // uniform trip count: the loop holds __syncthreads
+    const int d0 = db + lane * 4;
+    const bool act = d0 < D;
+    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int s2 = warp; act && s2 < n_splits; s2 += kWideMergeWarps) {
+      const float m = ws_ml[(base + s2) * 2];
+      if (m == -INFINITY) continue;
+      const float wgt = exp2f(m - M);
+      const float4 o4 = *reinterpret_cast<const float4*>(ws_o + (base + s2) * D + d0);
+      num.x = fmaf(wgt, o4.x, num.x);
+      num.y = fmaf(wgt, o4.y, num.y);
+      num.z = fmaf(wgt, o4.z, num.z);
+      num.w = fmaf(wgt, o4.w, num.w);
+    }
+    __syncthreads();
+    *reinterpret_cast<float4*>(&num_s[warp][lane * 4]) = num;
+    __syncthreads();
+    if (warp == 0 && act) {
+      float4 t = *reinterpret_cast<const float4*>(&num_s[0][lane * 4]);
+#pragma unroll
+      for (int w = 1; w < kWideMergeWarps; ++w) {
+        const float4 u = *reinterpret_cast<const float4*>(&num_s[w][lane * 4]);
+        t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+      }
+      __nv_bfloat16* orow = out + (int64_t)b * ldo + (int64_t)hq * D + d0;
+      *reinterpret_cast<uint2*>(orow) =
+          make_uint2(pack_bf16x2(t.x * inv, t.y * inv), pack_bf16x2(t.z * inv, t.w * inv));
+    }
+  }
+}
+
 constexpr int kMergeWarps = 4;
 __global__ void __launch_bounds__(kMergeWarps * 32) decode_merge_kernel(const float* __restrict__ ws_o,
                                                                         const float* __restrict__ ws_ml, int n_splits,
@@ -514,8 +584,17 @@ extern "C" int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, vo
   const int rc = head_dim == 128 ? launch_decode<128>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st)
                                  : launch_decode<64>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st);
   if (rc != HAP_OK) return rc;
-  { if (hap::launch_k(decode_merge_kernel, dim3((unsigned)((B * n_q_heads + kMergeWarps - 1) / kMergeWarps)), dim3(kMergeWarps * 32), 0, st, ws_o, ws_ml, ns, (int)n_q_heads, (int)B, (int)head_dim,
-                                                                              reinterpret_cast<__nv_bfloat16*>(out), ldo) != cudaSuccess) return HAP_ERR_LAUNCH; }
+  if (ns > 32) {
+    if (hap::launch_k(decode_merge_wide_kernel, dim3((unsigned)(B * n_q_heads)), dim3(kWideMergeWarps * 32), 0, st,
+                      ws_o, ws_ml, ns, (int)n_q_heads, (int)head_dim, reinterpret_cast<__nv_bfloat16*>(out),
+                      ldo) != cudaSuccess)
+      return HAP_ERR_LAUNCH;
+  } else {
+    if (hap::launch_k(decode_merge_kernel, dim3((unsigned)((B * n_q_heads + kMergeWarps - 1) / kMergeWarps)),
+                      dim3(kMergeWarps * 32), 0, st, ws_o, ws_ml, ns, (int)n_q_heads, (int)B, (int)head_dim,
+                      reinterpret_cast<__nv_bfloat16*>(out), ldo) != cudaSuccess)
+      return HAP_ERR_LAUNCH;
+  }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
 }

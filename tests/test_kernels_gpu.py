@@ -400,6 +400,30 @@ def test_attn_decode(d, nq, nkv):
         assert rel_err(np32(out[b]), ref) < 2e-2
 
 
+@pytest.mark.parametrize("d,nq,nkv,L", [(128, 28, 4, 2048), (64, 8, 2, 4000)])
+def test_attn_decode_single_sequence_many_splits(d, nq, nkv, L):
+    """B = 1: the key range is cut into > 32 splits (wide merge kernel)."""
+    B = 1
+    qkv = bf16((B, (nq + 2 * nkv) * d), seed=23)
+    kc = bf16((B, nkv, L, d), seed=24)
+    vc = bf16((B, nkv, L, d), seed=25)
+    pos = torch.tensor([L - 1], device=dev, dtype=torch.int32)
+    kc0, vc0 = np32(kc), np32(vc)
+    ops = K()
+    out = torch.empty(B, nq * d, device=dev, dtype=torch.bfloat16)
+    ws = torch.empty(ops.attn_decode_workspace_bytes(B, nq, d, L), device=dev, dtype=torch.uint8)
+    ops.attn_decode(qkv, kc, vc, pos, nq, nkv, d, out, ws)
+    torch.cuda.synchronize()
+    a = np32(qkv)
+    p = L - 1
+    knew = a[0, nq * d:(nq + nkv) * d].reshape(nkv, d)
+    vnew = a[0, (nq + nkv) * d:].reshape(nkv, d)
+    kk = np.concatenate([kc0[0, :, :p], knew[:, None]], 1).transpose(1, 0, 2)
+    vv = np.concatenate([vc0[0, :, :p], vnew[:, None]], 1).transpose(1, 0, 2)
+    ref = O.attention(a[0, :nq * d].reshape(1, nq, d), kk, vv, causal=True).reshape(-1)
+    assert rel_err(np32(out[0]), ref) < 2e-2
+
+
 def test_attn_decode_many_items_per_warp():
     """More (sequence, kv head, split) items than warp workers, ragged lengths:
     every warp walks several items through its TMA ring."""
