@@ -188,6 +188,92 @@ __global__ void __launch_bounds__(kRanges * NE) router_small_kernel(const __nv_b
   finish_token<NE>(tot, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
 }
 
+// Small T, wide router (rows > 8): one CTA per (token, group of 8 router rows)
+// instead of one per token, so a decode step with few tokens streams the
+// router rows on rows/8 SMs.  Chains and range order are those of
+// router_small_kernel (bit-identical logits); each CTA parks its 8 logits in a
+// device scratch row, and the token's last CTA (atomic count, reset by itself)
+// runs the softmax / top-k.  One launch in flight per device.
+constexpr int kGroupRows = 8;
+constexpr int kMaxRouterRows = 80;
+__device__ float g_router_logits[kSmallT * kMaxRouterRows];
+__device__ int g_router_cnt[kSmallT];
+
+template <int NE>
+__global__ void __launch_bounds__(kRanges * kGroupRows) router_group_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w, int T, int h, int n_rows_w, int E,
+    int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+    float* __restrict__ shared_gate, float* __restrict__ logits_out) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ uint4 xs[];  // token row (h/8 vectors), then the group's (row, range) segments
+  __shared__ float part[kRanges][kGroupRows];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int last_s;
+  const int t = blockIdx.x, g = blockIdx.y, n_groups = gridDim.y;
+  const int p = threadIdx.x / kGroupRows, el = threadIdx.x % kGroupRows, e = g * kGroupRows + el;
+  const int hr = h / kRanges, nv = hr / 8;
+  const int rows_here = min(kGroupRows, n_rows_w - g * kGroupRows);
+  // token row and this group's router rows arrive by 1D bulk copies in one
+  // round trip; segments nv+1 vectors apart keep the threads' reads in
+  // different banks
+  uint4* ws = xs + h / 8;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)(h * 2) * (uint32_t)(1 + rows_here));
+    bulk_load(xs, x + (int64_t)t * h, (uint32_t)(h * 2), &bar);
+    for (int r = 0; r < rows_here * kRanges; ++r) {
+      const int rl = r / kRanges, pp = r % kRanges;
+      bulk_load(ws + (rl * kRanges + pp) * (nv + 1), w + (int64_t)(g * kGroupRows + rl) * h + pp * hr,
+                (uint32_t)(hr * 2), &bar);
+    }
+  }
+  mbar_wait(&bar, 0);
+  float acc = 0.f;
+  if (e < n_rows_w) {
+    const uint4* wr = ws + (el * kRanges + p) * (nv + 1);
+    const uint4* xr = xs + p * nv;
+#pragma unroll 4
+    for (int v = 0; v < nv; ++v) {
+      const uint4 wv = wr[v];
+      const uint4 xv = xr[v];
+      const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+      const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 fx = unpack_bf16x2(xw[q]);
+        const float2 fw = unpack_bf16x2(ww[q]);
+        acc = __fmaf_rn(fx.x, fw.x, acc);
+        acc = __fmaf_rn(fx.y, fw.y, acc);
+      }
+    }
+  }
+  part[p][el] = acc;
+  __syncthreads();
+  if (threadIdx.x < kGroupRows && e < n_rows_w) {
+    float s2 = part[0][el];
+#pragma unroll
+    for (int pp = 1; pp < kRanges; ++pp) s2 = __fadd_rn(s2, part[pp][el]);
+    g_router_logits[(int64_t)t * kMaxRouterRows + e] = s2;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last_s = atomicAdd(&g_router_cnt[t], 1) == n_groups - 1;
+  __syncthreads();
+  if (!last_s || threadIdx.x != 0) return;
+  __threadfence();
+  g_router_cnt[t] = 0;  // ready for the next launch
+  float tot[NE];
+#pragma unroll
+  for (int ee = 0; ee < NE; ++ee)
+    tot[ee] = ee < n_rows_w ? __ldcg(&g_router_logits[(int64_t)t * kMaxRouterRows + ee]) : 0.f;
+  finish_token<NE>(tot, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
+}
+
 template <int NE>
 __global__ void __launch_bounds__(kThreads) router_kernel(const __nv_bfloat16* __restrict__ x,
                                                           const __nv_bfloat16* __restrict__ w, int T, int h,
@@ -434,6 +520,22 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
     }();
     const bool stage = allow_stage && xs_bytes + ws_bytes <= kStageLimit && (reinterpret_cast<uintptr_t>(w) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const int gs_bytes = xs_bytes + kGroupRows * kRanges * (int)(h / kRanges / 8 + 1) * 16;
+    if (!stage && E + has_shared > kGroupRows && E + has_shared <= kMaxRouterRows && gs_bytes <= kStageLimit &&
+        ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(x)) & 15) == 0) {
+      static int configured_group = 0;
+      if (!configured_group) {
+        if (configure_smem((const void*)router_group_kernel<NE>, kStageLimit)) return HAP_ERR_LAUNCH;
+        configured_group = 1;
+      }
+      const int n_groups = (int)((E + has_shared + kGroupRows - 1) / kGroupRows);
+      { if (hap::launch_k(router_group_kernel<NE>, dim3((unsigned)T, (unsigned)n_groups), dim3(kRanges * kGroupRows),
+                          gs_bytes, st, reinterpret_cast<const __nv_bfloat16*>(x),
+                          reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared), (int)E,
+                          (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
+      HAP_CHECK_LAUNCH();
+      return HAP_OK;
+    }
     auto kern = stage ? router_small_kernel<NE, true> : router_small_kernel<NE, false>;
     { if (hap::launch_k(kern, dim3((int)T), dim3(kRanges * NE), stage ? xs_bytes + ws_bytes : xs_bytes, st,
         reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h,
