@@ -605,8 +605,21 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(Params p) {
 static void plan_split(Params& p, int64_t a_rows, int64_t K, int64_t N, int64_t n_segs, size_t ws_bytes) {
   p.ksplit = 1;
   auto tiles = [&](int64_t bn) { return ((a_rows + BM - 1) / BM + (n_segs - 1)) * ((N + bn - 1) / bn); };
-  if (2 * tiles(p.BN) > kNumSMs || N % 8) return;
+  if (N % 8) return;
   const int64_t num_kb = (K + BK - 1) / BK;
+  if (2 * tiles(p.BN) > kNumSMs) {
+    // Many tiles, but a badly quantised last wave (e.g. 160 tiles = 1.08 waves
+    // on 148 SMs: the weight stream takes two rounds).  Dense launches only —
+    // a grouped launch's real tile count is known on the device alone.
+    if (n_segs != 1) return;
+    const int64_t t = tiles(p.BN);
+    auto rounds = [&](int64_t ks) { return (double)((t * ks + kNumSMs - 1) / kNumSMs) / (double)ks; };
+    int64_t best = 1;
+    for (int64_t ks = 2; ks <= 8 && ks <= num_kb / 4; ++ks)
+      if ((size_t)ks * a_rows * N * sizeof(float) <= ws_bytes && rounds(ks) < rounds(best)) best = ks;
+    if (rounds(best) <= 0.85 * rounds(1)) p.ksplit = (int32_t)best;
+    return;
+  }
   int64_t cands[3] = {p.BN, 0, 0};
   int nc = 1;
   if (p.epi == HAP_EPI_STORE) {
