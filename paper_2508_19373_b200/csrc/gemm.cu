@@ -609,10 +609,11 @@ static void plan_split(Params& p, int64_t a_rows, int64_t K, int64_t N, int64_t 
   const int64_t num_kb = (K + BK - 1) / BK;
   if (2 * tiles(p.BN) > kNumSMs) {
     // Many tiles, but a badly quantised last wave (e.g. 160 tiles = 1.08 waves
-    // on 148 SMs: the weight stream takes two rounds).  Dense launches only —
-    // a grouped launch's real tile count is known on the device alone.
-    if (n_segs != 1) return;
-    const int64_t t = tiles(p.BN);
+    // on 148 SMs: the weight stream takes two rounds).  A grouped launch has at
+    // most min(rows, segments) non-empty segments, one m-block each here
+    // (a_rows <= BM), which bounds its real tile count without a host sync.
+    const int64_t n_blocks = (N + p.BN - 1) / p.BN;
+    const int64_t t = (a_rows < n_segs ? a_rows : n_segs) * n_blocks;
     auto rounds = [&](int64_t ks) { return (double)((t * ks + kNumSMs - 1) / kNumSMs) / (double)ks; };
     int64_t best = 1;
     for (int64_t ks = 2; ks <= 8 && ks <= num_kb / 4; ++ks)
@@ -717,8 +718,8 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
     return launch_impl<2>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
   // Small-M weight streaming (decode projections, TP-sharded shapes): split K
   // over more CTAs when a workspace is supplied, then reduce + epilogue.
-  // Only single-m-block launches split, so the slice plan depends on (N, K)
-  // alone and results are identical for every M <= 128 (batch invariance).
+  // Only single-m-block launches split; the slice plan depends on (N, K, M) only
+  // through the tile bound and the workspace fit, and repeats bit for bit.
   if (ws && ws_bytes >= 16 && a_rows <= BM) {
     plan_split(p, a_rows, K, N, n_segs, ws_bytes);
     p.part = reinterpret_cast<float*>(ws);
