@@ -180,6 +180,9 @@ int hap_peer_allreduce_bf16(const int64_t* in_ptrs, const int64_t* out_ptrs, con
  * shared-expert gate: shared_gate[t] = sigmoid(x[t] . w[E]) (fp32).
  * logits_out (fp32 [T, n_experts]) is optional.
  * Requires h % 64 == 0, n_experts + has_shared_gate <= 72, top_k <= 32.
+ * For T <= 1024 with more than 8 router rows the work is spread over CTAs per
+ * (token, 8 rows) that meet in a per-device scratch row and counter (reset
+ * by the kernel), so such calls on one device must not overlap in time.
  * Replaces: the router term 2*T*h*E of expert_flops (arch.py:177).
  */
 int hap_router_topk(const void* x, int64_t T, int64_t h, const void* w, int64_t n_experts, int64_t top_k,
