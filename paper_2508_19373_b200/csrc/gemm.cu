@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
                 float sn, cs;
-                sincosf(pos * inv_freq_s[i + k], &sn, &cs);
+                rope_sincos(pos * inv_freq_s[i + k], &sn, &cs);
                 y1[k] = x1[k] * cs - x2[k] * sn;
                 y2[k] = x2[k] * cs + x1[k] * sn;
               }
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(Params p) {
       for (int k = 0; k < 8; ++k) {
         const float inv_freq = 1.0f / powf(p.theta, (float)(2 * (i0 + k)) / (float)d);
         float sn, cs;
-        sincosf(pos * inv_freq, &sn, &cs);
+        rope_sincos(pos * inv_freq, &sn, &cs);
         const float y1 = x1[k] * cs - x2[k] * sn;
         const float y2 = x2[k] * cs + x1[k] * sn;
         x1[k] = y1;
