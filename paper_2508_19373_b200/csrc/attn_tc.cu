@@ -530,7 +530,7 @@ template <int D, int kPoly, bool kSpin = true>  // kPoly of every 8 exp2 pairs o
 __global__ void __launch_bounds__(kThreads, 1)
     attn_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out, int64_t ldo, int S,
-                     int n_q, int n_kv, int n_seqs, float scale_log2, int causal) {
+                     int n_q, int n_kv, int n_seqs, float scale_log2, int causal, int st32) {
   pdl_trigger();
   pdl_wait();
   constexpr int kTile = PairSmem<D>::kTile;
@@ -820,13 +820,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_x32(tO(t) + lane_off + c, ov);
         tmem_ld_wait();
         if (qi < S) {
+          if (st32) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint32_t pk[4];
+            for (int i = 0; i < 32; i += 16) {
+              uint32_t pk[8];
 #pragma unroll
-            for (int k2 = 0; k2 < 4; ++k2)
-              pk[k2] = pack_bf16x2(__uint_as_float(ov[i + 2 * k2]) * inv, __uint_as_float(ov[i + 2 * k2 + 1]) * inv);
-            *reinterpret_cast<uint4*>(orow + c + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              for (int k2 = 0; k2 < 8; ++k2)
+                pk[k2] = pack_bf16x2(__uint_as_float(ov[i + 2 * k2]) * inv, __uint_as_float(ov[i + 2 * k2 + 1]) * inv);
+              st_global_v8(orow + c + i, pk);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int k2 = 0; k2 < 4; ++k2)
+                pk[k2] = pack_bf16x2(__uint_as_float(ov[i + 2 * k2]) * inv, __uint_as_float(ov[i + 2 * k2 + 1]) * inv);
+              *reinterpret_cast<uint4*>(orow + c + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
           }
         }
       }
@@ -869,7 +880,8 @@ static int launch_pair(const void* q, int64_t ldq, const void* k, int64_t ldk, c
   const unsigned grid = (unsigned)(n_items < kNumSMs ? n_items : kNumSMs);
   if (hap::launch_k(kern, dim3(grid), dim3(kThreads), PairSmem<D>::kTotal, st, mq, mk, mv,
                     reinterpret_cast<__nv_bfloat16*>(out), ldo, (int)S, (int)n_q, (int)n_kv, (int)n_seqs,
-                    scale * 1.4426950408889634f, causal) != cudaSuccess)
+                    scale * 1.4426950408889634f, causal,
+                    (int)(((reinterpret_cast<uintptr_t>(out) | (uintptr_t)(ldo * 2)) & 31) == 0)) != cudaSuccess)
     return HAP_ERR_LAUNCH;
   HAP_CHECK_LAUNCH();
   return HAP_OK;
