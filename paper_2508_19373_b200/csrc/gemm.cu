@@ -63,6 +63,7 @@ struct Params {
   int32_t rope_cols;
   float theta;
   int32_t group_m;  // raster group (m-blocks)
+  int32_t st32;     // C rows 32-byte aligned: 32-byte stores in the store epilogue
   // split-K (small-M, weight-streaming shapes): each tile's K range is cut in
   // ksplit slices computed by different CTAs; slice ks writes its fp32
   // partial to part[ks][row][col] (row-major over the B rows N) and
@@ -412,9 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_x32(t_row + j, v);
           tmem_ld_wait();
           if (row_ok) {
+            uint32_t o32[8];  // two 8-column groups gathered for one 32-byte store
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
               const int col = col0 + j + s * 8;
+              const bool pair32 = p.st32 && ((s & 1) ? col - 8 : col + 8) < p.out_cols;
               if (col < p.out_cols) {
                 float f[8];
 #pragma unroll
@@ -442,7 +445,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t o[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) o[i] = pack_bf16x2(f[2 * i], f[2 * i + 1]);
-                *reinterpret_cast<uint4*>(crow + col) = make_uint4(o[0], o[1], o[2], o[3]);
+                if (pair32) {
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) o32[(s & 1) * 4 + i] = o[i];
+                  if (s & 1) st_global_v8(crow + col - 8, o32);
+                } else {
+                  *reinterpret_cast<uint4*>(crow + col) = make_uint4(o[0], o[1], o[2], o[3]);
+                }
               }
             }
           }
@@ -674,6 +683,8 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
     const char* e = getenv("HAP_GEMM_RASTER_MB");  // tuning experiments only
     return e ? (int64_t)atoi(e) << 20 : kRasterL2Bytes;
   }();
+  p.st32 = (p.seg_dst == nullptr && p.C != nullptr &&
+            ((reinterpret_cast<uintptr_t>(p.C) | (uintptr_t)(p.ldc * 2)) & 31) == 0) ? 1 : 0;
   int64_t gm = l2_budget / (K * 2 * TM);
   p.group_m = (int32_t)(gm < 1 ? 1 : (gm > 1024 ? 1024 : gm));
   const int64_t max_tiles = ((a_rows + TM - 1) / TM + (n_segs - 1)) * n_blocks;
