@@ -335,20 +335,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (p.epi == HAP_EPI_SWIGLU) {
         const int hw = p.hw;
         const int col0 = c.n_blk * hw;
-        for (int j = 0; j < hw; j += 8) {
-          uint32_t g[8], u[8];
-          tmem_ld_x8(t_row + j, g);
-          tmem_ld_x8(t_row + hw + j, u);
-          tmem_ld_wait();
-          if (row_ok && col0 + j < p.out_cols) {
-            uint32_t o[4];
+        if (p.st32 && (hw & 15) == 0) {
+          // 16 output columns per step, one 32-byte store
+          for (int j = 0; j < hw; j += 16) {
+            uint32_t g[8], g2[8], u[8], u2[8];
+            tmem_ld_x8(t_row + j, g);
+            tmem_ld_x8(t_row + j + 8, g2);
+            tmem_ld_x8(t_row + hw + j, u);
+            tmem_ld_x8(t_row + hw + j + 8, u2);
+            tmem_ld_wait();
+            if (row_ok && col0 + j < p.out_cols) {
+              uint32_t o[8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
-              const float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
-              o[i] = pack_bf16x2(a0, a1);
+              for (int i = 0; i < 4; ++i) {
+                o[i] = pack_bf16x2(silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]),
+                                   silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]));
+                o[4 + i] = pack_bf16x2(silu(__uint_as_float(g2[2 * i])) * __uint_as_float(u2[2 * i]),
+                                       silu(__uint_as_float(g2[2 * i + 1])) * __uint_as_float(u2[2 * i + 1]));
+              }
+              if (col0 + j + 16 <= p.out_cols) {
+                st_global_v8(crow + col0 + j, o);
+              } else {
+                *reinterpret_cast<uint4*>(crow + col0 + j) = make_uint4(o[0], o[1], o[2], o[3]);
+                if (col0 + j + 8 < p.out_cols)
+                  *reinterpret_cast<uint4*>(crow + col0 + j + 8) = make_uint4(o[4], o[5], o[6], o[7]);
+              }
             }
-            *reinterpret_cast<uint4*>(crow + col0 + j) = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        } else {
+          for (int j = 0; j < hw; j += 8) {
+            uint32_t g[8], u[8];
+            tmem_ld_x8(t_row + j, g);
+            tmem_ld_x8(t_row + hw + j, u);
+            tmem_ld_wait();
+            if (row_ok && col0 + j < p.out_cols) {
+              uint32_t o[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+                const float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+                o[i] = pack_bf16x2(a0, a1);
+              }
+              *reinterpret_cast<uint4*>(crow + col0 + j) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
           }
         }
       } else if (p.epi == kEpiRope) {
@@ -683,7 +712,11 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
     const char* e = getenv("HAP_GEMM_RASTER_MB");  // tuning experiments only
     return e ? (int64_t)atoi(e) << 20 : kRasterL2Bytes;
   }();
-  p.st32 = (p.seg_dst == nullptr && p.C != nullptr &&
+  static const bool st32_ok = [] {
+    const char* e = getenv("HAP_GEMM_ST32");  // A/B experiments only
+    return !(e && e[0] == '0');
+  }();
+  p.st32 = (st32_ok && p.seg_dst == nullptr && p.C != nullptr &&
             ((reinterpret_cast<uintptr_t>(p.C) | (uintptr_t)(p.ldc * 2)) & 31) == 0) ? 1 : 0;
   int64_t gm = l2_budget / (K * 2 * TM);
   p.group_m = (int32_t)(gm < 1 ? 1 : (gm > 1024 ? 1024 : gm));
