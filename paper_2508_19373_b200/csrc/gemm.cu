@@ -322,12 +322,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_x32(t_row + j, v);
           tmem_ld_wait();
           if (row_ok) {
+            if (p.st32 && (p.N & 7) == 0 && (reinterpret_cast<uintptr_t>(p.part) & 31) == 0) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              if (j + i < ncols)
-                __stcg(reinterpret_cast<float4*>(dst + j + i),
-                       make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
-                                   __uint_as_float(v[i + 3])));
+              for (int i = 0; i < 32; i += 8)
+                if (j + i < ncols) {
+                  const uint32_t w8[8] = {v[i], v[i + 1], v[i + 2], v[i + 3], v[i + 4], v[i + 5], v[i + 6], v[i + 7]};
+                  st_global_v8(dst + j + i, w8);
+                }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                if (j + i < ncols)
+                  __stcg(reinterpret_cast<float4*>(dst + j + i),
+                         make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                                     __uint_as_float(v[i + 3])));
+            }
           }
         }
       }
