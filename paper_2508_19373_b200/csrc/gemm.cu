@@ -399,49 +399,58 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int hb = 0; hb < p.BN; hb += d) {
           const int hcol = col0 + hb;
           const bool rot = hcol < p.rope_cols;
-          for (int i = 0; i < half; i += 8) {
-            uint32_t a[8], b[8];
-            tmem_ld_x8(t_row + hb + i, a);
-            tmem_ld_x8(t_row + hb + half + i, b);
-            tmem_ld_wait();
+          // 8 rotation pairs per sub-step; with 32-byte stores two sub-steps
+          // (16 columns of each half) leave together
+          const bool wide = p.st32 && (half % 16) == 0;
+          for (int i = 0; i < half; i += (wide ? 16 : 8)) {
+            uint32_t o1w[8], o2w[8];
+#pragma unroll
+            for (int sub = 0; sub < 2; ++sub) {
+              if (sub == 1 && !wide) break;
+              const int ii = i + sub * 8;
+              uint32_t a[8], b[8];
+              tmem_ld_x8(t_row + hb + ii, a);
+              tmem_ld_x8(t_row + hb + half + ii, b);
+              tmem_ld_wait();
+              if (!row_ok || hcol >= p.out_cols) continue;
+              float x1[8], x2[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                x1[k] = __uint_as_float(a[k]);
+                x2[k] = __uint_as_float(b[k]);
+              }
+              if (p.bias) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  x1[k] += __bfloat162float(p.bias[hcol + ii + k]);
+                  x2[k] += __bfloat162float(p.bias[hcol + half + ii + k]);
+                }
+              }
+              if (rot) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  float sn, cs;
+                  rope_sincos(pos * inv_freq_s[ii + k], &sn, &cs);
+                  const float y1 = x1[k] * cs - x2[k] * sn;
+                  const float y2 = x2[k] * cs + x1[k] * sn;
+                  x1[k] = y1;
+                  x2[k] = y2;
+                }
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                o1w[sub * 4 + k] = pack_bf16x2(x1[2 * k], x1[2 * k + 1]);
+                o2w[sub * 4 + k] = pack_bf16x2(x2[2 * k], x2[2 * k + 1]);
+              }
+            }
             if (!row_ok || hcol >= p.out_cols) continue;
-            float x1[8], x2[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              x1[k] = __uint_as_float(a[k]);
-              x2[k] = __uint_as_float(b[k]);
-            }
-            if (p.bias) {
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                x1[k] += __bfloat162float(p.bias[hcol + i + k]);
-                x2[k] += __bfloat162float(p.bias[hcol + half + i + k]);
-              }
-            }
-            uint32_t o1[4], o2[4];
-            if (rot) {
-              float y1[8], y2[8];
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                float sn, cs;
-                rope_sincos(pos * inv_freq_s[i + k], &sn, &cs);
-                y1[k] = x1[k] * cs - x2[k] * sn;
-                y2[k] = x2[k] * cs + x1[k] * sn;
-              }
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                o1[k] = pack_bf16x2(y1[2 * k], y1[2 * k + 1]);
-                o2[k] = pack_bf16x2(y2[2 * k], y2[2 * k + 1]);
-              }
+            if (wide) {
+              st_global_v8(crow + hcol + i, o1w);
+              st_global_v8(crow + hcol + half + i, o2w);
             } else {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                o1[k] = pack_bf16x2(x1[2 * k], x1[2 * k + 1]);
-                o2[k] = pack_bf16x2(x2[2 * k], x2[2 * k + 1]);
-              }
+              *reinterpret_cast<uint4*>(crow + hcol + i) = make_uint4(o1w[0], o1w[1], o1w[2], o1w[3]);
+              *reinterpret_cast<uint4*>(crow + hcol + half + i) = make_uint4(o2w[0], o2w[1], o2w[2], o2w[3]);
             }
-            *reinterpret_cast<uint4*>(crow + hcol + i) = make_uint4(o1[0], o1[1], o1[2], o1[3]);
-            *reinterpret_cast<uint4*>(crow + hcol + half + i) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
           }
         }
       } else {
