@@ -44,6 +44,7 @@ typedef enum {
 /* GEMM epilogues */
 #define HAP_EPI_STORE 0  /* C = acc (+bias) (+residual)                        */
 #define HAP_EPI_SWIGLU 1 /* C = silu(acc[:, gate]) * acc[:, up] per tile        */
+#define HAP_EPI_F32 2    /* C (float, ldc == N) = acc: the raw fp32 accumulator */
 
 const char* hap_status_string(int status);
 
@@ -78,6 +79,9 @@ int64_t hap_swiglu_half_width(int64_t inter_dim);
  * hw = swiglu_half; out_cols = N/2 and C[r, j*hw+i] = silu(g)*u.
  * HAP_EPI_STORE: optional bias (bf16[N]) and residual (bf16, ldr) are added in
  * fp32 before the single bf16 rounding.
+ * HAP_EPI_F32: C is float [a_rows, N] (ldc == N) and receives the fp32 TMEM
+ * accumulator unrounded (no bias/residual) — the fp32-accumulate parity
+ * check of the expert and projection GEMMs.
  *
  * Replaces: the per-expert gated-MLP FLOP term of expert_flops (arch.py:174-176)
  * and the projection term of attention_flops (arch.py:157-160).

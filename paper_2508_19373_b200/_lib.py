@@ -31,6 +31,7 @@ HAP_ERR_DRIVER = -6
 
 HAP_EPI_STORE = 0
 HAP_EPI_SWIGLU = 1
+HAP_EPI_F32 = 2
 
 # name -> (restype, argtypes); must mirror include/hap_kernels.h exactly.
 SIGNATURES = {

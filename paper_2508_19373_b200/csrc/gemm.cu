@@ -78,7 +78,7 @@ struct Params {
   const int32_t* seg_dst_row0;
 };
 
-constexpr int kEpiRope = 2;     // internal epilogue id (hap_gemm_qkv_rope)
+constexpr int kEpiRope = 3;     // internal epilogue id (hap_gemm_qkv_rope)
 constexpr int64_t kSplitMax = 16;
 constexpr size_t kSplitWorkspaceBytes = (size_t)32 << 20;
 constexpr int64_t kRasterL2Bytes = 48ll << 20;  // A rows of one raster group kept L2-resident across n-blocks
@@ -312,7 +312,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                           (int64_t)(row - seg_s[c.s] + p.seg_dst_row0[c.s]) * p.ldc
                     : p.C + (int64_t)row * p.ldc;
       bool do_epi = true;
-      if (ksplit > 1) {
+      if (ksplit > 1 || p.epi == HAP_EPI_F32) {
+        // fp32 partials (split-K slice ks) or the raw fp32 accumulator
+        // (HAP_EPI_F32: part == C, ksplit == 1, row pitch N).
         // tcgen05.ld is warp-collective: every lane loads, stores are predicated
         do_epi = false;
         float* dst = p.part + ((int64_t)ks * p.a_rows + row) * p.N + c.n_blk * p.BN;
@@ -857,6 +859,15 @@ extern "C" int hap_grouped_gemm_bf16_ex(const void* A, int64_t a_rows, int64_t l
     p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
     p.resid = reinterpret_cast<const __nv_bfloat16*>(residual);
     p.ldr = ldr;
+  } else if (epilogue == HAP_EPI_F32) {
+    // raw fp32 accumulators (no bias / residual / rounding): C is float
+    // [a_rows, N] dense (ldc == N); never split (one K pass per element)
+    if (bias || residual || ldc != N) return HAP_ERR_UNSUPPORTED;
+    if (reinterpret_cast<uintptr_t>(C) & 15) return HAP_ERR_MISALIGNED;
+    p.BN = pick_bn(N);
+    p.out_cols = (int32_t)N;
+    p.part = reinterpret_cast<float*>(C);
+    return hap::gemm::launch(p, A, a_rows, lda, K, B, n_groups, N, n_segs, nullptr, 0, stream);
   } else {
     return HAP_ERR_INVALID_ARG;
   }

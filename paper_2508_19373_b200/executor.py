@@ -344,7 +344,7 @@ class HapMoEBlock:
         else:
             hn_s = hn
         if self.capture is not None:
-            self.capture.update(h1=h1, hn=hn, hn_s=hn_s)
+            self.capture.update(qkv=qkv, attn=attn, h1=h1, hn=hn, hn_s=hn_s)
 
         # ---------------- expert module (partial over expert tp)
         c = rows // self.deg.a_tp  # rows this rank owns after the reduce-scatter

@@ -14,7 +14,7 @@ from typing import Optional, Tuple
 import torch
 
 from . import _lib
-from ._lib import HAP_EPI_STORE, HAP_EPI_SWIGLU, check
+from ._lib import HAP_EPI_F32, HAP_EPI_STORE, HAP_EPI_SWIGLU, check
 
 BF16 = torch.bfloat16
 
@@ -78,9 +78,13 @@ def grouped_gemm(a: torch.Tensor, b: torch.Tensor, n_groups: int, seg: Optional[
                  out: torch.Tensor, *, swiglu_half: int = 0, bias: Optional[torch.Tensor] = None,
                  residual: Optional[torch.Tensor] = None,
                  seg_group: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """out[r] = epi(a[r] @ b[g*N:(g+1)*N]^T) for rows r of segment s, g = seg_group[s] (tcgen05 kernel)."""
+    """out[r] = epi(a[r] @ b[g*N:(g+1)*N]^T) for rows r of segment s, g = seg_group[s] (tcgen05 kernel).
+
+    A float32 ``out`` selects HAP_EPI_F32: the unrounded fp32 accumulators
+    (no bias / residual / SwiGLU), the fp32-accumulate parity check."""
     lib = _lib.load()
-    _need(a, "a", BF16); _need(b, "b", BF16); _need(out, "out", BF16)
+    f32 = out.dtype == torch.float32
+    _need(a, "a", BF16); _need(b, "b", BF16); _need(out, "out", torch.float32 if f32 else BF16)
     _rowmajor(a, "a"); _rowmajor(out, "out")
     if not b.is_contiguous():
         raise ValueError("b must be contiguous [n_groups*N, K]")
@@ -102,6 +106,10 @@ def grouped_gemm(a: torch.Tensor, b: torch.Tensor, n_groups: int, seg: Optional[
     elif n_groups != 1:
         raise ValueError("seg is required when n_groups > 1")
     epi = HAP_EPI_SWIGLU if swiglu_half else HAP_EPI_STORE
+    if f32:
+        if swiglu_half or bias is not None or residual is not None:
+            raise ValueError("a float32 out takes the raw accumulators: no SwiGLU, bias or residual")
+        epi = HAP_EPI_F32
     if residual is not None:
         _need(residual, "residual", BF16); _rowmajor(residual, "residual")
     if bias is not None:

@@ -9,8 +9,24 @@ Parity definition:
      <= 2e-2 against the oracle run with bf16 rounding at the executor's
      storage points, over tokens whose routing agrees (a bf16 rounding
      difference in the router *input* can legitimately flip a near-tie);
-     at least 99% of tokens must agree;
+     at least 99% of tokens must agree, and every token that disagrees must
+     be a near-tie of the oracle's own logits (``near_tie_only``);
   4. fp32 quantities (router logits, routing weights) within 1e-4.
+
+At the BASELINE sizes (``check_full_size``):
+  * module level (oracle experts on the GPU's router input and routing): the
+    block output per element, |gpu - ref| <= 2e-2 * max(|ref|, rms(ref row))
+    (``elem_rel_err``);
+  * end to end from the same x (oracle attention module -> oracle router on
+    the oracle's own router input -> oracle experts) on whole sequences: per
+    row max|gpu - ref| / max|ref| <= 2e-2 (``row_rel_err``), and per element
+    within 2e-2 plus the oracle's own spread: the oracle run on the GPU's
+    (bf16) h1 and router input differs from the oracle run end to end by up to
+    3-5e-2 per element, because a one-ulp difference of a bf16 h1 / router
+    input element (different fp32 accumulation order in attention) moves the
+    fp64 expert MLP output (profiles/r02_parity_breakdown.txt).  By the
+    triangle inequality this bound is the module-level check carried to the
+    end-to-end reference; the row bound is the independent one.
 """
 
 import numpy as np
@@ -65,7 +81,7 @@ def check_block(cfg, batch, seq):
     assert np.array_equal(dst, od) and np.array_equal(seg, os_)
     # (3) block output vs the independent oracle forward
     ref = O.block_forward(spec, Wn, np32(x), batch, bf16_mirror=True)
-    agree = (np.sort(ref["topk_idx"], 1) == np.sort(idx, 1)).all(1)
+    agree = near_tie_only(idx, ref["topk_idx"], ref["logits"], cfg.top_k)
     assert agree.mean() >= 0.99, f"routing agreement {agree.mean():.4f}"
     got = np32(out)
     err = rel_err_rows(got[agree], ref["out"][agree])
@@ -77,6 +93,50 @@ def check_block(cfg, batch, seq):
 
 def rel_err_rows(a, b):
     return float(np.abs(a - b).max() / np.abs(b).max())
+
+
+def row_rel_err(got, ref):
+    """max over rows of max|got - ref| / max|ref| (each row judged on its own scale)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(got - ref).max(-1) / np.abs(ref).max(-1)))
+
+
+def check_e2e(got, ref, what, via=None):
+    """End-to-end bound (see the module docstring).  via: the oracle evaluated
+    on the GPU's own intermediates (h1, router input, routing); its distance
+    to ref is the oracle's own spread, allowed on top of 2e-2 per element."""
+    r, e = row_rel_err(got, ref), elem_rel_err(got, ref)
+    spread = elem_rel_err(via, ref) if via is not None else 0.0
+    print(f"{what}: row-relative {r:.3e}, per-element {e:.3e} (oracle spread {spread:.3e})")
+    assert r <= 2e-2 and e <= 2e-2 + spread, (what, r, e, spread)
+
+
+def elem_rel_err(got, ref):
+    """max over elements of |got - ref| / max(|ref|, rms of the ref row): a
+    per-element relative error whose denominator is floored at the row's RMS
+    (an element near zero is judged against the row's scale)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    floor = np.sqrt(np.mean(ref * ref, axis=-1, keepdims=True))
+    return float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), floor)))
+
+
+# a bf16 rounding of the router input moves fp32 logits by ~|x|*|w|*2^-9*sqrt(h);
+# routing may legitimately differ only where the oracle's k-th / (k+1)-th logit
+# gap is below this (the logits have std ~1.3 at init std 0.02)
+NEAR_TIE = 5e-2
+
+
+def near_tie_only(idx_gpu, idx_ref, logits_ref, top_k):
+    """Tokens whose top-k sets differ must be near-ties of the reference logits."""
+    agree = (np.sort(idx_gpu, 1) == np.sort(idx_ref, 1)).all(1)
+    margin = O.topk_margin(logits_ref, top_k)
+    if (~agree).any():
+        print(f"routing flips: {(~agree).sum()} of {agree.size}, max oracle margin {margin[~agree].max():.3e}")
+    bad = (~agree) & (margin > NEAR_TIE)
+    assert not bad.any(), f"routing differs on {bad.sum()} tokens with margin > {NEAR_TIE}: {margin[bad][:5]}"
+    return agree
 
 
 def test_block_tiny():
@@ -214,32 +274,21 @@ def test_forward_host_pipelines_successive_batches():
         assert torch.equal(o, r)
 
 
-def test_full_size_mixtral_prefill_properties():
-    """Mixtral-8x7B at the bench size (8 x 2048): routing and permutation
-    bit-exact on a token sample; output finite; rows of the permuted buffer
-    match the source tokens."""
-    from paper_2508_19373_b200.config import get_config
-
-    cfg = get_config("mixtral-8x7b")
-    blk, x, out, Wn = run_block(cfg, 8, 2048)
-    assert torch.isfinite(out.float()).all()
-    idx, dst, seg = (t.cpu().numpy() for t in blk.last_routing)
-    od, os_ = O.permute_index(idx.reshape(-1), cfg.n_experts)
-    assert np.array_equal(dst, od) and np.array_equal(seg, os_)
-    sample = np.arange(0, 16384, 61)
-    hn = np32(blk.capture["hn_s"])[sample]
-    oi, _ = O.router_topk(O.router_logits(hn, Wn["router"]), cfg.top_k, True)
-    assert np.array_equal(idx[sample], oi)
-
-
 # ---------------------------------------------------------------------------
-# BASELINE.json configs 3-5 at their full sizes (N = 1 here; the multi-GPU
-# plans are covered on gloo).  The full oracle block does not fit a test's
-# time budget at these sizes, so the checks are: routing bit-exact on a token
-# sample (oracle router on the GPU's own router input), the permutation
-# bit-exact for every row, the expert module of sampled tokens vs the oracle's
-# moe_forward (GPU routing, fp32/fp64 math) and the attention module of one
-# whole sequence vs the oracle — all within the block tolerance.
+# BASELINE.json configs 2-5 at their full sizes (N = 1 here; the multi-GPU
+# plans are covered on gloo).  The checks, per config:
+#   * routing bit-exact for EVERY token (oracle fixed-order router on the
+#     GPU's own router input), routing weights within 1e-4, the permutation
+#     bit-exact for every row;
+#   * expert module (sampled tokens): out == h1 + moe(hn) with the oracle's
+#     fp64 experts on the GPU's hn and routing, per element within 2e-2;
+#   * end to end from the same x on whole sequences (prefill: the first
+#     min(S, 2048) tokens of sequence 0 — causal, so they depend only on
+#     themselves; decode: up to 64 sequences): oracle attention module (bf16
+#     rounding mirrored) -> oracle router on the oracle's own router input ->
+#     oracle experts.  h1 per element within 2e-2; routing equal except on
+#     near-ties of the oracle's logits; out per element within 2e-2 on tokens
+#     whose routing agrees (>= 99 %).
 class _LazyW(dict):
     """Oracle weight dict that pulls per-expert slices from the GPU on demand."""
 
@@ -262,23 +311,30 @@ class _LazyExperts:
         return np32(self.t[e])
 
 
-def _oracle_h1_one_sequence(cfg, W, xs):
-    """Attention module (rmsnorm -> qkv (+bias) -> RoPE -> causal GQA -> o-proj + residual) for one sequence."""
-    spec = oracle_spec(cfg)
-    S, d = xs.shape[0], cfg.head_dim
-    f = lambda k: np32(W[k])  # noqa: E731
-    xn = O.rmsnorm(xs, f("ln1"), spec.rms_eps).astype(np.float32)
-    q, k, v = xn @ f("wq").T, xn @ f("wk").T, xn @ f("wv").T
-    if cfg.qkv_bias:
-        q, k, v = q + f("bq"), k + f("bk"), v + f("bv")
-    pos = np.arange(S)
-    q = O.rope(q.reshape(S, cfg.n_q_heads, d).astype(np.float64), pos, spec.rope_theta)
-    k = O.rope(k.reshape(S, cfg.n_kv_heads, d).astype(np.float64), pos, spec.rope_theta)
-    attn = O.attention(q, k, v.reshape(S, cfg.n_kv_heads, d).astype(np.float64)).reshape(S, -1)
-    return xs.astype(np.float64) + attn.astype(np.float32) @ f("wo").T
+def _np_weights(W, keys):
+    return {k: np32(W[k]) for k in keys if k in W}
 
 
-def check_full_size(cfg, batch, seq, n_sample=192, attn_check=True):
+_ATTN_KEYS = ("ln1", "wq", "wk", "wv", "wo", "bq", "bk", "bv", "ln2")
+
+
+def _moe_ref(cfg, W, hn, routing):
+    return O.moe_forward(oracle_spec(cfg), _LazyW(W), hn, routing=routing)["moe"]
+
+
+def _check_routing_all(cfg, blk, W):
+    idx, dst, seg = (t.cpu().numpy() for t in blk.last_routing)
+    od, os_ = O.permute_index(idx.reshape(-1), cfg.n_experts)
+    assert np.array_equal(dst, od) and np.array_equal(seg, os_)
+    hn = np32(blk.capture["hn_s"])
+    oi, ow = O.router_topk(O.router_logits(hn, np32(W["router"])), cfg.top_k, cfg.norm_topk_prob)
+    assert np.array_equal(idx, oi), f"routing differs on {(idx != oi).any(1).sum()} tokens"
+    tw = blk.capture["topk_w"].cpu().numpy()
+    assert np.abs(tw - ow).max() < 1e-4
+    return idx, tw, hn
+
+
+def check_full_size(cfg, batch, seq, n_sample=192, e2e_tokens=2048, n_e2e=128):
     from paper_2508_19373_b200.executor import HapMoEBlock
     from paper_2508_19373_b200.layout import PlanDegrees
     from paper_2508_19373_b200.weights import synthetic_weights
@@ -293,23 +349,57 @@ def check_full_size(cfg, batch, seq, n_sample=192, attn_check=True):
     out = blk.forward(x, "prefill", batch, seq)
     torch.cuda.synchronize()
     assert torch.isfinite(out.float()).all()
-    idx, dst, seg = (t.cpu().numpy() for t in blk.last_routing)
-    od, os_ = O.permute_index(idx.reshape(-1), cfg.n_experts)
-    assert np.array_equal(dst, od) and np.array_equal(seg, os_)
-    sample = np.linspace(0, T - 1, n_sample).astype(np.int64)
-    hn = np32(blk.capture["hn_s"][torch.from_numpy(sample).cuda()])
-    oi, ow = O.router_topk(O.router_logits(hn, np32(W["router"])), cfg.top_k, cfg.norm_topk_prob)
-    assert np.array_equal(idx[sample], oi)
-    tw = blk.capture["topk_w"].cpu().numpy()[sample]
-    assert np.abs(tw - ow).max() < 1e-4
-    moe = O.moe_forward(oracle_spec(cfg), _LazyW(W), hn, routing=(idx[sample], tw))["moe"]
-    h1 = np32(blk.capture["h1"])[sample]
-    got = np32(out)[sample]
-    assert rel_err_rows(got - h1, moe) <= 3e-2
-    if attn_check:  # causal: the first P tokens of sequence 0 depend only on themselves
-        P = min(seq, 1024)
-        h1_ref = _oracle_h1_one_sequence(cfg, W, np32(x[:P]))
-        assert rel_err_rows(np32(blk.capture["h1"][:P]), h1_ref) <= 2e-2
+    idx, tw, hn = _check_routing_all(cfg, blk, W)
+    h1 = np32(blk.capture["h1"])
+    cap_qkv, cap_attn = blk.capture["qkv"], blk.capture["attn"]
+    got = np32(out)
+    del blk
+    # end to end from x: the first P tokens of sequence 0
+    P = min(seq, e2e_tokens)
+    spec = oracle_spec(cfg)
+    Wa = _np_weights(W, _ATTN_KEYS)
+    xs = np32(x[:P])
+    h1_ref = O.attention_module(spec, Wa, xs, 1, bf16_mirror=True)["h1"]
+    # module level: attention core on the GPU's own q/k/v, o-proj on the GPU's attention output
+    d, Hq, Hkv = cfg.head_dim, cfg.n_q_heads, cfg.n_kv_heads
+    qkv, att = np32(cap_qkv[:P]), np32(cap_attn[:P])
+    att_ref = O.attention(qkv[:, :Hq * d].reshape(P, Hq, d), qkv[:, Hq * d:(Hq + Hkv) * d].reshape(P, Hkv, d),
+                          qkv[:, (Hq + Hkv) * d:].reshape(P, Hkv, d)).reshape(P, -1)
+    err_att = elem_rel_err(att, att_ref)
+    h1_via = xs.astype(np.float64) + att.astype(np.float64) @ Wa["wo"].astype(np.float64).T
+    err_o = elem_rel_err(h1[:P], h1_via)
+    print(f"{cfg.name} attention core (module level): per-element {err_att:.3e}; o-proj + residual {err_o:.3e}")
+    assert err_att <= 2e-2 and err_o <= 2e-2, (err_att, err_o)
+    check_e2e(h1[:P], h1_ref, f"{cfg.name} h1", via=h1_via)
+    hn_ref = O.bf16_round(O.rmsnorm(h1_ref, Wa["ln2"], spec.rms_eps).astype(np.float32))
+    lg_ref = O.router_logits(hn_ref, np32(W["router"]))
+    oi_ref, ow_ref = O.router_topk(lg_ref, cfg.top_k, cfg.norm_topk_prob)
+    agree = near_tie_only(idx[:P], oi_ref, lg_ref, cfg.top_k)
+    assert agree.mean() >= 0.99, agree.mean()
+    # one oracle expert pass over both samples: module level (GPU hn, GPU routing)
+    # and end to end (oracle hn, oracle routing)
+    # and end to end (oracle hn, oracle routing), plus the oracle on the GPU's
+    # hn for the end-to-end tokens (the oracle's own spread)
+    s_mod = np.linspace(0, T - 1, n_sample).astype(np.int64)
+    s_e2e = np.linspace(0, P - 1, n_e2e).astype(np.int64)
+    hn_all = np.concatenate([hn[s_mod], hn_ref[s_e2e], hn[s_e2e]])
+    r_all = (np.concatenate([idx[s_mod], oi_ref[s_e2e], idx[s_e2e]]),
+             np.concatenate([tw[s_mod], ow_ref[s_e2e], tw[s_e2e]]))
+    moe = _moe_ref(cfg, W, hn_all, r_all)
+    m_mod, m_e2e, m_via = moe[:n_sample], moe[n_sample:n_sample + n_e2e], moe[n_sample + n_e2e:]
+    err_mod = elem_rel_err(got[s_mod], h1[s_mod] + m_mod)
+    print(f"{cfg.name} out (module level): per-element {err_mod:.3e}")
+    assert err_mod <= 2e-2, err_mod
+    ok = agree[s_e2e]
+    check_e2e(got[s_e2e][ok], h1_ref[s_e2e][ok] + m_e2e[ok], f"{cfg.name} out (end to end)",
+              via=(h1[s_e2e] + m_via)[ok])
+
+
+def test_full_size_mixtral_prefill():
+    """BASELINE config 2 (the headline bench config): Mixtral-8x7B block, prefill 8 x 2048."""
+    from paper_2508_19373_b200.config import get_config
+
+    check_full_size(get_config("mixtral-8x7b"), 8, 2048)
 
 
 def test_full_size_qwen15_moe_prefill():
@@ -323,46 +413,58 @@ def test_full_size_mixtral_8x22b_prefill():
     """BASELINE config 5 block (h 6144, 48/8 heads, I 16384), prefill 16 x 4096 (T = 65536)."""
     from paper_2508_19373_b200.config import get_config
 
-    check_full_size(get_config("mixtral-8x22b"), 16, 4096, n_sample=128)
+    check_full_size(get_config("mixtral-8x22b"), 16, 4096, n_sample=128, e2e_tokens=1024, n_e2e=96)
 
 
-@pytest.mark.parametrize("batch", [1, 8, 64, 512])
-def test_full_size_qwen2_57b_decode_sweep(batch):
-    """BASELINE config 4 block (64 experts top-8 + 8 shared units), decode at kv 2048 over the batch sweep:
-    routing + permutation bit-exact for every sequence, expert module and attention vs the oracle."""
-    from paper_2508_19373_b200.config import get_config
+def check_full_size_decode(cfg, batch, L=2048, n_e2e=64):
     from paper_2508_19373_b200.executor import HapMoEBlock, KVCache
     from paper_2508_19373_b200.layout import PlanDegrees
     from paper_2508_19373_b200.weights import synthetic_weights
 
-    cfg = get_config("qwen2-57b-a14b")
     W = synthetic_weights(cfg, "cuda", seed=0)
     blk = HapMoEBlock(cfg, PlanDegrees(1, 1, 1, 1), None, weights=W)
     blk.capture = {}
-    L = 2048
     cache = KVCache.empty(batch, cfg.n_kv_heads, L, cfg.head_dim, "cuda", random=True)
     pos = torch.full((batch,), L - 1, device="cuda", dtype=torch.int32)
     g = torch.Generator(device="cuda")
     g.manual_seed(5)
     x = torch.randn(batch, cfg.hidden, device="cuda", generator=g).to(torch.bfloat16)
-    k0 = cache.k[:min(batch, 2)].clone()
-    v0 = cache.v[:min(batch, 2)].clone()
+    nb = min(batch, n_e2e)
+    k0, v0 = np32(cache.k[:nb]), np32(cache.v[:nb])
     out = blk.forward(x, "decode", batch, kv_cache=cache, positions=pos)
     torch.cuda.synchronize()
     assert torch.isfinite(out.float()).all()
-    idx, dst, seg = (t.cpu().numpy() for t in blk.last_routing)
-    hn = np32(blk.capture["hn_s"])
-    oi, ow = O.router_topk(O.router_logits(hn, np32(W["router"])), cfg.top_k, cfg.norm_topk_prob)
-    assert np.array_equal(idx, oi)
-    od, os_ = O.permute_index(idx.reshape(-1), cfg.n_experts)
-    assert np.array_equal(dst, od) and np.array_equal(seg, os_)
-    tw = blk.capture["topk_w"].cpu().numpy()
-    s = np.arange(min(batch, 64))
-    moe = O.moe_forward(oracle_spec(cfg), _LazyW(W), hn[s], routing=(idx[s], tw[s]))["moe"]
-    assert rel_err_rows(np32(out)[s] - np32(blk.capture["h1"])[s], moe) <= 3e-2
-    # attention of the first sequences vs the oracle decode (cache + the new token)
-    spec = oracle_spec(cfg)
-    nb = min(batch, 2)
-    ref = O.decode_forward(spec, _LazyW(W), np32(x[:nb]), np32(k0), np32(v0), pos[:nb].cpu().numpy())
-    assert rel_err_rows(np32(blk.capture["h1"][:nb]), ref["h1"]) <= 2e-2
+    idx, tw, hn = _check_routing_all(cfg, blk, W)
+    h1, got = np32(blk.capture["h1"]), np32(out)
+    kn, vn = np32(cache.k[:nb, :, L - 1]), np32(cache.v[:nb, :, L - 1])
+    # expert module on the GPU's hn and routing
+    s = np.arange(nb)
+    moe = _moe_ref(cfg, W, hn[s], (idx[s], tw[s]))
+    err_mod = elem_rel_err(got[s], h1[s] + moe)
+    print(f"{cfg.name} decode B={batch} out (module level): per-element {err_mod:.3e}")
+    assert err_mod <= 2e-2, err_mod
+    # end to end from x (oracle attention over cache + new token, oracle routing)
+    ref = O.decode_forward(oracle_spec(cfg), _LazyW(W), np32(x[:nb]), k0, v0, pos[:nb].cpu().numpy())
+    check_e2e(h1[:nb], ref["h1"], f"{cfg.name} decode B={batch} h1")
+    # the new token's post-RoPE k and its v were appended at pos
+    check_e2e(kn.reshape(nb, -1), ref["k"].reshape(nb, -1), "k appended")
+    check_e2e(vn.reshape(nb, -1), ref["v"].reshape(nb, -1), "v appended")
+    agree = near_tie_only(idx[:nb], ref["topk_idx"], ref["logits"], cfg.top_k)
+    assert agree.sum() >= nb - max(1, nb // 100)
+    check_e2e(got[:nb][agree], ref["out"][agree], f"{cfg.name} decode B={batch} out (end to end)",
+              via=(h1[s] + moe)[agree])
 
+
+def test_full_size_mixtral_decode_b64():
+    """BASELINE config 2, decode half: Mixtral-8x7B block, batch 64 at kv 2048."""
+    from paper_2508_19373_b200.config import get_config
+
+    check_full_size_decode(get_config("mixtral-8x7b"), 64)
+
+
+@pytest.mark.parametrize("batch", [1, 8, 64, 512])
+def test_full_size_qwen2_57b_decode_sweep(batch):
+    """BASELINE config 4 block (64 experts top-8 + 8 shared units), decode at kv 2048 over the batch sweep."""
+    from paper_2508_19373_b200.config import get_config
+
+    check_full_size_decode(get_config("qwen2-57b-a14b"), batch)

@@ -190,6 +190,45 @@ def test_grouped_gemm_segment_groups():
     assert rel_err(np32(c), ref) < 1e-2
 
 
+def elem_rel_err(got, ref):
+    """max |got - ref| / max(|ref|, rms of the ref row) over elements."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    floor = np.sqrt(np.mean(ref * ref, axis=-1, keepdims=True))
+    return float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), floor)))
+
+
+@pytest.mark.parametrize("rows,N,Kd", [((300, 600), 28672, 4096),   # Mixtral gate|up, 2-CTA pair tiles
+                                       ((300, 600), 4096, 14336),   # Mixtral down, 2-CTA pair tiles
+                                       ((37, 27), 28672, 4096),     # decode-size segments, 1-CTA tiles
+                                       ((64,), 4096, 14336)])
+def test_grouped_gemm_fp32_accumulate(rows, N, Kd):
+    """north_star's fp32-accumulate check: the tcgen05 accumulator (HAP_EPI_F32,
+    no bf16 rounding) of the expert GEMMs at Mixtral-8x7B shapes vs fp64 on the
+    same bf16 operands, per element within 1e-4 (row-RMS floored)."""
+    E = len(rows)
+    seg = np.zeros(E + 1, dtype=np.int32)
+    seg[1:] = np.cumsum(rows)
+    R = int(seg[-1])
+    a, b = bf16((R, Kd), seed=11), bf16((E * N, Kd), 0.02, seed=12)
+    c = torch.full((R, N), float("nan"), device=dev, dtype=torch.float32)
+    K().grouped_gemm(a, b, E, torch.from_numpy(seg).to(dev), c)
+    torch.cuda.synchronize()
+    an, bn, cn = np32(a).astype(np.float64), np32(b), np32(c)
+    for e in range(E):
+        r0, r1 = seg[e], seg[e + 1]
+        ref = an[r0:r1] @ bn[e * N:(e + 1) * N].astype(np.float64).T
+        err = elem_rel_err(cn[r0:r1], ref)
+        assert err <= 1e-4, (e, err)
+
+
+def test_gemm_fp32_rejects_epilogue_args():
+    a, b = bf16((128, 256), seed=1), bf16((256, 256), seed=2)
+    c = torch.empty(128, 256, device=dev, dtype=torch.float32)
+    with pytest.raises(ValueError):
+        K().grouped_gemm(a, b, 1, None, c, residual=bf16((128, 256)))
+
+
 # ---------------------------------------------------------------- router --
 @pytest.mark.parametrize("T,h,E,k,renorm,shared", [(1000, 512, 8, 2, True, False), (517, 2048, 60, 4, False, True),
                                                    (300, 3584, 64, 8, False, True), (64, 4096, 8, 2, True, False),
