@@ -184,14 +184,19 @@ int hap_peer_allreduce_bf16(const int64_t* in_ptrs, const int64_t* out_ptrs, con
  * shared-expert gate: shared_gate[t] = sigmoid(x[t] . w[E]) (fp32).
  * logits_out (fp32 [T, n_experts]) is optional.
  * Requires h % 64 == 0, n_experts + has_shared_gate <= 72, top_k <= 32.
- * For T <= 1024 with more than 8 router rows the work is spread over CTAs per
- * (token, 8 rows) that meet in a per-device scratch row and counter (reset
- * by the kernel), so such calls on one device must not overlap in time.
+ * Workspace (caller-owned, zero-filled once before first use; the kernel
+ * leaves it zeroed): hap_router_workspace_bytes(T, n_experts, has_shared_gate)
+ * bytes, non-zero only for T <= 1024 with more than 8 router rows, where the
+ * work is spread over CTAs per (token, 8 rows) that meet in the workspace.
+ * With a NULL / smaller workspace such calls use one CTA per token instead
+ * (same logits bit for bit, slower for wide routers).  Concurrent calls need
+ * distinct workspaces.
  * Replaces: the router term 2*T*h*E of expert_flops (arch.py:177).
  */
+size_t hap_router_workspace_bytes(int64_t T, int64_t n_experts, int32_t has_shared_gate);
 int hap_router_topk(const void* x, int64_t T, int64_t h, const void* w, int64_t n_experts, int64_t top_k,
                     int32_t renormalize, int32_t has_shared_gate, int32_t* topk_idx, float* topk_w,
-                    float* shared_gate, float* logits_out, void* stream);
+                    float* shared_gate, float* logits_out, void* workspace, size_t ws_bytes, void* stream);
 
 /*
  * Stable counting-sort permute (scan + scatter).  Row r of the logical input
@@ -240,14 +245,17 @@ int hap_rope_qk(void* qkv, int64_t T, int64_t ld, int64_t n_q_heads, int64_t n_k
  * softmax.  Token (s, i) = row s*seq_len + i.  q/k/v/out addressed by leading
  * dims (multiples of 8, 16-byte aligned bases); head h of a row starts at
  * column h*head_dim.  head_dim in {64, 128}.  The persistent kernel hands out
- * work through a per-device ticket counter that it re-zeroes on exit, so calls
- * on one device must not overlap in time (issue them on one stream, or order
- * the streams).
+ * work items through two int32 tickets in the caller's workspace
+ * (hap_attn_prefill_workspace_bytes(), 4-byte aligned, zero-filled once before
+ * first use; the kernel re-zeroes them on exit, so a workspace is reusable by
+ * the next call on its stream).  Concurrent calls need distinct workspaces.
  * Replaces: score+value term 4*n*kv_len*h of attention_flops (arch.py:161).
  */
+size_t hap_attn_prefill_workspace_bytes(void);
 int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                      void* out, int64_t ldo, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
-                     int64_t n_kv_heads, int64_t head_dim, float scale, int32_t causal, void* stream);
+                     int64_t n_kv_heads, int64_t head_dim, float scale, int32_t causal, void* workspace,
+                     size_t ws_bytes, void* stream);
 
 /*
  * Prefill: copy the (post-RoPE) k and v of every token of n_seqs sequences of

@@ -75,10 +75,11 @@ SIGNATURES = {
         [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, ctypes.c_int32, ctypes.c_int32,
          ctypes.c_int32, ctypes.c_int32, c_void_p],
     ),
+    "hap_router_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int32]),
     "hap_router_topk": (
         ctypes.c_int,
         [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int32, c_int32, c_void_p, c_void_p,
-         c_void_p, c_void_p, c_void_p],
+         c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     ),
     "hap_moe_permute_workspace_bytes": (c_size_t, [c_int64, c_int64]),
     "hap_moe_permute": (
@@ -99,10 +100,11 @@ SIGNATURES = {
         ctypes.c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p, c_float, c_void_p],
     ),
+    "hap_attn_prefill_workspace_bytes": (c_size_t, []),
     "hap_attn_prefill": (
         ctypes.c_int,
         [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
-         c_int64, c_int64, c_int64, c_float, c_int32, c_void_p],
+         c_int64, c_int64, c_int64, c_float, c_int32, c_void_p, c_size_t, c_void_p],
     ),
     "hap_kv_cache_fill": (
         ctypes.c_int,

@@ -110,31 +110,55 @@ def measure_attention(cfg: BlockConfig, tp: int, b_rep: int, S: int, stage: str,
 
 
 # ---------------------------------------------------------------- experts --
+def skewed_router(router: torch.Tensor, n_experts: int) -> torch.Tensor:
+    """SURVEY §8(d) skewed-routing workload: router row e scaled by 1 + 0.1*e
+    (expert E-1 is picked most), so EP groups receive unequal row counts."""
+    scale = torch.ones(router.shape[0], 1, device=router.device, dtype=torch.float32)
+    scale[:n_experts, 0] = 1.0 + 0.1 * torch.arange(n_experts, device=router.device, dtype=torch.float32)
+    return (router.float() * scale).to(router.dtype)
+
+
 def measure_experts(cfg: BlockConfig, tp: int, ep: int, dp: int, B: int, S: int, stage: str,
-                    reps: int = 5) -> float:
-    """Per-device expert-module time of one rank under expert (tp, ep, dp):
+                    reps: int = 5, skew: bool = False, detail: Optional[dict] = None) -> float:
+    """Per-device expert-module time of the slowest rank under expert (tp, ep, dp):
     router + permute over the rank's own token shard, grouped gate/up + down
-    GEMMs over the rows the routing sends to its E/ep experts (I/tp slice),
-    shared expert, weighted combine.  Collectives excluded (priced by rho)."""
+    GEMMs over the rows the routing of its expert-DP replica's tokens
+    (T / dp) sends to its E/ep experts (I/tp slice), shared expert, weighted
+    combine.  The EP group measured is the one receiving the most rows (the
+    reference charges EP a fixed gamma = 1.3 for this imbalance,
+    planner.py:54, 243-248; here it is measured, and reported in
+    detail["imbalance"] = max / mean rows over the EP groups).  skew: the
+    skewed-routing workload (skewed_router).  Collectives excluded (priced by rho)."""
     h, E, k = cfg.hidden, cfg.n_experts, cfg.top_k
     T_all = B * S if stage == "prefill" else B
     n_shards = ep * dp
     T_own = max(1, math.ceil(T_all / n_shards)) if n_shards > 1 else T_all
+    T_rep = max(1, math.ceil(T_all / dp)) if dp > 1 else T_all  # tokens of one expert-DP replica
     El = E // ep
     Il = cfg.inter // tp
     hw = swiglu_half_width(Il)
     x_all = _rand((T_all, h))
     router = _rand((E + (1 if cfg.n_shared else 0), h), 0.02)
+    if skew:
+        router = skewed_router(router, E)
     w13 = _rand((El, 2 * Il, h), 0.02)
     w2 = _rand((El, h, Il), 0.02)
-    # routing of all tokens -> rows received by EP group 0 (untimed setup)
-    idx_all = torch.empty(T_all, k, device="cuda", dtype=torch.int32)
-    tw_all = torch.empty(T_all, k, device="cuda", dtype=torch.float32)
-    sg_all = torch.empty(T_all, device="cuda", dtype=torch.float32) if cfg.n_shared else None
-    K.router_topk(x_all, router, E, k, cfg.norm_topk_prob, bool(cfg.n_shared), idx_all, tw_all, sg_all)
-    local = idx_all.view(-1).clone()
-    local = torch.where(local < El, local, torch.full_like(local, -1))
-    R_all = T_all * k
+    # routing of the replica's tokens -> rows received by the busiest EP group (untimed setup)
+    x_rep = x_all[:T_rep].contiguous()
+    idx_all = torch.empty(T_rep, k, device="cuda", dtype=torch.int32)
+    tw_all = torch.empty(T_rep, k, device="cuda", dtype=torch.float32)
+    sg_all = torch.empty(T_rep, device="cuda", dtype=torch.float32) if cfg.n_shared else None
+    K.router_topk(x_rep, router, E, k, cfg.norm_topk_prob, bool(cfg.n_shared), idx_all, tw_all, sg_all)
+    counts = torch.bincount(idx_all.view(-1).long(), minlength=E).cpu()
+    group_rows = counts.view(ep, El).sum(1)
+    g_max = int(torch.argmax(group_rows))
+    if detail is not None:
+        detail["group_rows"] = [int(r) for r in group_rows]
+        detail["imbalance"] = float(group_rows.max()) / max(float(group_rows.float().mean()), 1e-9)
+        detail["ep_group"] = g_max
+    local = idx_all.view(-1).clone() - g_max * El
+    local = torch.where((local >= 0) & (local < El), local, torch.full_like(local, -1))
+    R_all = T_rep * k
     ws_all = torch.empty(max(K.permute_workspace_bytes(R_all, El), 16), device="cuda", dtype=torch.uint8)
     dst_all = torch.empty(R_all, device="cuda", dtype=torch.int32)
     seg_l = torch.empty(El + 1, device="cuda", dtype=torch.int32)
@@ -175,7 +199,7 @@ def measure_experts(cfg: BlockConfig, tp: int, ep: int, dp: int, B: int, S: int,
             ys = K.gemm(hs, ws2)
         K.moe_combine(y_back, dst, tw, T_own, k, out, residual=x_own, shared_y=ys, shared_gate=sg)
     t = _events_time(fn, reps)
-    del x_all, w13, w2, x_recv, H, Y
+    del x_all, x_rep, w13, w2, x_recv, H, Y
     torch.cuda.empty_cache()
     return t
 
@@ -195,6 +219,7 @@ class Measurement:
     flops: float         # planner flop charge of this cell
     measured_s: float
     roofline_s: float
+    imbalance: float = 1.0  # experts: measured max/mean EP-group rows (the reference's gamma)
 
     @property
     def eta(self) -> float:
@@ -203,7 +228,7 @@ class Measurement:
 
 def measure_catalog(cfg: BlockConfig, n: int, batch: int, input_len: int, output_len: int,
                     reps: int = 5, gamma: float = 1.3, cache: Optional[dict] = None,
-                    stages: Optional[Tuple[str, ...]] = None) -> List[Measurement]:
+                    stages: Optional[Tuple[str, ...]] = None, skew: bool = False) -> List[Measurement]:
     """Measured per-device module time for every (strategy, stage) cell the
     planner prices for this scenario (build_cost_tensors, planner.py:222-250).
     Cells of stages not measured keep the planner's own estimate."""
@@ -231,15 +256,17 @@ def measure_catalog(cfg: BlockConfig, n: int, batch: int, input_len: int, output
             out.append(Measurement(cfg.name, n, "attention", st, a.label(), k_, b_rep, s, cfg.hidden, fl,
                                    cache[key], fl / hw.peak_flops))
         for i, e in enumerate(cat.expert):
-            key = ("exp", cfg.name, e.tp_degree, e.ep_degree, e.dp_degree, batch, input_len, st)
+            key = ("exp", cfg.name, e.tp_degree, e.ep_degree, e.dp_degree, batch, input_len, st, skew)
             if key not in cache:
-                cache[key] = measure_experts(cfg, e.tp_degree, e.ep_degree, e.dp_degree, batch, input_len, st, reps)
+                det = {}
+                cache[key] = (measure_experts(cfg, e.tp_degree, e.ep_degree, e.dp_degree, batch, input_len, st,
+                                              reps, skew=skew, detail=det), det.get("imbalance", 1.0))
             imb = gamma if e.ep_degree > 1 else 1.0
             tokens = batch * input_len if st == "prefill" else batch
             fl = mp.expert_flops(spec, tokens) * imb / n
             out.append(Measurement(cfg.name, n, "experts", st, e.label(), i, batch,
-                                   input_len if st == "prefill" else 1, cfg.hidden, fl, cache[key],
-                                   fl / hw.peak_flops))
+                                   input_len if st == "prefill" else 1, cfg.hidden, fl, cache[key][0],
+                                   fl / hw.peak_flops, imbalance=cache[key][1]))
     return out
 
 

@@ -87,7 +87,7 @@ def cmd_plan(args) -> Dict:
     hw = _hardware(args)
     t = time.perf_counter()
     if args.calibrated:
-        res, src = calibrated_plan(cfg, hw.n_devices, args.batch, args.input_len, args.output_len)
+        res, src = calibrated_plan(cfg, hw.n_devices, args.batch, args.input_len, args.output_len, hw=hw)
     else:
         res, src = plan_for(cfg, hw.n_devices, args.batch, args.input_len, args.output_len, hw=hw), "roofline"
     solve_s = time.perf_counter() - t

@@ -15,7 +15,8 @@
 namespace hap {
 int attn_prefill_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* out,
                     int64_t ldo, int64_t n_seqs, int64_t S, int64_t n_q, int64_t n_kv, int64_t head_dim, float scale,
-                    int32_t causal, cudaStream_t st);
+                    int32_t causal, int* sched, cudaStream_t st);
+size_t attn_prefill_tc_workspace_bytes();
 
 namespace attn {
 
@@ -32,6 +33,7 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t 
   pdl_wait();
   const int b = blockIdx.x;
   const int p = pos[b];
+  if (p < 0 || p >= max_len) return;  // outside the cache: nothing is written
   const __nv_bfloat16* row = qkv + (int64_t)b * ld;
   for (int i = threadIdx.x; i < n_kv * D / 8; i += blockDim.x) {
     const int hh = i / (D / 8), c = (i % (D / 8)) * 8;
@@ -79,13 +81,16 @@ struct DecItem {
   int b, kvh, k0, nk;
 };
 
-__device__ __forceinline__ DecItem dec_item(int item, int n_kv, int ns, int split, const int32_t* pos) {
+// Keys [0, min(pos[b] + 1, max_len)) of sequence b: a position outside the
+// cache never makes the kernels touch memory beyond the sequence's rows
+// (kv_append_kernel skips it; the host API rejects it where it can see it).
+__device__ __forceinline__ DecItem dec_item(int item, int n_kv, int ns, int split, const int32_t* pos, int max_len) {
   DecItem it;
   const int bk = item / ns, s = item - bk * ns;
   it.b = bk / n_kv;
   it.kvh = bk - it.b * n_kv;
   it.k0 = s * split;
-  it.nk = max(0, min(pos[it.b] + 1, it.k0 + split) - it.k0);
+  it.nk = max(0, min(min(pos[it.b] + 1, max_len), it.k0 + split) - it.k0);
   return it;
 }
 
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
   int l_item = worker, l_c = 0;
   auto skip_empty = [&]() {
     while (l_item < n_items) {
-      li = dec_item(l_item, n_kv, ns, split, pos);
+      li = dec_item(l_item, n_kv, ns, split, pos, max_len);
       if (li.nk > 0) return;
       l_item += W;
     }
@@ -153,7 +158,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
   int stage = 0;
   uint32_t phase = 0;
   for (int item = worker; item < n_items; item += W) {
-    const DecItem it = dec_item(item, n_kv, ns, split, pos);
+    const DecItem it = dec_item(item, n_kv, ns, split, pos, max_len);
     const int sidx = item % ns;
     const int64_t obase = ((int64_t)it.b * n_q + it.kvh * G + g) * ns + sidx;
     if (it.nk == 0) {
@@ -459,10 +464,15 @@ extern "C" int hap_kv_cache_fill(const void* qkv, int64_t ldqkv, int64_t n_seqs,
   return HAP_OK;
 }
 
+extern "C" size_t hap_attn_prefill_workspace_bytes(void) { return hap::attn_prefill_tc_workspace_bytes(); }
+
 extern "C" int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                                 void* out, int64_t ldo, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
-                                int64_t n_kv_heads, int64_t head_dim, float scale, int32_t causal, void* stream) {
+                                int64_t n_kv_heads, int64_t head_dim, float scale, int32_t causal, void* workspace,
+                                size_t ws_bytes, void* stream) {
   if (!q || !k || !v || !out || n_seqs < 0 || seq_len < 0 || n_q_heads < 1 || n_kv_heads < 1) return HAP_ERR_INVALID_ARG;
+  if (!workspace || ws_bytes < hap::attn_prefill_tc_workspace_bytes()) return HAP_ERR_WORKSPACE;
+  if (reinterpret_cast<uintptr_t>(workspace) & 3) return HAP_ERR_MISALIGNED;
   if (n_q_heads % n_kv_heads) return HAP_ERR_INVALID_ARG;
   if (head_dim != 64 && head_dim != 128) return HAP_ERR_UNSUPPORTED;
   if (ldq % 8 || ldk % 8 || ldv % 8 || ldo % 8) return HAP_ERR_MISALIGNED;
@@ -471,7 +481,7 @@ extern "C" int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64
     return HAP_ERR_MISALIGNED;
   if (n_seqs == 0 || seq_len == 0) return HAP_OK;
   return hap::attn_prefill_tc(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, seq_len, n_q_heads, n_kv_heads, head_dim,
-                              scale, causal, reinterpret_cast<cudaStream_t>(stream));
+                              scale, causal, reinterpret_cast<int*>(workspace), reinterpret_cast<cudaStream_t>(stream));
 }
 
 // Key-split size for the warp-pipelined decode: items = B * n_kv * ceil(len/split)

@@ -95,4 +95,4 @@ extern "C" const char* hap_status_string(int status) {
   }
 }
 
-extern "C" int hap_abi_version(void) { return 1; }
+extern "C" int hap_abi_version(void) { return 2; }

@@ -192,20 +192,25 @@ __global__ void __launch_bounds__(kRanges * NE) router_small_kernel(const __nv_b
 // instead of one per token, so a decode step with few tokens streams the
 // router rows on rows/8 SMs.  Chains and range order are those of
 // router_small_kernel (bit-identical logits); each CTA parks its 8 logits in a
-// device scratch row, and the token's last CTA (atomic count, reset by itself)
-// runs the softmax / top-k.  One launch in flight per device.
+// scratch row of the caller's workspace, and the token's last CTA (atomic
+// count, reset by itself) runs the softmax / top-k.  Workspace layout
+// (independent of T, so launches of any size can share it): int32
+// cnt[kSmallT] (zero before the first launch; every launch leaves it zeroed),
+// then float logits[T][kMaxRouterRows].  Concurrent launches need distinct
+// workspaces.
 constexpr int kGroupRows = 8;
 constexpr int kMaxRouterRows = 80;
-__device__ float g_router_logits[kSmallT * kMaxRouterRows];
-__device__ int g_router_cnt[kSmallT];
+constexpr int64_t kGroupCntBytes = (int64_t)kSmallT * 4;
 
 template <int NE>
 __global__ void __launch_bounds__(kRanges * kGroupRows) router_group_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w, int T, int h, int n_rows_w, int E,
     int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
-    float* __restrict__ shared_gate, float* __restrict__ logits_out) {
+    float* __restrict__ shared_gate, float* __restrict__ logits_out, uint8_t* __restrict__ scratch) {
   pdl_trigger();
   pdl_wait();
+  int* cnt_ws = reinterpret_cast<int*>(scratch);
+  float* logits_ws = reinterpret_cast<float*>(scratch + kGroupCntBytes);
   extern __shared__ uint4 xs[];  // token row (h/8 vectors), then the group's (row, range) segments
   __shared__ float part[kRanges][kGroupRows];
   __shared__ __align__(8) uint64_t bar;
@@ -258,19 +263,19 @@ __global__ void __launch_bounds__(kRanges * kGroupRows) router_group_kernel(
     float s2 = part[0][el];
 #pragma unroll
     for (int pp = 1; pp < kRanges; ++pp) s2 = __fadd_rn(s2, part[pp][el]);
-    g_router_logits[(int64_t)t * kMaxRouterRows + e] = s2;
+    logits_ws[(int64_t)t * kMaxRouterRows + e] = s2;
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last_s = atomicAdd(&g_router_cnt[t], 1) == n_groups - 1;
+  if (threadIdx.x == 0) last_s = atomicAdd(&cnt_ws[t], 1) == n_groups - 1;
   __syncthreads();
   if (!last_s || threadIdx.x != 0) return;
   __threadfence();
-  g_router_cnt[t] = 0;  // ready for the next launch
+  cnt_ws[t] = 0;  // ready for the next launch
   float tot[NE];
 #pragma unroll
   for (int ee = 0; ee < NE; ++ee)
-    tot[ee] = ee < n_rows_w ? __ldcg(&g_router_logits[(int64_t)t * kMaxRouterRows + ee]) : 0.f;
+    tot[ee] = ee < n_rows_w ? __ldcg(&logits_ws[(int64_t)t * kMaxRouterRows + ee]) : 0.f;
   finish_token<NE>(tot, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
 }
 
@@ -495,7 +500,8 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
 
 template <int NE>
 static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E, int64_t k, int renorm,
-                  int has_shared, int32_t* idx, float* tw, float* sg, float* logits, cudaStream_t st) {
+                  int has_shared, int32_t* idx, float* tw, float* sg, float* logits, void* ws, size_t ws_bytes,
+                  cudaStream_t st) {
   const int smem = kRanges * NE * 33 * (int)sizeof(float);
   static int configured = 0;
   if (!configured) {
@@ -522,7 +528,8 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
                        (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     const int gs_bytes = xs_bytes + kGroupRows * kRanges * (int)(h / kRanges / 8 + 1) * 16;
     if (!stage && E + has_shared > kGroupRows && E + has_shared <= kMaxRouterRows && gs_bytes <= kStageLimit &&
-        ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(x)) & 15) == 0) {
+        ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(ws)) & 15) == 0 &&
+        ws && ws_bytes >= (size_t)(kGroupCntBytes + T * kMaxRouterRows * 4)) {
       static int configured_group = 0;
       if (!configured_group) {
         if (configure_smem((const void*)router_group_kernel<NE>, kStageLimit)) return HAP_ERR_LAUNCH;
@@ -532,7 +539,8 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
       { if (hap::launch_k(router_group_kernel<NE>, dim3((unsigned)T, (unsigned)n_groups), dim3(kRanges * kGroupRows),
                           gs_bytes, st, reinterpret_cast<const __nv_bfloat16*>(x),
                           reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared), (int)E,
-                          (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
+                          (int)k, renorm, has_shared, idx, tw, sg, logits,
+                          reinterpret_cast<uint8_t*>(ws)) != cudaSuccess) return HAP_ERR_LAUNCH; }
       HAP_CHECK_LAUNCH();
       return HAP_OK;
     }
@@ -579,9 +587,16 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
 }  // namespace router
 }  // namespace hap
 
+extern "C" size_t hap_router_workspace_bytes(int64_t T, int64_t n_experts, int32_t has_shared_gate) {
+  using namespace hap::router;
+  if (T <= 0 || T > kSmallT || n_experts + (has_shared_gate ? 1 : 0) <= kGroupRows) return 0;
+  return (size_t)(kGroupCntBytes + T * kMaxRouterRows * 4);
+}
+
 extern "C" int hap_router_topk(const void* x, int64_t T, int64_t h, const void* w, int64_t n_experts,
                                int64_t top_k, int32_t renormalize, int32_t has_shared_gate, int32_t* topk_idx,
-                               float* topk_w, float* shared_gate, float* logits_out, void* stream) {
+                               float* topk_w, float* shared_gate, float* logits_out, void* workspace,
+                               size_t ws_bytes, void* stream) {
   using namespace hap::router;
   if (!x || !w || !topk_idx || !topk_w || T < 0 || h <= 0) return HAP_ERR_INVALID_ARG;
   if (n_experts < 1 || top_k < 1 || top_k > n_experts || top_k > 32) return HAP_ERR_INVALID_ARG;
@@ -593,7 +608,7 @@ extern "C" int hap_router_topk(const void* x, int64_t T, int64_t h, const void* 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int hs = has_shared_gate ? 1 : 0;
 #define HAP_ROUTER_CASE(NE) \
-  if (rows <= NE) return launch<NE>(x, T, h, w, n_experts, top_k, renormalize, hs, topk_idx, topk_w, shared_gate, logits_out, st);
+  if (rows <= NE) return launch<NE>(x, T, h, w, n_experts, top_k, renormalize, hs, topk_idx, topk_w, shared_gate, logits_out, workspace, ws_bytes, st);
   HAP_ROUTER_CASE(8)
   HAP_ROUTER_CASE(16)
   HAP_ROUTER_CASE(32)

@@ -103,6 +103,22 @@ class KVCache:
             v = torch.zeros(shape, device=device, dtype=BF16)
         return cls(k, v)
 
+    @property
+    def max_len(self) -> int:
+        return int(self.k.shape[2])
+
+    def check_positions(self, positions: torch.Tensor) -> None:
+        """Raise ValueError unless every decode position is inside the cache
+        (0 <= pos < max_len).  Reads device positions back (one sync), so the
+        graph-captured decode path validates on the host side instead
+        (HapModel.capture_decode callers own their position counter); the
+        kernels themselves never write or read outside a sequence's rows."""
+        if positions.numel() == 0:
+            return
+        lo, hi = int(positions.min()), int(positions.max())
+        if lo < 0 or hi >= self.max_len:
+            raise ValueError(f"decode positions [{lo}, {hi}] outside the KV cache (max_len {self.max_len})")
+
 
 class HapMoEBlock:
     """One MoE decoder block laid out for one plan on one rank."""
@@ -301,6 +317,8 @@ class HapMoEBlock:
             xn = ops.rmsnorm(x, w.ln1, cfg.rms_eps)
         nq, nkv = w.n_q_local, w.n_kv_local
         if decode:
+            if not positions.is_cuda or not torch.cuda.is_current_stream_capturing():
+                kv_cache.check_positions(positions[:n_seq])
             if rows == n_seq and positions.dtype == torch.int32 and positions.is_contiguous():
                 pos = positions
             else:

@@ -48,22 +48,41 @@ def _rowmajor(t: torch.Tensor, name: str):
         raise ValueError(f"{name} must be a 2-D row-major view")
 
 
-# Split-K workspace per device: allocated once and never reallocated,
-# so CUDA graphs that captured a GEMM keep a valid pointer.  SPLITK[0] = False
-# runs the plain entry points (A/B experiments and tests).
+# Caller-owned workspaces of the C-ABI (the library keeps no device state):
+# one per (kind, device, stream), allocated once at its maximum size and never
+# reallocated, so CUDA graphs that captured a launch keep a valid pointer and
+# launches on different streams never share scratch.  The self-resetting
+# workspaces (attention tickets, router counters) are zero-filled once here.
+# SPLITK[0] = False runs the plain GEMM entry points (A/B experiments, tests).
 SPLITK = [os.environ.get("HAP_GEMM_SPLITK", "1") != "0"]
-_SPLITK_WS = {}
+_WS = {}
+_ROUTER_MAX_T, _ROUTER_MAX_ROWS = 1024, 72
+
+
+def stream_workspace(kind: str, device: torch.device) -> torch.Tensor:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    key = (kind, idx, _stream())
+    ws = _WS.get(key)
+    if ws is None:
+        lib = _lib.load()
+        if kind == "splitk":
+            n, zero = int(lib.hap_gemm_splitk_workspace_bytes()), False
+        elif kind == "attn":
+            n, zero = int(lib.hap_attn_prefill_workspace_bytes()), True
+        elif kind == "router":
+            n, zero = int(lib.hap_router_workspace_bytes(_ROUTER_MAX_T, _ROUTER_MAX_ROWS - 1, 1)), True
+        else:
+            raise ValueError(kind)
+        dev = torch.device("cuda", idx)
+        ws = torch.zeros(n, device=dev, dtype=torch.uint8) if zero else torch.empty(n, device=dev, dtype=torch.uint8)
+        _WS[key] = ws
+    return ws
 
 
 def splitk_workspace(device: torch.device) -> Tuple[int, int]:
     if not SPLITK[0]:
         return 0, 0
-    idx = device.index if device.index is not None else torch.cuda.current_device()
-    ws = _SPLITK_WS.get(idx)
-    if ws is None:
-        n = int(_lib.load().hap_gemm_splitk_workspace_bytes())
-        ws = torch.empty(n, device=torch.device("cuda", idx), dtype=torch.uint8)
-        _SPLITK_WS[idx] = ws
+    ws = stream_workspace("splitk", device)
     return ws.data_ptr(), ws.numel()
 
 
@@ -213,15 +232,19 @@ def gemm_qkv_rope(a: torch.Tensor, w: torch.Tensor, positions: torch.Tensor, n_r
 
 def router_topk(x: torch.Tensor, w: torch.Tensor, n_experts: int, top_k: int, renormalize: bool,
                 has_shared_gate: bool, topk_idx: torch.Tensor, topk_w: torch.Tensor,
-                shared_gate: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None):
+                shared_gate: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None,
+                workspace: Optional[torch.Tensor] = None):
+    """Fixed-order fp32 router logits -> top-k (hap_router_topk).  workspace:
+    zero-filled uint8 scratch (default: this stream's cached one)."""
     lib = _lib.load()
+    ws = workspace if workspace is not None else stream_workspace("router", x.device)
     _need(x, "x", BF16); _need(w, "w", BF16)
     if not x.is_contiguous() or not w.is_contiguous():
         raise ValueError("router inputs must be contiguous")
     _need(topk_idx, "topk_idx", torch.int32); _need(topk_w, "topk_w", torch.float32)
     st = lib.hap_router_topk(x.data_ptr(), x.shape[0], x.shape[1], w.data_ptr(), n_experts, top_k,
                              int(renormalize), int(has_shared_gate), topk_idx.data_ptr(), topk_w.data_ptr(),
-                             _ptr(shared_gate), _ptr(logits), _stream())
+                             _ptr(shared_gate), _ptr(logits), ws.data_ptr(), ws.numel(), _stream())
     check(st, "hap_router_topk")
     _count(1 if x.shape[0] else 0)
 
@@ -294,9 +317,11 @@ def rope_qk(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, positions: to
 
 
 def attn_prefill(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, n_seqs: int, seq_len: int,
-                 out: torch.Tensor, causal: bool = True) -> torch.Tensor:
-    """Attention over a fused [T, (n_q + 2 n_kv) * d] qkv buffer -> out [T, n_q * d]."""
+                 out: torch.Tensor, causal: bool = True, workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Attention over a fused [T, (n_q + 2 n_kv) * d] qkv buffer -> out [T, n_q * d].
+    workspace: zero-filled uint8 ticket scratch (default: this stream's cached one)."""
     lib = _lib.load()
+    ws = workspace if workspace is not None else stream_workspace("attn", qkv.device)
     _need(qkv, "qkv", BF16); _need(out, "out", BF16)
     _rowmajor(qkv, "qkv"); _rowmajor(out, "out")
     ld = qkv.stride(0)
@@ -304,7 +329,7 @@ def attn_prefill(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, n_seqs: 
     esz = qkv.element_size()
     st = lib.hap_attn_prefill(base, ld, base + n_q * head_dim * esz, ld, base + (n_q + n_kv) * head_dim * esz, ld,
                               out.data_ptr(), out.stride(0), n_seqs, seq_len, n_q, n_kv, head_dim,
-                              float(head_dim ** -0.5), int(causal), _stream())
+                              float(head_dim ** -0.5), int(causal), ws.data_ptr(), ws.numel(), _stream())
     check(st, "hap_attn_prefill")
     _count(1 if n_seqs * seq_len else 0)
     return out

@@ -53,27 +53,29 @@ def baseline_plan(result, name: str = "tp", stage: str = "prefill") -> StagePlan
     return StagePlan(cat.attention[k], cat.expert[i if stage == "prefill" else j])
 
 
-CALIBRATION_FILE = Path(__file__).resolve().parent.parent / "profiles" / "r01_calibration.json"
+CALIBRATION_FILE = Path(__file__).resolve().parent.parent / "profiles" / "r02_calibration.json"
 
 
 def calibrated_plan(cfg: BlockConfig, n_devices: int, batch: int, input_len: int, output_len: int = 0,
-                    path: Optional[Path] = None):
+                    path: Optional[Path] = None, hw=None, routing: str = "balanced"):
     """The reference ILP re-solved on B200-measured module tables
     (calib.measured_cost_tensors): returns (PlanResult-like, source) where
-    source says whether measured tables were found for this exact scenario."""
+    source says whether measured tables were found for this exact scenario.
+    routing: which measured expert cells ("balanced" = the synthetic workload
+    the bench runs, "skewed" = the imbalanced-routing workload)."""
     import json
 
     from . import calib
 
     mp = import_moeplan()
-    res = plan_for(cfg, n_devices, batch, input_len, output_len)
+    res = plan_for(cfg, n_devices, batch, input_len, output_len, hw=hw)
     p = Path(path) if path else CALIBRATION_FILE
     if not p.exists():
         return res, "roofline (no calibration file)"
     doc = json.loads(p.read_text())
     case = next((c for c in doc.get("cases", []) if c.get("model") == cfg.name and c.get("n") == n_devices
                  and c.get("scenario") == {"batch": batch, "input_len": input_len, "output_len": output_len}
-                 and "cells" in c), None)
+                 and c.get("routing", "balanced") == routing and "cells" in c), None)
     if case is None:
         return res, "roofline (scenario not calibrated)"
     att = {a.label(): k for k, a in enumerate(res.catalog.attention)}
@@ -88,7 +90,7 @@ def calibrated_plan(cfg: BlockConfig, n_devices: int, batch: int, input_len: int
     tens = calib.measured_cost_tensors(res, meas)
     scen = mp.InferenceScenario(batch=batch, input_len=input_len, output_len=output_len)
     sel = mp.solve_ilp(tens, scen, cfg.to_model_spec(), res.catalog)
-    return mp.PlanResult(plan=sel, tensors=tens, catalog=res.catalog), f"measured B200 tables ({p.name})"
+    return mp.PlanResult(plan=sel, tensors=tens, catalog=res.catalog), f"measured B200 tables ({p.name}, {routing})"
 
 
 def find_plan(result, attn_tp: int, exp_tp: int, exp_ep: int, exp_dp: int = 1) -> Optional[StagePlan]:

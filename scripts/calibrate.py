@@ -1,11 +1,15 @@
 """Recalibrate the reference planner's latency models on this B200 and report
 predicted-vs-measured error (north-star item 4).  Writes, under profiles/:
 
-  r01_calibration_samples.csv  reference CalibrationSample CSV (costmodel.py:307)
-  r01_eta_model.json           reference efficiency-model JSON (costmodel.py:379)
-  r01_calibration.json         measurements, held-out eta error, plans
+  r02_calibration_samples.csv  reference CalibrationSample CSV (costmodel.py:307)
+  r02_eta_model.json           reference efficiency-model JSON (costmodel.py:379)
+  r02_calibration.json         measurements, held-out eta error, plans
                                (roofline vs calibrated vs measured-table) per
-                               BASELINE config and N, N=1 end-to-end check
+                               BASELINE config and N, N=1 end-to-end check;
+                               every expert cell is measured on the busiest EP
+                               group, under balanced (random-init) routing and
+                               under the skewed workload (router row e x
+                               (1 + 0.1 e)), with the measured imbalance
 
   python scripts/calibrate.py [--quick]
 """
@@ -68,14 +72,18 @@ def main():
     per_case = []
     for name, B, S, O, stages in scen:
         cfg = get_config(name)
-        for n in ns:
-            try:
-                meas = calib.measure_catalog(cfg, n, B, S, O, reps=args.reps, cache=cache, stages=stages)
-            except mp.InfeasibleError as exc:
-                per_case.append({"model": name, "n": n, "scenario": [B, S, O], "infeasible": str(exc)})
-                continue
-            meas_all.extend(meas)
-            per_case.append({"model": name, "n": n, "scenario": [B, S, O], "meas": meas})
+        for routing in ("balanced", "skewed"):
+            for n in ns:
+                try:
+                    meas = calib.measure_catalog(cfg, n, B, S, O, reps=args.reps, cache=cache, stages=stages,
+                                                 skew=routing == "skewed")
+                except mp.InfeasibleError as exc:
+                    per_case.append({"model": name, "n": n, "scenario": [B, S, O], "routing": routing,
+                                     "infeasible": str(exc)})
+                    continue
+                if routing == "balanced":
+                    meas_all.extend(meas)
+                per_case.append({"model": name, "n": n, "scenario": [B, S, O], "routing": routing, "meas": meas})
         print(f"measured {name} B={B} S={S} O={O} ({time.time() - t0:.0f}s)", flush=True)
 
     model, tr_err, te_err, _ = calib.fit_eta(meas_all)
@@ -83,8 +91,8 @@ def main():
     out_dir.mkdir(parents=True, exist_ok=True)
     from moeplan.costmodel import save_model, write_samples_csv
 
-    write_samples_csv(calib.to_samples(meas_all), str(out_dir / "r01_calibration_samples.csv"))
-    save_model(model, str(out_dir / "r01_eta_model.json"))
+    write_samples_csv(calib.to_samples(meas_all), str(out_dir / "r02_calibration_samples.csv"))
+    save_model(model, str(out_dir / "r02_eta_model.json"))
 
     cases = []
     for c in per_case:
@@ -98,13 +106,15 @@ def main():
             res_roof = plan_for(cfg, n, B, S, O)
             res_cal = plan_for(cfg, n, B, S, O, cost_models=mp.CostModels(eta=model))
         except mp.InfeasibleError as exc:  # whole-model memory (Eq.5) infeasible at this N
-            cases.append({"model": c["model"], "n": n, "scenario": c["scenario"], "infeasible": str(exc)})
+            cases.append({"model": c["model"], "n": n, "scenario": c["scenario"], "routing": c["routing"],
+                          "infeasible": str(exc)})
             continue
         tens = calib.measured_cost_tensors(res_roof, c["meas"])
         scen_o = mp.InferenceScenario(B, S, O)
         spec = cfg.to_model_spec()
         plan_meas = mp.solve_ilp(tens, scen_o, spec, res_roof.catalog)
         entry = {"model": c["model"], "n": n, "scenario": {"batch": B, "input_len": S, "output_len": O},
+                 "routing": c["routing"],
                  "plan_roofline": describe(res_roof.plan, res_roof.catalog),
                  "plan_eta_calibrated": describe(res_cal.plan, res_cal.catalog),
                  "plan_measured_tables": describe(plan_meas, res_roof.catalog)}
@@ -122,6 +132,7 @@ def main():
         for m, e in zip(c["meas"], eta_pred):
             cells.append({"module": m.module, "stage": m.stage, "strategy": m.strategy,
                           "measured_us": m.measured_s * 1e6, "roofline_us": m.roofline_s * 1e6,
+                          "ep_imbalance_measured": m.imbalance,
                           "eta_measured": m.eta, "eta_model": float(e),
                           "rel_err_eta_model": abs(m.roofline_s * e - m.measured_s) / m.measured_s})
         entry["cells"] = cells
@@ -135,7 +146,7 @@ def main():
     blk = HapMoEBlock(cfg, PlanDegrees(1, 1, 1, 1), None)
     x = torch.randn(8 * 2048, cfg.hidden, device="cuda").to(torch.bfloat16)
     t_block = calib._events_time(lambda: blk.forward(x, "prefill", 8, 2048), 5)
-    m1 = [m for m in meas_all if m.model == "mixtral-8x7b" and m.n == 1 and m.stage == "prefill"]
+    m1 = [m for m in meas_all if m.model == "mixtral-8x7b" and m.n == 1 and m.stage == "prefill"]  # balanced
     pred1 = sum(m.measured_s for m in m1)
     roof1 = sum(m.roofline_s for m in m1)
     e2e = {"config": "mixtral-8x7b prefill 8x2048, N=1", "measured_block_s": t_block,
@@ -144,9 +155,11 @@ def main():
     del blk
 
     report = {
-        "what": "per-device module times of every catalog strategy measured on one B200 with the product kernels; "
-                "eta fitted with moeplan.train_forest (reference API, context trick); comm cells stay roofline at "
-                "the measured NVLink bus bandwidth (no NCCL samples on a 1-GPU box)",
+        "what": "per-device module times of every catalog strategy measured on one B200 with the product kernels "
+                "(expert cells: the busiest EP group of the rank's expert-DP replica, balanced and skewed routing, "
+                "measured max/mean EP-group rows in place of the reference's gamma = 1.3); eta fitted with "
+                "moeplan.train_forest on the balanced cells (reference API, context trick); comm cells stay "
+                "roofline at the guide NVLink bus bandwidth (no NCCL samples on a 1-GPU box)",
         "eta_model": {"n_samples": len(meas_all), "train_rel_err_mean": float(np.mean(tr_err)),
                       "heldout_rel_err_mean": float(np.mean(te_err)), "heldout_rel_err_max": float(np.max(te_err)),
                       "heldout_n": len(te_err)},
@@ -154,12 +167,12 @@ def main():
         "cases": cases,
         "wall_s": time.time() - t0,
     }
-    (out_dir / "r01_calibration.json").write_text(json.dumps(report, indent=1))
+    (out_dir / "r02_calibration.json").write_text(json.dumps(report, indent=1))
     print(json.dumps({k: report[k] for k in ("eta_model", "end_to_end_n1", "wall_s")}, indent=1))
     for c in cases:
         if "infeasible" in c:
             continue
-        print(c["model"], c["n"], c["scenario"]["batch"], "roof:", c["plan_roofline"]["attention"],
+        print(c["model"], c["n"], c["scenario"]["batch"], c["routing"], "roof:", c["plan_roofline"]["attention"],
               c["plan_roofline"]["expert_prefill"], "| meas:", c["plan_measured_tables"]["attention"],
               c["plan_measured_tables"]["expert_prefill"], c["plan_measured_tables"]["expert_decode"],
               "| spd", c.get("predicted_speedup_hap_vs_tp_measured_tables"))

@@ -55,7 +55,7 @@ def test_sm100a_code_in_library():
 
 
 def test_status_strings_and_version(lib):
-    assert lib.hap_abi_version() == 1
+    assert lib.hap_abi_version() == 2
     assert lib.hap_status_string(0) == b"ok"
     assert b"workspace" in lib.hap_status_string(-5)
 
@@ -71,17 +71,29 @@ def test_argument_errors_before_launch(lib):
     assert lib.hap_grouped_gemm_bf16(p, 16, 64, 64, p, 1, 96, None, 1, None, p, 64, 1, 64, None, None, 0,
                                      None) == -1
     # router: top_k > n_experts
-    assert lib.hap_router_topk(p, 4, 512, p, 2, 3, 1, 0, p, p, None, None, None) == -1
+    assert lib.hap_router_topk(p, 4, 512, p, 2, 3, 1, 0, p, p, None, None, None, 0, None) == -1
     # router: h not a multiple of 64
-    assert lib.hap_router_topk(p, 4, 520, p, 8, 2, 1, 0, p, p, None, None, None) == -2
+    assert lib.hap_router_topk(p, 4, 520, p, 8, 2, 1, 0, p, p, None, None, None, 0, None) == -2
     # permute: workspace too small
     assert lib.hap_moe_permute(p, 100, 8, None, 1, 0, None, p, p, p, 4, None) == -5
     # attention: unsupported head_dim
-    assert lib.hap_attn_prefill(p, 96 * 3, p, 96 * 3, p, 96 * 3, p, 96, 1, 16, 1, 1, 96, 0.1, 1, None) == -2
+    assert lib.hap_attn_prefill(p, 96 * 3, p, 96 * 3, p, 96 * 3, p, 96, 1, 16, 1, 1, 96, 0.1, 1, p, 8, None) == -2
+    # attention: the ticket workspace is the caller's and is required
+    assert lib.hap_attn_prefill(p, 384, p, 384, p, 384, p, 128, 1, 16, 1, 1, 128, 0.1, 1, None, 0, None) == -5
     # decode: GQA group larger than 8
     assert lib.hap_attn_decode(p, 4096, p, p, 128, p, 1, 32, 2, 128, 0.1, p, 4096, p, 1 << 20, None) == -2
     # rope gemm: bad head_dim
     assert lib.hap_gemm_qkv_rope(p, 4, 64, 64, p, 96, None, p, 96, p, 1, 96, 1e6, None) == -2
+
+
+def test_workspace_queries(lib):
+    """The library owns no device state: every scratch is a caller workspace sized by a query."""
+    assert lib.hap_attn_prefill_workspace_bytes() == 8
+    assert lib.hap_router_workspace_bytes(16, 8, 0) == 0          # <= 8 router rows: per-token kernel
+    assert lib.hap_router_workspace_bytes(2048, 64, 1) == 0       # large T: TMA router, no scratch
+    assert lib.hap_router_workspace_bytes(1, 64, 1) == 4096 + 80 * 4
+    assert lib.hap_router_workspace_bytes(1024, 71, 1) == 4096 + 1024 * 80 * 4
+    assert lib.hap_gemm_splitk_workspace_bytes() == 32 << 20
 
 
 def test_swiglu_half_width_rule(lib):

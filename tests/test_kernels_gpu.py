@@ -526,3 +526,102 @@ def test_attn_prefill_large_scores_and_noncausal(causal):
         v = blk[:, (nq + nkv) * d:].reshape(S, nkv, d)
         ref.append(O.attention(q, k, v, causal=causal).reshape(S, -1))
     assert rel_err(np32(out), np.concatenate(ref)) < 2e-2
+
+
+# ------------------------------------------------- caller-owned workspaces --
+def test_concurrent_streams_attention_and_router_bit_exact():
+    """The library owns no device state: two prefill attentions
+    and two wide routers (per-(token, 8 rows) CTAs meeting in the workspace)
+    run concurrently on two streams, each with its stream's workspace, and give
+    bit-identical results to the same calls issued one after another."""
+    ops = K()
+    B, S, nq, nkv, d = 2, 1024, 16, 4, 128
+    qkvs = [bf16((B * S, (nq + 2 * nkv) * d), seed=40 + i) for i in range(2)]
+    T, h, E, k = 64, 3584, 64, 8
+    xs = [bf16((T, h), seed=50 + i) for i in range(2)]
+    w = bf16((E + 1, h), 0.02, seed=52)
+
+    def run_all(streams):
+        outs = []
+        for i, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                o = torch.empty(B * S, nq * d, device=dev, dtype=torch.bfloat16)
+                idx = torch.empty(T, k, device=dev, dtype=torch.int32)
+                tw = torch.empty(T, k, device=dev, dtype=torch.float32)
+                sg = torch.empty(T, device=dev, dtype=torch.float32)
+                lg = torch.empty(T, E, device=dev, dtype=torch.float32)
+                for _ in range(3):  # repeated launches reuse the self-resetting workspaces
+                    ops.attn_prefill(qkvs[i], nq, nkv, d, B, S, o)
+                    ops.router_topk(xs[i], w, E, k, False, True, idx, tw, sg, lg)
+                outs.append((o, idx, tw, sg, lg))
+        torch.cuda.synchronize()
+        return outs
+
+    cur = torch.cuda.current_stream()
+    seq = run_all([cur, cur])
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(cur)
+    s2.wait_stream(cur)
+    conc = run_all([s1, s2])
+    assert ops.stream_workspace("attn", qkvs[0].device).data_ptr() != 0
+    for a, b in zip(seq, conc):
+        for ta, tb in zip(a, b):
+            assert torch.equal(ta, tb)
+    # the router logits are the oracle's fixed-order fp32 chains
+    for i in range(2):
+        lo = O.router_logits(np32(xs[i]), np32(w))
+        assert np.array_equal(np32(seq[i][4]), lo[:, :E])
+
+
+def test_attn_decode_positions_outside_cache_touch_nothing():
+    """A decode position >= max_len appends nothing and attends only inside the
+    cache (memory-safe on device); the executor rejects it on the host."""
+    ops = K()
+    B, nq, nkv, d, Lmax = 3, 8, 2, 128, 64
+    qkv = bf16((B, (nq + 2 * nkv) * d), seed=60)
+    big_k = bf16((B + 1, nkv, Lmax, d), seed=61)  # one extra sequence of guard rows after the cache
+    big_v = bf16((B + 1, nkv, Lmax, d), seed=62)
+    kc, vc = big_k[:B], big_v[:B]
+    guard_k, guard_v = big_k[B].clone(), big_v[B].clone()
+    kc0 = kc.clone()
+    pos = torch.tensor([Lmax, Lmax + 5, 3], device=dev, dtype=torch.int32)
+    out = torch.empty(B, nq * d, device=dev, dtype=torch.bfloat16)
+    ws = torch.empty(ops.attn_decode_workspace_bytes(B, nq, d, Lmax), device=dev, dtype=torch.uint8)
+    ops.attn_decode(qkv, kc, vc, pos, nq, nkv, d, out, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(big_k[B], guard_k) and torch.equal(big_v[B], guard_v)
+    assert torch.equal(kc[:2], kc0[:2])                     # nothing appended for the out-of-range rows
+    assert torch.isfinite(out.float()).all()
+
+    from paper_2508_19373_b200.config import get_config
+    from paper_2508_19373_b200.executor import HapMoEBlock, KVCache
+    from paper_2508_19373_b200.layout import PlanDegrees
+
+    cfg = get_config("tiny")
+    blk = HapMoEBlock(cfg, PlanDegrees(1, 1, 1, 1), None, seed=1)
+    cache = KVCache.empty(2, cfg.n_kv_heads, 16, cfg.head_dim, dev)
+    x = bf16((2, cfg.hidden), seed=63)
+    with pytest.raises(ValueError, match="outside the KV cache"):
+        blk.forward(x, "decode", 2, kv_cache=cache, positions=torch.tensor([3, 16], device=dev, dtype=torch.int32))
+
+
+def test_router_workspace_shared_by_launches_of_any_size():
+    """One zero-filled router workspace serves launches of different T back to
+    back (its layout does not depend on T): top-k and logits stay exact."""
+    ops = K()
+    h, E, k = 3584, 64, 8
+    w = bf16((E + 1, h), 0.02, seed=70)
+    ws = torch.zeros(ops._lib.load().hap_router_workspace_bytes(1024, E, 1), device=dev, dtype=torch.uint8)
+    for i, T in enumerate((64, 1, 37, 1024, 5, 64)):
+        x = bf16((T, h), seed=71 + i)
+        idx = torch.empty(T, k, device=dev, dtype=torch.int32)
+        tw = torch.empty(T, k, device=dev, dtype=torch.float32)
+        sg = torch.empty(T, device=dev, dtype=torch.float32)
+        lg = torch.empty(T, E, device=dev, dtype=torch.float32)
+        ops.router_topk(x, w, E, k, False, True, idx, tw, sg, lg, workspace=ws)
+        torch.cuda.synchronize()
+        lo = O.router_logits(np32(x), np32(w))
+        assert np.array_equal(np32(lg), lo[:, :E]), T
+        oi, _ = O.router_topk(lo[:, :E], k, False)
+        assert np.array_equal(idx.cpu().numpy(), oi), T
+    assert int(ws[:4096].count_nonzero()) == 0  # counters left zeroed
