@@ -254,30 +254,74 @@ def cpu_cores() -> int:
 
 
 def cpu_reference_setup(cfg, sample_tokens: int):
-    """The oracle port of the block (numpy, all host cores) on a bounded sample."""
+    """The oracle port of the block (numpy fp32 matmuls on every host core, the
+    BASELINE.md §3 plan) on a bounded prefill sample."""
     import numpy as np
 
     from oracle import moe_block as O
 
-    spec = O.BlockSpec(hidden=cfg.hidden, n_q_heads=cfg.n_q_heads, n_kv_heads=cfg.n_kv_heads,
-                       head_dim=cfg.head_dim, n_experts=cfg.n_experts, top_k=cfg.top_k, inter=cfg.inter,
-                       n_shared=cfg.n_shared, norm_topk_prob=cfg.norm_topk_prob, qkv_bias=cfg.qkv_bias,
-                       rope_theta=cfg.rope_theta, rms_eps=cfg.rms_eps)
-    W = O.random_weights(spec, seed=0, bf16=False)
+    O.set_precision("f32")
+    spec = _oracle_spec(cfg)
+    W = _oracle_weights(cfg)
     x = np.random.default_rng(1).standard_normal((sample_tokens, cfg.hidden)).astype(np.float32)
     return lambda: O.block_forward(spec, W, x, 1)
 
 
-def cpu_baseline(cfg, sample_tokens: int, reps: int = 2):
+def _oracle_spec(cfg):
+    from oracle import moe_block as O
+
+    return O.BlockSpec(hidden=cfg.hidden, n_q_heads=cfg.n_q_heads, n_kv_heads=cfg.n_kv_heads,
+                       head_dim=cfg.head_dim, n_experts=cfg.n_experts, top_k=cfg.top_k, inter=cfg.inter,
+                       n_shared=cfg.n_shared, norm_topk_prob=cfg.norm_topk_prob, qkv_bias=cfg.qkv_bias,
+                       rope_theta=cfg.rope_theta, rms_eps=cfg.rms_eps)
+
+
+_ORACLE_W = {}
+
+
+def _oracle_weights(cfg):
+    from oracle import moe_block as O
+
+    if cfg.name not in _ORACLE_W:
+        _ORACLE_W[cfg.name] = O.random_weights(_oracle_spec(cfg), seed=0, bf16=False)
+    return _ORACLE_W[cfg.name]
+
+
+def cpu_decode_baseline(cfg, batch: int = DECODE_BATCH, kv: int = DECODE_KV):
+    """One full-size decode step (B=64 @ kv 2048) of the oracle port, fp32, all host cores."""
+    import numpy as np
+
+    from oracle import moe_block as O
+
+    O.set_precision("f32")
+    spec = _oracle_spec(cfg)
+    W = _oracle_weights(cfg)
+    rng = np.random.default_rng(7)
+    kc = rng.standard_normal((batch, cfg.n_kv_heads, kv, cfg.head_dim), dtype=np.float32)
+    vc = rng.standard_normal((batch, cfg.n_kv_heads, kv, cfg.head_dim), dtype=np.float32)
+    x = rng.standard_normal((batch, cfg.hidden), dtype=np.float32)
+    pos = np.full(batch, kv - 1)
+    O.decode_forward(spec, W, x, kc, vc, pos)
+    t0 = time.perf_counter()
+    O.decode_forward(spec, W, x, kc, vc, pos)
+    dt = time.perf_counter() - t0
+    return {"value": batch / dt, "unit": "tokens/s", "ms_per_step": dt * 1e3, "cores": cpu_cores(),
+            "sample": f"one {cfg.name} decode step B={batch} @ kv {kv} through oracle decode_forward (fp32)"}
+
+
+def cpu_baseline(cfg, sample_tokens: int, reps: int = 2, decode: bool = True):
     fn = cpu_reference_setup(cfg, sample_tokens)
     fn()
     t0 = time.perf_counter()
     for _ in range(reps):
         fn()
     dt = (time.perf_counter() - t0) / reps
-    return {"value": sample_tokens / dt, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
-            "sample": f"oracle/moe_block.py block_forward (numpy fp64 matmuls, {cfg.name} full dims), "
-                      f"1 sequence x {sample_tokens} tokens prefill, mean of {reps}"}
+    out = {"value": sample_tokens / dt, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+           "sample": f"oracle/moe_block.py block_forward (numpy fp32 matmuls on all host cores, {cfg.name} full "
+                     f"dims), 1 sequence x {sample_tokens} tokens prefill, mean of {reps}"}
+    if decode:
+        out["decode"] = cpu_decode_baseline(cfg)
+    return out
 
 
 def run_reference(args):
@@ -305,11 +349,11 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name} MoE block prefill (bounded CPU sample)", "model": cfg.name,
                    "global_batch": 1, "seq_len": args.cpu_sample_tokens, "parallelism": "host cores"},
         "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
-                         "sample": f"1 x {args.cpu_sample_tokens} tokens per step through oracle/moe_block.py"},
+                         "sample": f"1 x {args.cpu_sample_tokens} tokens per step through oracle/moe_block.py (numpy fp32, all host cores)"},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -344,13 +344,26 @@ class HapMoEBlock:
                 ops.attn_prefill(qkv, nq, nkv, d, n_seq, S, attn)
         with self._timed("o_proj"):
             h1 = ops.gemm(attn, w.wo, residual=x if lay.a_tp_rank == 0 else None)
-        self._coll("all_reduce", h1, "attn_tp_group")
+        c = rows // self.deg.a_tp  # rows this rank owns after the reduce-scatter
+        # expert shard = this rank's 1/a_tp of its replica (expert tp 1): the
+        # attention partial sums are reduce-scattered straight onto the shards
+        # (RS here + the AllGather after the experts = the AllReduce the
+        # reference charges, strategies.py:314-322), else all-reduced
+        rs_attn = self.deg.a_tp > 1 and self.deg.e_tp == 1
+        if rs_attn:
+            h1c = torch.empty(c, h, device=dev, dtype=BF16)
+            self.comm.reduce_scatter(h1c, h1, "attn_tp_group")
+            h1 = h1c
+        else:
+            self._coll("all_reduce", h1, "attn_tp_group")
         with self._timed("norm"):
             hn = ops.rmsnorm(h1, w.ln2, cfg.rms_eps)
 
         # ---------------- boundary: attention layout -> expert shard
         S_e, a_dp = lay.n_shards, self.deg.a_dp
-        if S_e < a_dp:
+        if rs_attn:
+            hn_s = hn
+        elif S_e < a_dp:
             R = a_dp // S_e
             hn_s = torch.empty(R * rows, h, device=dev, dtype=BF16)
             self.comm.all_gather(hn_s, hn, "gather_group")
@@ -365,8 +378,7 @@ class HapMoEBlock:
             self.capture.update(qkv=qkv, attn=attn, h1=h1, hn=hn, hn_s=hn_s)
 
         # ---------------- expert module (partial over expert tp)
-        c = rows // self.deg.a_tp  # rows this rank owns after the reduce-scatter
-        residual = h1[lay.a_tp_rank * c:(lay.a_tp_rank + 1) * c]
+        residual = h1 if rs_attn else h1[lay.a_tp_rank * c:(lay.a_tp_rank + 1) * c]
         y = self._experts(hn_s, residual, res_row0=lay.e_tp_rank * c, res_rows=c)
 
         # ---------------- back to the attention layout
