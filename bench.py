@@ -485,17 +485,23 @@ def main():
     gu_flops = 2.0 * rows_here * 2 * il * cfg.hidden
     dn_flops = 2.0 * rows_here * il * cfg.hidden
     achieved = gu_flops / (gu_ms / 1e3) / 1e12
-    prof = ROOT / "profiles" / "r01_gateup_traffic.json"
-    traffic = None
-    if prof.exists():
+    # DRAM traffic of the same launch from the newest committed ncu --set full capture
+    # (profiles/<round>_gemm_traffic.json, written by scripts/summarize_profiles.py)
+    traffic, traffic_src, traffic_ratio = None, None, None
+    caps = sorted((ROOT / "profiles").glob("r*_gemm_traffic.json"))
+    if caps:
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(caps[-1].read_text())
+            traffic = tj["gate_up"]["dram_bytes_per_launch"]
+            traffic_ratio = tj["gate_up"]["traffic_over_algorithmic"]
+            traffic_src = f"profiles/{caps[-1].name}"
         except Exception:
             traffic = None
     roofline = {"kernel": "hap::gemm::grouped_gemm_kernel (expert gate/up, SwiGLU epilogue)", "bound": "tensor",
                 "achieved": achieved, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16_tflops_sustained"], "peak_kind": f"{peaks['source']} sustained",
                 "frac_of_burst_peak": achieved / peaks["bf16_tflops"], "traffic": traffic,
+                "traffic_over_algorithmic_bytes": traffic_ratio, "traffic_source": traffic_src,
                 "algorithmic_flops_per_launch": gu_flops, "launch_ms": gu_ms,
                 "down_proj": {"launch_ms": dn_ms, "achieved": dn_flops / (dn_ms / 1e3) / 1e12},
                 "expert_gemms_share_of_step": (gu_ms + dn_ms) / results["hap"]["prefill_ms"]}

@@ -228,9 +228,66 @@ int hap_moe_combine(const void* y, const int32_t* dst_of_row, const float* topk_
                     int64_t h, const void* residual, int64_t res_row0, int64_t res_rows, const void* shared_y,
                     const float* shared_gate, void* out, void* stream);
 
+/*
+ * Combine whose output rows leave as a reduce-scatter push: token t's row goes
+ * to row (slot*chunk_rows + t % chunk_rows) of the buffer dst_tab[t / chunk_rows]
+ * (device int64 table of peer-mapped bases, one per chunk owner; T a multiple
+ * of chunk_rows).  With slot = this rank's index in the group every owner
+ * receives the partial sums of its chunk from every rank, in slot order, for
+ * hap_reduce_slots_bf16.  Same arithmetic as hap_moe_combine.
+ * Replaces: the expert-TP ReduceScatter / DP<-TP boundary of comm_volume
+ * (strategies.py:324-332, 341-342) as a separate NCCL call.
+ */
+int hap_moe_combine_chunked(const void* y, const int32_t* dst_of_row, const float* topk_w, int64_t T, int64_t k,
+                            int64_t h, const void* residual, int64_t res_row0, int64_t res_rows,
+                            const void* shared_y, const float* shared_gate, const int64_t* dst_tab,
+                            int64_t chunk_rows, int64_t slot, void* stream);
+
 /* RMSNorm (fp32 statistics): out = w * (x * rsqrt(mean(x^2) + eps)). */
 int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, const void* w, float eps, void* out,
                 int64_t ldo, void* stream);
+
+/*
+ * RMSNorm whose rows are stored to every base in dst_tab (device int64 table
+ * of n_dst <= 64 bases, typically this replica's row block in every rank's
+ * peer-mapped gather buffer): the DP->TP boundary AllGather pushed by the
+ * kernel that produces the rows (strategies.py:324-332).
+ */
+int hap_rmsnorm_multi(const void* x, int64_t T, int64_t h, int64_t ldx, const void* w, float eps,
+                      const int64_t* dst_tab, int32_t n_dst, int64_t ldo, void* stream);
+
+/*
+ * Device-side group barrier over peer memory: sig_tab holds n_ranks device
+ * addresses of each rank's int32[n_ranks] flag row (peer-mapped), epoch is
+ * this rank's int32 counter (device).  Waits for every earlier kernel of the
+ * stream, publishes epoch+1 to every rank (system-scope release) and spins
+ * until all ranks published it.  Flags and counters start at 0 on every
+ * rank.  No host work: CUDA-graph capturable.
+ */
+int hap_peer_barrier(const int64_t* sig_tab, int32_t* epoch, int32_t n_ranks, int32_t rank, void* stream);
+
+/*
+ * out[r, :] = sum_{s < n_slots} slots[s*rows + r, :]  (fp32 in slot order,
+ * one bf16 rounding): the owner side of a pushed reduce-scatter.
+ */
+int hap_reduce_slots_bf16(const void* slots, int64_t n_slots, int64_t rows, int64_t h, void* out, void* stream);
+
+/* Copy n int32 from src to (dst_tab[p] + dst_offset_bytes) for each of the n_dst device bases. */
+int hap_peer_broadcast_i32(const int32_t* src, int64_t n, const int64_t* dst_tab, int32_t n_dst,
+                           int64_t dst_offset_bytes, void* stream);
+
+/*
+ * EP dispatch/combine plan on the device from the gathered segment offsets
+ * segs[s][0..E] (int32 [ep][E+1], E = ep*experts_local) of every EP rank s:
+ * dst_row0[e] (int64) = row of this rank's expert-e segment in rank
+ * e/experts_local's receive buffer (blocks (source, local expert) in
+ * lexicographic order); seg_r (int32 [E+1]) = this rank's receive-block
+ * offsets; seg_dst_row0 (int32 [E]) = for receive block (s, j) the row of
+ * source s's permuted segment of expert me*experts_local + j.  Replaces the
+ * host-side count exchange of the EP all-to-alls (strategies.py:334-338).
+ */
+int hap_ep_exchange_plan(const int32_t* segs, int32_t ep, int32_t experts_local, int32_t me, int64_t* dst_row0,
+                         int32_t* seg_r, int32_t* seg_dst_row0, void* stream);
 
 /*
  * In-place rotary embedding (rotate-half convention) on the q and k heads of

@@ -92,9 +92,25 @@ SIGNATURES = {
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p,
          c_void_p, c_void_p, c_void_p],
     ),
+    "hap_moe_combine_chunked": (
+        ctypes.c_int,
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p,
+         c_void_p, c_void_p, c_int64, c_int64, c_void_p],
+    ),
     "hap_rmsnorm": (
         ctypes.c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_float, c_void_p, c_int64, c_void_p],
+    ),
+    "hap_rmsnorm_multi": (
+        ctypes.c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_float, c_void_p, ctypes.c_int32, c_int64, c_void_p],
+    ),
+    "hap_peer_barrier": (ctypes.c_int, [c_void_p, c_void_p, ctypes.c_int32, ctypes.c_int32, c_void_p]),
+    "hap_reduce_slots_bf16": (ctypes.c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "hap_peer_broadcast_i32": (ctypes.c_int, [c_void_p, c_int64, c_void_p, ctypes.c_int32, c_int64, c_void_p]),
+    "hap_ep_exchange_plan": (
+        ctypes.c_int,
+        [c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p],
     ),
     "hap_rope_qk": (
         ctypes.c_int,

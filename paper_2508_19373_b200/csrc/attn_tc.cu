@@ -143,7 +143,7 @@ __device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int32
 constexpr size_t kSchedBytes = 2 * sizeof(int);
 
 #define WAIT(b, p) mbar_wait_spin(b, p)
-template <int D>
+template <int D, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out, int64_t ldo, int S,
@@ -199,6 +199,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tS = [&](int t) { return tmem + 128u * t; };
   auto tO = [&](int t) { return tmem + 256u + (uint32_t)D * t; };
 
+  // registers: the role warpgroup (warps 0-3) runs scalar loops; each softmax
+  // thread holds a 128-key S row plus its packed P (96*128 + 200*256 <= the
+  // 168*384 the launch reserves)
+  if (warp < 4) {
+  setmaxnreg_dec<96>();
   if (warp == 0) {
     // ============ scheduler + Q loads ============
     if (lane == 0) {
@@ -264,8 +269,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ============ MMA issuer ============
+  } else {
+    // ============ MMA issuer (warp 1) ============
     // Per K/V step j: [PV_a,j-1  S_a,j] [PV_b,j-1  S_b,j].  S_t,j overwrites
     // P_t,j-1, so it is issued behind PV_t,j-1 (tcgen05 ops of one thread run
     // in order); the PVs of an item's last step are issued at the next item's
@@ -345,7 +350,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (pend[0].valid) issue_pv(0);
       if (pend[1].valid) issue_pv(1);
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    setmaxnreg_inc<200>();
     // ============ softmax + epilogue, warpgroup t owns Q tile t ============
     const int t = (warp - 4) >> 2;
     const int q = warp & 3;
@@ -390,22 +397,36 @@ __global__ void __launch_bounds__(kThreads, 1)
           l_run *= alpha;
         }
         const float msub = (m_run == -INFINITY) ? 0.f : m_run;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        // x = s*scale - m and the row sums in packed fp32 pairs (FFMA2/FADD2);
+        // with EMU one pair in four takes 2^x on the FMA pipe (exp2_poly2), so
+        // the SFU queue of the two softmax warpgroups sharing an SMSP is 3/4 as
+        // long as the tensor pipe's S+PV work per K/V step
+        const uint64_t sc2 = f2dup(scale_log2), nm2 = f2dup(-msub);
+        uint64_t ls2[2] = {0ull, 0ull};
 #pragma unroll
         for (int h = 0; h < BN / 64; ++h) {
           uint32_t pk[32];
 #pragma unroll
           for (int c2 = 0; c2 < 32; ++c2) {
-            const float x0 = fmaf(__uint_as_float(sv[64 * h + 2 * c2]), scale_log2, -msub);
-            const float x1 = fmaf(__uint_as_float(sv[64 * h + 2 * c2 + 1]), scale_log2, -msub);
-            const float p0 = fast_exp2(x0);
-            const float p1 = fast_exp2(x1);
-            ls[c2 & 3] += p0 + p1;
-            pk[c2] = pack_bf16x2(p0, p1);
+            const uint64_t x01 =
+                ffma2r(f2pack(__uint_as_float(sv[64 * h + 2 * c2]), __uint_as_float(sv[64 * h + 2 * c2 + 1])), sc2, nm2);
+            uint64_t p01;
+            if ((EMU == 1 && (c2 & 3) == 3) || (EMU == 2 && (c2 & 7) == 7)) {
+              p01 = exp2_poly2(x01);
+            } else {
+              const float2 xx = f2split(x01);
+              p01 = f2pack(fast_exp2(xx.x), fast_exp2(xx.y));
+            }
+            fadd2(ls2[c2 & 1], p01);
+            const float2 pp = f2split(p01);
+            pk[c2] = pack_bf16x2(pp.x, pp.y);
           }
           tmem_st_x32(tS(t) + lane_off + 32 * h, pk);
         }
-        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        {
+          const float2 a0 = f2split(ls2[0]), a1 = f2split(ls2[1]);
+          l_run += (a0.x + a0.y) + (a1.x + a1.y);
+        }
         // rescale O in TMEM when the running max moved (PV_t,j-1 must have landed)
         if (__any_sync(0xffffffffu, j > 0 && alpha != 1.f)) {
           WAIT(&o_done[t], (sc - 1) & 1);
@@ -469,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int D>
+template <int D, int EMU>
 static int launch_pair(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* out,
                        int64_t ldo, int64_t n_seqs, int64_t S, int64_t n_q, int64_t n_kv, float scale, int32_t causal,
                        int* sched, cudaStream_t st) {
@@ -479,7 +500,7 @@ static int launch_pair(const void* q, int64_t ldq, const void* k, int64_t ldk, c
       !encode_tmap_2d_bf16(&mk, k, (uint64_t)(n_kv * D), (uint64_t)T, (uint64_t)ldk * 2, 64, BN, true) ||
       !encode_tmap_2d_bf16(&mv, v, (uint64_t)(n_kv * D), (uint64_t)T, (uint64_t)ldv * 2, 64, BN, true))
     return HAP_ERR_DRIVER;
-  auto kern = attn_pair_kernel<D>;
+  auto kern = attn_pair_kernel<D, EMU>;
   static int configured = 0;
   if (!configured) {
     if (configure_smem((const void*)kern, PairSmem<D>::kTotal)) return HAP_ERR_LAUNCH;
@@ -505,9 +526,28 @@ size_t attn_prefill_tc_workspace_bytes() { return attn_tc::kSchedBytes; }
 int attn_prefill_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* out,
                     int64_t ldo, int64_t n_seqs, int64_t S, int64_t n_q, int64_t n_kv, int64_t head_dim, float scale,
                     int32_t causal, int* sched, cudaStream_t st) {
+  static int emu = -1;
+  if (emu < 0) {
+    // A/B switch: 0 = every exponential on the SFU (default, measured fastest:
+    // causal 316-318 us vs 340-343 us with one pair in four on the FMA pipe),
+    // 1 = one exp2 pair in four / 2 = one in eight through exp2_poly2
+    const char* e = getenv("HAP_ATTN_EMU");
+    emu = e ? atoi(e) : 0;
+  }
+#define HAP_ATTN_CASE(DD, EE)                                                                                    \
+  if (head_dim == DD && emu == EE)                                                                               \
+    return attn_tc::launch_pair<DD, EE>(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, S, n_q, n_kv, scale, causal, \
+                                        sched, st);
+  HAP_ATTN_CASE(128, 1)
+  HAP_ATTN_CASE(128, 2)
+  HAP_ATTN_CASE(64, 1)
+  HAP_ATTN_CASE(64, 2)
+#undef HAP_ATTN_CASE
   if (head_dim == 128)
-    return attn_tc::launch_pair<128>(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, S, n_q, n_kv, scale, causal, sched, st);
-  return attn_tc::launch_pair<64>(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, S, n_q, n_kv, scale, causal, sched, st);
+    return attn_tc::launch_pair<128, 0>(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, S, n_q, n_kv, scale, causal, sched,
+                                        st);
+  return attn_tc::launch_pair<64, 0>(q, ldq, k, ldk, v, ldv, out, ldo, n_seqs, S, n_q, n_kv, scale, causal, sched,
+                                     st);
 }
 
 }  // namespace hap

@@ -146,6 +146,44 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x for a pair of fp32 on the FMA pipe (x <= ~16; -inf and anything below
+// -125 give ~2^-125): round-to-nearest split x = j + f with the 1.5*2^23 shift,
+// f in [-0.5, 0.5], degree-3 minimax 2^f (max rel err 1.0e-4, far below the
+// bf16 rounding of P), then j added into the exponent field.  Used for a
+// fraction of the softmax exponentials so they do not all queue on the SFU.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  float2 v = f2split(x);
+  const uint64_t xc = f2pack(fmaxf(v.x, -125.f), fmaxf(v.y, -125.f));
+  const uint64_t t = ffma2r(xc, f2dup(1.f), f2dup(12582912.f));
+  const uint64_t j = ffma2r(f2dup(1.f), f2dup(-12582912.f), t);
+  const uint64_t f = ffma2r(j, f2dup(-1.f), xc);
+  uint64_t p = ffma2r(f, f2dup(0.05500871f), f2dup(0.24221068f));
+  p = ffma2r(p, f, f2dup(0.69328292f));
+  p = ffma2r(p, f, f2dup(1.f));
+  const float2 tp = f2split(t), pp = f2split(p);
+  return f2pack(__uint_as_float(__float_as_uint(pp.x) + (__float_as_uint(tp.x) << 23)),
+                __uint_as_float(__float_as_uint(pp.y) + (__float_as_uint(tp.y) << 23)));
+}
+
+// System-scope flag release / acquire for cross-GPU signalling over peer memory.
+__device__ __forceinline__ void st_release_sys(int32_t* p, int32_t v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <uint32_t R>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R));
+}
+template <uint32_t R>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R));
+}
+
 // sin/cos of a RoPE angle (|x| up to ~1e4 rad): Cody-Waite reduction to
 // [-pi, pi] with a two-term 2*pi, then the SFU sin/cos (max abs error ~2^-21
 // on the reduced range) — ~8 instructions instead of sincosf's ~40, far below

@@ -62,7 +62,8 @@ struct Params {
   int32_t head_dim;
   int32_t rope_cols;
   float theta;
-  int32_t group_m;  // raster group (m-blocks)
+  int32_t group_m;  // raster group (m-blocks; < 0: -group_m n-blocks, n fastest)
+  uint64_t hint_a, hint_b;  // L2 cache policies of the A / B TMA loads
   int32_t st32;     // C rows 32-byte aligned: 32-byte stores in the store epilogue
   // split-K (small-M, weight-streaming shapes): each tile's K range is cut in
   // ksplit slices computed by different CTAs; slice ks writes its fp32
@@ -104,16 +105,26 @@ __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, 
   // grouped raster: group_m m-blocks x all n-blocks, m fastest inside a group.
   // group_m is sized so a group's A rows fit the L2 budget: the weight tile of
   // an n-block is then read once per group while the group's A rows stay hot.
-  const int grp = local / (group_m * n_blocks);
-  const int g0 = grp * group_m;
-  const int gsz = min(group_m, m_blocks - g0);
-  const int r = local - grp * group_m * n_blocks;
   TileCoord c;
   c.g = seg_group[g];
   c.s = g;
-  c.m0 = seg[g] + (g0 + r % gsz) * TM;
   c.m_end = seg[g + 1];
-  c.n_blk = r / gsz;
+  if (group_m > 0) {
+    const int grp = local / (group_m * n_blocks);
+    const int g0 = grp * group_m;
+    const int gsz = min(group_m, m_blocks - g0);
+    const int r = local - grp * group_m * n_blocks;
+    c.m0 = seg[g] + (g0 + r % gsz) * TM;
+    c.n_blk = r / gsz;
+  } else {  // n-grouped raster (tuning experiments): -group_m n-blocks x all m-blocks, n fastest
+    const int group_n = -group_m;
+    const int grp = local / (group_n * m_blocks);
+    const int n0 = grp * group_n;
+    const int gsz = min(group_n, n_blocks - n0);
+    const int r = local - grp * group_n * m_blocks;
+    c.n_blk = n0 + r % gsz;
+    c.m0 = seg[g] + (r / gsz) * TM;
+  }
   return c;
 }
 
@@ -227,10 +238,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < npre; ++i) {
           if (kPair == 1) {
             mbar_arrive_expect_tx(&full_bar[i], tx_bytes);
-            tma_load_2d(smB + i * kBBytes, &tmB, &full_bar[i], (kb0 + i) * BK, b_row, kEvictNormal);
+            tma_load_2d(smB + i * kBBytes, &tmB, &full_bar[i], (kb0 + i) * BK, b_row, p.hint_b);
           } else {
             if (leader) mbar_arrive_expect_tx(&full_bar[i], tx_bytes);
-            tma_load_2d_pair(smB + i * kBBytes, &tmB, &full_bar[i], (kb0 + i) * BK, b_row, kEvictNormal);
+            tma_load_2d_pair(smB + i * kBBytes, &tmB, &full_bar[i], (kb0 + i) * BK, b_row, p.hint_b);
           }
         }
       }
@@ -246,13 +257,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!pre) mbar_wait_spin(&empty_bar[stage], phase ^ 1);
           if (kPair == 1) {
             if (!pre) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
-            tma_load_2d(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, kEvictNormal);
-            if (!pre) tma_load_2d(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
+            tma_load_2d(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, p.hint_a);
+            if (!pre) tma_load_2d(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, p.hint_b);
           } else {
             if (leader && !pre) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
-            tma_load_2d_pair(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, kEvictNormal);
+            tma_load_2d_pair(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, p.hint_a);
             if (!pre)
-              tma_load_2d_pair(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, kEvictNormal);
+              tma_load_2d_pair(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, p.hint_b);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -738,8 +749,24 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
   }();
   p.st32 = (st32_ok && p.seg_dst == nullptr && p.C != nullptr &&
             ((reinterpret_cast<uintptr_t>(p.C) | (uintptr_t)(p.ldc * 2)) & 31) == 0) ? 1 : 0;
-  int64_t gm = l2_budget / (K * 2 * TM);
+  // tuning experiments only: HAP_GEMM_HINT=<A><B> with N(ormal) / F(irst) / L(ast)
+  // L2 eviction priorities, HAP_GEMM_RASTER_N=1 for the n-grouped raster
+  static const uint64_t hints[2] = {[] {
+    const char* e = getenv("HAP_GEMM_HINT");
+    return e && e[0] == 'F' ? kEvictFirst : (e && e[0] == 'L' ? kEvictLast : kEvictNormal);
+  }(), [] {
+    const char* e = getenv("HAP_GEMM_HINT");
+    return e && e[0] && e[1] == 'F' ? kEvictFirst : (e && e[0] && e[1] == 'L' ? kEvictLast : kEvictNormal);
+  }()};
+  static const bool raster_n = [] {
+    const char* e = getenv("HAP_GEMM_RASTER_N");
+    return e && e[0] == '1';
+  }();
+  p.hint_a = hints[0];
+  p.hint_b = hints[1];
+  int64_t gm = l2_budget / (K * 2 * (raster_n ? (int64_t)p.BN : (int64_t)TM));
   p.group_m = (int32_t)(gm < 1 ? 1 : (gm > 1024 ? 1024 : gm));
+  if (raster_n) p.group_m = -p.group_m;
   const int64_t max_tiles = ((a_rows + TM - 1) / TM + (n_segs - 1)) * n_blocks;
   const int64_t max_units = kNumSMs / kPair;
   const int64_t units = max_tiles * p.ksplit;

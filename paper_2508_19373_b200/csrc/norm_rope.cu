@@ -11,11 +11,24 @@ namespace norm {
 
 constexpr int kThreads = 256;
 
+// Store one 16-byte vector to out, or (dst_tab != nullptr) to every base in
+// the device table — the all-gather push of hap_rmsnorm_multi: peer-mapped
+// bases make the normalised rows leave over NVLink as they are produced.
+__device__ __forceinline__ void store_row(uint4* out, const int64_t* __restrict__ dst_tab, int n_dst, int64_t off,
+                                          uint4 v) {
+  if (dst_tab == nullptr) {
+    out[off] = v;
+    return;
+  }
+  for (int d = 0; d < n_dst; ++d) reinterpret_cast<uint4*>(__ldg(dst_tab + d))[off] = v;
+}
+
 // One warp per row; the row is held in registers (h/256 16-byte vectors per lane).
 template <int VPL>  // 16-byte vectors per lane
 __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const uint4* __restrict__ x, int T, int hv, int ldxv,
                                                            const uint4* __restrict__ w, float eps,
-                                                           uint4* __restrict__ out, int ldov) {
+                                                           uint4* __restrict__ out, int ldov,
+                                                           const int64_t* __restrict__ dst_tab, int n_dst) {
   pdl_trigger();
   pdl_wait();
   const int row = (blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -52,7 +65,7 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const uint4* __restri
       const float2 g = unpack_bf16x2(ww[j]);
       o[j] = pack_bf16x2(f.x * inv * g.x, f.y * inv * g.y);
     }
-    out[(int64_t)row * ldov + c] = make_uint4(o[0], o[1], o[2], o[3]);
+    store_row(out, dst_tab, n_dst, (int64_t)row * ldov + c, make_uint4(o[0], o[1], o[2], o[3]));
   }
 }
 
@@ -64,7 +77,8 @@ constexpr int kRowThreads = 128;
 template <int VPT>
 __global__ void __launch_bounds__(kRowThreads) rmsnorm_row_kernel(const uint4* __restrict__ x, int T, int hv, int ldxv,
                                                                   const uint4* __restrict__ w, float eps,
-                                                                  uint4* __restrict__ out, int ldov) {
+                                                                  uint4* __restrict__ out, int ldov,
+                                                                  const int64_t* __restrict__ dst_tab, int n_dst) {
   pdl_trigger();
   pdl_wait();
   __shared__ float red[kRowThreads / 32];
@@ -107,7 +121,7 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_row_kernel(const uint4* _
       const float2 g = unpack_bf16x2(ww[j]);
       o[j] = pack_bf16x2(f.x * inv * g.x, f.y * inv * g.y);
     }
-    out[(int64_t)row * ldov + c] = make_uint4(o[0], o[1], o[2], o[3]);
+    store_row(out, dst_tab, n_dst, (int64_t)row * ldov + c, make_uint4(o[0], o[1], o[2], o[3]));
   }
 }
 
@@ -144,9 +158,9 @@ __global__ void __launch_bounds__(kThreads) rope_kernel(__nv_bfloat16* __restric
 
 using namespace hap::norm;
 
-extern "C" int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, const void* w, float eps, void* out,
-                           int64_t ldo, void* stream) {
-  if (!x || !w || !out || T < 0 || h <= 0 || ldx < h || ldo < h) return HAP_ERR_INVALID_ARG;
+static int rmsnorm_launch(const void* x, int64_t T, int64_t h, int64_t ldx, const void* w, float eps, void* out,
+                          int64_t ldo, const int64_t* dst_tab, int n_dst, void* stream) {
+  if (!x || !w || (!out && !dst_tab) || T < 0 || h <= 0 || ldx < h || ldo < h) return HAP_ERR_INVALID_ARG;
   if (h % 8 || ldx % 8 || ldo % 8) return HAP_ERR_MISALIGNED;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) & 15)
     return HAP_ERR_MISALIGNED;
@@ -163,7 +177,8 @@ extern "C" int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, con
 #define HAP_ROW_CASE(V)                                                                                          \
   if (vpt <= V) {                                                                                               \
     { if (hap::launch_k(rmsnorm_row_kernel<V>, dim3((unsigned)T), dim3(kRowThreads), 0, st, xv, (int)T, hv,    \
-                        (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8)) != cudaSuccess) return HAP_ERR_LAUNCH; } \
+                        (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8), dst_tab, n_dst) != cudaSuccess)           \
+        return HAP_ERR_LAUNCH; }                                                                                \
     HAP_CHECK_LAUNCH();                                                                                         \
     return HAP_OK;                                                                                              \
   }
@@ -174,7 +189,7 @@ extern "C" int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, con
 #undef HAP_ROW_CASE
   }
 #define HAP_NORM_CASE(V) \
-  if (vpl <= V) { { if (hap::launch_k(rmsnorm_kernel<V>, dim3(grid), dim3(kThreads), 0, st, xv, (int)T, hv, (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8)) != cudaSuccess) return HAP_ERR_LAUNCH; } HAP_CHECK_LAUNCH(); return HAP_OK; }
+  if (vpl <= V) { { if (hap::launch_k(rmsnorm_kernel<V>, dim3(grid), dim3(kThreads), 0, st, xv, (int)T, hv, (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8), dst_tab, n_dst) != cudaSuccess) return HAP_ERR_LAUNCH; } HAP_CHECK_LAUNCH(); return HAP_OK; }
   HAP_NORM_CASE(2)
   HAP_NORM_CASE(4)
   HAP_NORM_CASE(8)
@@ -183,6 +198,18 @@ extern "C" int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, con
   HAP_NORM_CASE(32)
 #undef HAP_NORM_CASE
   return HAP_ERR_UNSUPPORTED;
+}
+
+extern "C" int hap_rmsnorm(const void* x, int64_t T, int64_t h, int64_t ldx, const void* w, float eps, void* out,
+                           int64_t ldo, void* stream) {
+  if (!out) return HAP_ERR_INVALID_ARG;
+  return rmsnorm_launch(x, T, h, ldx, w, eps, out, ldo, nullptr, 0, stream);
+}
+
+extern "C" int hap_rmsnorm_multi(const void* x, int64_t T, int64_t h, int64_t ldx, const void* w, float eps,
+                                 const int64_t* dst_tab, int32_t n_dst, int64_t ldo, void* stream) {
+  if (!dst_tab || n_dst < 1 || n_dst > 64) return HAP_ERR_INVALID_ARG;
+  return rmsnorm_launch(x, T, h, ldx, w, eps, nullptr, ldo, dst_tab, n_dst, stream);
 }
 
 extern "C" int hap_rope_qk(void* qkv, int64_t T, int64_t ld, int64_t n_q_heads, int64_t n_kv_heads,

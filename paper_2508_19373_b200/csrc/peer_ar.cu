@@ -27,14 +27,6 @@ namespace peer_ar {
 
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ void st_release_sys(int32_t* p, int32_t v) {
-  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 __global__ void __launch_bounds__(kThreads) allreduce_kernel(const int64_t* __restrict__ in_ptrs,
                                                              const int64_t* __restrict__ out_ptrs,

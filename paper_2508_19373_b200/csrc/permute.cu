@@ -167,12 +167,24 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const int32_t* __rest
 // 256-column item.  Same accumulation order as combine_kernel (slot order,
 // then shared, then residual; fp32; one bf16 rounding): bit-identical.
 constexpr int kCombineU = 4;
+
+// Output row of token t: out + t*hv, or (out_tab != nullptr, the reduce-scatter
+// push of hap_moe_combine_chunked) row (slot*chunk_rows + t % chunk_rows) of
+// the buffer out_tab[t / chunk_rows] — chunk q of the partial sums goes
+// straight into slot `slot` of its owner q's (peer-mapped) receive buffer.
+__device__ __forceinline__ uint4* combine_out_row(uint4* out, const int64_t* __restrict__ out_tab, int chunk_rows,
+                                                  int slot, int t, int hv) {
+  if (out_tab == nullptr) return out + (int64_t)t * hv;
+  return reinterpret_cast<uint4*>(__ldg(out_tab + t / chunk_rows)) +
+         ((int64_t)slot * chunk_rows + t % chunk_rows) * hv;
+}
 __global__ void __launch_bounds__(kThreads) combine_row_kernel(const uint4* __restrict__ y, const int32_t* __restrict__ dst,
                                                                const float* __restrict__ tw, int T, int k, int hv,
                                                                const uint4* __restrict__ resid, int res_row0,
                                                                int res_rows, const uint4* __restrict__ shared_y,
                                                                const float* __restrict__ shared_gate,
-                                                               uint4* __restrict__ out) {
+                                                               uint4* __restrict__ out, const int64_t* __restrict__ out_tab,
+                                                            int chunk_rows, int slot) {
   pdl_trigger();
   pdl_wait();
   const int warp_global = (blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -244,7 +256,7 @@ __global__ void __launch_bounds__(kThreads) combine_row_kernel(const uint4* __re
       for (int u = 0; u < kCombineU; ++u) {
         const int c = c0 + 32 * u;
         if (c < hv)
-          out[(int64_t)t * hv + c] = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
+          combine_out_row(out, out_tab, chunk_rows, slot, t, hv)[c] = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
                                                 pack_bf16x2(acc[u][4], acc[u][5]), pack_bf16x2(acc[u][6], acc[u][7]));
       }
     }
@@ -259,7 +271,8 @@ __global__ void __launch_bounds__(kThreads) combine_kernel(const uint4* __restri
                                                            const uint4* __restrict__ resid, int res_row0,
                                                            int res_rows, const uint4* __restrict__ shared_y,
                                                            const float* __restrict__ shared_gate,
-                                                           uint4* __restrict__ out) {
+                                                           uint4* __restrict__ out, const int64_t* __restrict__ out_tab,
+                                                            int chunk_rows, int slot) {
   pdl_trigger();
   pdl_wait();
   const int warp_global = (blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -310,8 +323,9 @@ __global__ void __launch_bounds__(kThreads) combine_kernel(const uint4* __restri
         acc[2 * i + 1] += f.y;
       }
     }
-    out[(int64_t)t * hv + c] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
-                                          pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+    combine_out_row(out, out_tab, chunk_rows, slot, t, hv)[c] =
+        make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                   pack_bf16x2(acc[6], acc[7]));
   }
 }
 
@@ -398,10 +412,12 @@ extern "C" int hap_moe_permute(const int32_t* expert_of_row, int64_t R, int64_t 
   return HAP_OK;
 }
 
-extern "C" int hap_moe_combine(const void* y, const int32_t* dst_of_row, const float* topk_w, int64_t T, int64_t k,
-                               int64_t h, const void* residual, int64_t res_row0, int64_t res_rows,
-                               const void* shared_y, const float* shared_gate, void* out, void* stream) {
-  if (!y || !dst_of_row || !topk_w || !out || T < 0 || k < 1 || k > 32 || h <= 0) return HAP_ERR_INVALID_ARG;
+static int combine_launch(const void* y, const int32_t* dst_of_row, const float* topk_w, int64_t T, int64_t k,
+                          int64_t h, const void* residual, int64_t res_row0, int64_t res_rows, const void* shared_y,
+                          const float* shared_gate, void* out, const int64_t* out_tab, int64_t chunk_rows,
+                          int64_t slot, void* stream) {
+  if (!y || !dst_of_row || !topk_w || (!out && !out_tab) || T < 0 || k < 1 || k > 32 || h <= 0)
+    return HAP_ERR_INVALID_ARG;
   if (h % 8) return HAP_ERR_MISALIGNED;
   if ((shared_y == nullptr) != (shared_gate == nullptr)) return HAP_ERR_INVALID_ARG;
   if (residual && (res_row0 < 0 || res_rows < 0)) return HAP_ERR_INVALID_ARG;
@@ -416,7 +432,7 @@ extern "C" int hap_moe_combine(const void* y, const int32_t* dst_of_row, const f
     { if (hap::launch_k(combine_row_kernel, dim3(grid_r), dim3(kThreads), 0, st, reinterpret_cast<const uint4*>(y),
                         dst_of_row, topk_w, (int)T, (int)k, (int)(h / 8), reinterpret_cast<const uint4*>(residual),
                         (int)res_row0, (int)res_rows, reinterpret_cast<const uint4*>(shared_y), shared_gate,
-                        reinterpret_cast<uint4*>(out)) != cudaSuccess) return HAP_ERR_LAUNCH; }
+                        reinterpret_cast<uint4*>(out), out_tab, (int)chunk_rows, (int)slot) != cudaSuccess) return HAP_ERR_LAUNCH; }
     HAP_CHECK_LAUNCH();
     return HAP_OK;
   }
@@ -426,9 +442,26 @@ extern "C" int hap_moe_combine(const void* y, const int32_t* dst_of_row, const f
   { if (hap::launch_k(combine_kernel, dim3(grid), dim3(kThreads), 0, st, reinterpret_cast<const uint4*>(y), dst_of_row, topk_w, (int)T, (int)k,
                                             (int)(h / 8), reinterpret_cast<const uint4*>(residual), (int)res_row0,
                                             (int)res_rows, reinterpret_cast<const uint4*>(shared_y), shared_gate,
-                                            reinterpret_cast<uint4*>(out)) != cudaSuccess) return HAP_ERR_LAUNCH; }
+                                            reinterpret_cast<uint4*>(out), out_tab, (int)chunk_rows, (int)slot) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
+}
+
+extern "C" int hap_moe_combine(const void* y, const int32_t* dst_of_row, const float* topk_w, int64_t T, int64_t k,
+                               int64_t h, const void* residual, int64_t res_row0, int64_t res_rows,
+                               const void* shared_y, const float* shared_gate, void* out, void* stream) {
+  if (!out) return HAP_ERR_INVALID_ARG;
+  return combine_launch(y, dst_of_row, topk_w, T, k, h, residual, res_row0, res_rows, shared_y, shared_gate, out,
+                        nullptr, 1, 0, stream);
+}
+
+extern "C" int hap_moe_combine_chunked(const void* y, const int32_t* dst_of_row, const float* topk_w, int64_t T,
+                                       int64_t k, int64_t h, const void* residual, int64_t res_row0,
+                                       int64_t res_rows, const void* shared_y, const float* shared_gate,
+                                       const int64_t* out_tab, int64_t chunk_rows, int64_t slot, void* stream) {
+  if (!out_tab || chunk_rows < 1 || slot < 0 || T % chunk_rows) return HAP_ERR_INVALID_ARG;
+  return combine_launch(y, dst_of_row, topk_w, T, k, h, residual, res_row0, res_rows, shared_y, shared_gate, nullptr,
+                        out_tab, chunk_rows, slot, stream);
 }
 
 extern "C" int hap_peer_copy_rows(const void* src, int64_t rows_max, int64_t h, const int32_t* seg, int64_t n_segs,

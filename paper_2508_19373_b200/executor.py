@@ -48,6 +48,14 @@ def _maybe_peer_allreduce(comm) -> None:
         comm.enable_peer_allreduce(["attn_tp_group", "exp_tp_group"])
 
 
+def _boundary_peer_default() -> bool:
+    """DP<->TP boundary pushed through peer memory (HAP_BOUNDARY_PEER=1) instead of
+    NCCL AllGather + ReduceScatter; opt-in until measured on a multi-GPU box."""
+    import os
+
+    return os.environ.get("HAP_BOUNDARY_PEER", "0") == "1"
+
+
 def _ep_peer_default() -> bool:
     """EP dispatch/combine through peer-mapped buffers (HAP_EP_PEER=1) instead of
     NCCL all-to-alls; opt-in until measured on a multi-GPU box."""
@@ -143,6 +151,7 @@ class HapMoEBlock:
         self.capture = None       # set to {} to keep references to intermediates (tests only)
         self.timers = None        # set to {} to record CUDA events around each kernel phase (bench)
         self.ep_peer = _ep_peer_default()
+        self.boundary_peer = _boundary_peer_default()
 
     @classmethod
     def from_rank_weights(cls, cfg: BlockConfig, deg: PlanDegrees, rank: int, w: RankWeights, *, device=None,
@@ -160,6 +169,7 @@ class HapMoEBlock:
         blk.capture = None
         blk.timers = None
         blk.ep_peer = _ep_peer_default()
+        blk.boundary_peer = _boundary_peer_default()
         return blk
 
     @classmethod
@@ -356,12 +366,22 @@ class HapMoEBlock:
             h1 = h1c
         else:
             self._coll("all_reduce", h1, "attn_tp_group")
-        with self._timed("norm"):
-            hn = ops.rmsnorm(h1, w.ln2, cfg.rms_eps)
+        S_e, a_dp = lay.n_shards, self.deg.a_dp
+        pb = self._peer_boundary(rows) if self._uses_peer_boundary() else None
+        if pb is not None:
+            # boundary all-gather pushed by the norm into every rank's gather buffer
+            with self._timed("norm"):
+                ops.rmsnorm_multi(h1, w.ln2, cfg.rms_eps, pb.ag_tab, h)
+            pb.barrier()
+            hn = hn_s = pb.gath.local[:pb.n * rows]
+        else:
+            with self._timed("norm"):
+                hn = ops.rmsnorm(h1, w.ln2, cfg.rms_eps)
 
         # ---------------- boundary: attention layout -> expert shard
-        S_e, a_dp = lay.n_shards, self.deg.a_dp
-        if rs_attn:
+        if pb is not None:
+            pass
+        elif rs_attn:
             hn_s = hn
         elif S_e < a_dp:
             R = a_dp // S_e
@@ -379,6 +399,12 @@ class HapMoEBlock:
 
         # ---------------- expert module (partial over expert tp)
         residual = h1 if rs_attn else h1[lay.a_tp_rank * c:(lay.a_tp_rank + 1) * c]
+        if pb is not None:
+            # expert-TP reduce-scatter pushed by the combine, summed by the owner in rank order
+            self._experts(hn_s, residual, res_row0=lay.e_tp_rank * c, res_rows=c, push=pb)
+            pb.barrier()
+            out = ops.reduce_slots(pb.slots.local, pb.n, rows, torch.empty(rows, h, device=dev, dtype=BF16))
+            return out[:T_real]
         y = self._experts(hn_s, residual, res_row0=lay.e_tp_rank * c, res_rows=c)
 
         # ---------------- back to the attention layout
@@ -397,6 +423,30 @@ class HapMoEBlock:
             out = chunk
         return out[:T_real]
 
+    def _uses_peer_boundary(self) -> bool:
+        """Peer-memory boundary: pure attention DP, and the expert shard gathers
+        exactly the expert-TP group (gather group == expert-TP group)."""
+        c = self.comm
+        return (self.boundary_peer and c is not None and self.deg.a_tp == 1 and self.deg.e_ep == 1
+                and self.lay.n_shards < self.deg.a_dp and self.deg.e_tp > 1
+                and c.groups["gather_group"][0] == c.groups["exp_tp_group"][0])
+
+    def _peer_boundary(self, rows: int):
+        """Symmetric gather / slot buffers for `rows` rows per replica, (re)allocated
+        collectively (every rank of the group sees the same rows)."""
+        from .peer import PeerBoundary
+
+        pb = getattr(self, "_pb", None)
+        if pb is not None and pb.rows == rows:
+            return pb
+        if pb is not None:
+            torch.cuda.synchronize()
+            self.comm.barrier("exp_tp_group")
+            pb.close()
+        self._pb = PeerBoundary(rows, self.cfg.hidden, self.device, self.comm._g("exp_tp_group"),
+                                self.comm.groups["exp_tp_group"][0])
+        return self._pb
+
     def _peer_allreduce_back(self, y) -> bool:
         c = self.comm
         return (c is not None and self.deg.e_tp > 1 and self.deg.a_tp == self.deg.e_tp
@@ -409,12 +459,17 @@ class HapMoEBlock:
         one-shot peer all-reduce (HAP_PEER_AR=1)."""
         if self.lay.n == 1:
             return True
+        if self._uses_peer_boundary():
+            return True
         c = self.comm
+        if (self.deg.e_ep > 1 and self.ep_peer and self.deg.a_tp == 1 and self.deg.e_tp == 1
+                and self.lay.n_shards == self.deg.a_dp):
+            return True  # attention DP x expert EP: every exchange is a peer store + device barrier
         return (self.deg.e_ep == 1 and self.lay.n_shards == self.deg.a_dp and c is not None
                 and all(c.size(k) == 1 or c.uses_peer_allreduce(k) for k in ("attn_tp_group", "exp_tp_group"))
                 and c.size("gather_group") == 1)
 
-    def _experts(self, hn_s, residual, res_row0, res_rows):
+    def _experts(self, hn_s, residual, res_row0, res_rows, push=None):
         cfg, w, lay, ops = self.cfg, self.w, self.lay, self.ops
         dev = self.device
         T, h = hn_s.shape
@@ -450,6 +505,11 @@ class HapMoEBlock:
         if cfg.n_shared:
             hs = ops.gemm(hn_s, w.ws13, swiglu_half=w.hw_s)
             ys = ops.gemm(hs, w.ws2)
+        if push is not None:  # chunk q of the partial sums straight into slot `me` of rank q
+            with self._timed("combine"):
+                ops.moe_combine_chunked(Y, dst, tw, T, k, h, push.rs_tab, push.rows, push.me, residual=residual,
+                                        shared_y=ys, shared_gate=sg, res_row0=res_row0, res_rows=res_rows)
+            return None
         out = torch.empty(T, h, device=dev, dtype=BF16)
         with self._timed("combine"):
             ops.moe_combine(Y, dst, tw, T, k, out, residual=residual, shared_y=ys, shared_gate=sg,
@@ -491,83 +551,51 @@ class HapMoEBlock:
 
     def close(self) -> None:
         """Release peer mappings (every rank, before a barrier and shutdown)."""
-        for b in getattr(self, "_peer", None) or ():
-            b.close()
-        self._peer = None
+        for name in ("_pb", "_pe"):
+            if getattr(self, name, None) is not None:
+                getattr(self, name).close()
+                setattr(self, name, None)
         for par in getattr(self.comm, "peer_ar", {}).values():
             par.close()
 
     # ------------------------------------------------ EP over peer memory --
-    def _peer_buffers(self, recv_rows: int, y_rows: int):
-        """Symmetric receive / expert-output buffers on the EP group, (re)allocated
-        collectively when a call needs more rows (every rank derives the same
-        sizes from the same count matrix, so the decision is identical)."""
-        from .peer import PeerBuffer
+    def _peer_ep(self, rows: int):
+        """Worst-case-sized symmetric EP buffers for `rows` permuted rows per rank,
+        grown collectively (every rank of the EP group has the same row count)."""
+        from .peer import PeerEP
 
-        bufs = getattr(self, "_peer", None)
-        if bufs is not None and bufs[0].rows >= recv_rows and bufs[1].rows >= y_rows:
-            return bufs
-        grow = lambda need, cur: max(need, int(cur * 1.25)) if cur else need  # noqa: E731
-        rr = grow(recv_rows, bufs[0].rows if bufs else 0)
-        yr = grow(y_rows, bufs[1].rows if bufs else 0)
-        ranks = self.comm.groups["a2a_group"][0]
-        g = self.comm._g("a2a_group")
-        h = self.cfg.hidden
-        self._peer = (PeerBuffer(max(rr, 1), h, BF16, self.device, g, ranks),
-                      PeerBuffer(max(yr, 1), h, BF16, self.device, g, ranks))
-        return self._peer
+        pe = getattr(self, "_pe", None)
+        if pe is not None and pe.rows >= rows:
+            return pe
+        if pe is not None:
+            torch.cuda.synchronize()
+            self.comm.barrier("a2a_group")
+            pe.close()
+        self._pe = PeerEP(rows, self.cfg.hidden, self.w.inter_local, self.cfg.n_experts, self.device,
+                          self.comm._g("a2a_group"), self.comm.groups["a2a_group"][0])
+        return self._pe
 
     def _ep_experts_peer(self, x_perm, seg):
         """EP dispatch -> local grouped GEMMs -> combine with both all-to-alls done
-        as direct stores into peer-mapped buffers: hap_peer_copy_rows writes each
-        rank's rows into the owning rank's receive buffer, and the down GEMM's
-        scatter epilogue writes every expert output back into its source rank's
-        output buffer.  Same row layouts as _ep_experts (received rows in
-        (source rank, local expert) blocks), so the results are identical."""
-        w, ops, comm = self.w, self.ops, self.comm
-        dev = self.device
-        ep, El, h = self.deg.e_ep, w.n_experts_local, self.cfg.hidden
-        E = ep * El
-        me = comm.index("a2a_group")
-        counts = (seg[1:] - seg[:-1]).contiguous()
-        allc = torch.empty(ep * E, device=dev, dtype=torch.int32)
-        comm.all_gather(allc, counts, "a2a_group")
-        C = allc.view(ep, E).cpu().to(torch.int64)          # C[s][e]: rows of source s for global expert e
-        # receive layout at destination d: blocks (s, j) in lexicographic order
-        blk = C.view(ep, ep, El).permute(1, 0, 2)            # [d][s][j]
-        off = torch.zeros(ep, ep * El + 1, dtype=torch.int64)
-        off[:, 1:] = torch.cumsum(blk.reshape(ep, ep * El), 1)
-        n_recv_all = off[:, -1]
-        src_prefix = torch.zeros(ep, E + 1, dtype=torch.int64)
-        src_prefix[:, 1:] = torch.cumsum(C, 1)               # each source's x_perm segment offsets
-        recv_buf, y_buf = self._peer_buffers(int(n_recv_all.max()), int(src_prefix[:, -1].max()))
-        # dispatch: my rows of global expert e go to rank e // El at block (me, e % El)
-        e_ids = torch.arange(E)
-        d_of_e = e_ids // El
-        dst_base = torch.tensor([recv_buf.ptrs[int(d)] for d in d_of_e], dtype=torch.int64)
-        dst_row0 = off[d_of_e, me * El + e_ids % El]
-        ops.peer_copy_rows(x_perm, seg, dst_base.to(dev), dst_row0.to(dev), h)
-        torch.cuda.current_stream().synchronize()
-        comm.barrier("a2a_group")                            # every rank's rows have landed
-        n_recv = int(n_recv_all[me])
-        Y = y_buf.local[:x_perm.shape[0]]
-        if n_recv:
-            seg_r = off[me].to(torch.int32).to(dev)
-            grp = torch.arange(El, dtype=torch.int32).repeat(ep).to(dev)
-            H = torch.empty(n_recv, w.inter_local, device=dev, dtype=BF16)
-            x_recv = recv_buf.local[:n_recv]
-            with self._timed("gate_up"):
-                ops.grouped_gemm(x_recv, w.w13, El, seg_r, H, swiglu_half=w.hw, seg_group=grp)
-            # combine: block (s, j) goes back to source s at its segment of expert me*El + j
-            s_ids = torch.arange(ep).repeat_interleave(El)
-            j_ids = torch.arange(El).repeat(ep)
-            seg_dst = torch.tensor([y_buf.ptrs[int(s)] for s in s_ids], dtype=torch.int64).to(dev)
-            seg_dst_row0 = src_prefix[s_ids, me * El + j_ids].to(torch.int32).to(dev)
-            with self._timed("down"):
-                ops.grouped_gemm_scatter(H, w.w2, El, seg_r, grp, seg_dst, seg_dst_row0, h)
-        torch.cuda.current_stream().synchronize()
-        comm.barrier("a2a_group")                            # every expert output is back at its source
-        return Y
+        as direct stores into peer-mapped buffers and the exchange planned on the
+        device (peer.PeerEP): no count reaches the host.  Received rows sit in
+        (source rank, local expert) blocks exactly as in _ep_experts, so the
+        GEMMs see the same rows and the results are identical."""
+        w, ops = self.w, self.ops
+        R, h = x_perm.shape
+        pe = self._peer_ep(R)
+        E, El = self.cfg.n_experts, pe.El
+        ops.peer_broadcast_i32(seg, pe.segs_tab, pe.me * (E + 1) * 4)
+        pe.barrier()                                          # every rank's segment offsets have landed
+        ops.ep_exchange_plan(pe.segs.local, pe.n, El, pe.me, pe.dst_row0, pe.seg_r, pe.seg_dst_row0)
+        ops.peer_copy_rows(x_perm, seg, pe.dst_base, pe.dst_row0, h)
+        pe.barrier()                                          # every rank's rows have landed
+        with self._timed("gate_up"):
+            ops.grouped_gemm(pe.recv.local, w.w13, El, pe.seg_r, pe.H, swiglu_half=w.hw, seg_group=pe.grp)
+        with self._timed("down"):
+            ops.grouped_gemm_scatter(pe.H, w.w2, El, pe.seg_r, pe.grp, pe.seg_dst, pe.seg_dst_row0, h)
+        pe.barrier()                                          # every expert output is back at its source
+        return pe.y.local[:R]
 
 
 def forward(block: HapMoEBlock, hidden: torch.Tensor, stage: str, batch: int, seq_len: int = 1,

@@ -293,6 +293,78 @@ def moe_combine(y: torch.Tensor, dst_of_row: torch.Tensor, topk_w: torch.Tensor,
     _count(1 if T else 0)
 
 
+def moe_combine_chunked(y: torch.Tensor, dst_of_row: torch.Tensor, topk_w: torch.Tensor, T: int, k: int, h: int,
+                        dst_tab: torch.Tensor, chunk_rows: int, slot: int, residual: Optional[torch.Tensor] = None,
+                        shared_y: Optional[torch.Tensor] = None, shared_gate: Optional[torch.Tensor] = None,
+                        res_row0: int = 0, res_rows: Optional[int] = None) -> None:
+    """moe_combine whose chunk q of rows is stored into slot `slot` of the buffer
+    dst_tab[q] (device int64 table of peer-mapped bases): the pushed reduce-scatter."""
+    lib = _lib.load()
+    _need(y, "y", BF16); _need(dst_tab, "dst_tab", torch.int64)
+    for t, n in ((y, "y"), (residual, "residual"), (shared_y, "shared_y")):
+        if t is not None and not t.is_contiguous():
+            raise ValueError(f"{n} must be contiguous")
+    if residual is not None and res_rows is None:
+        res_rows = residual.shape[0]
+    st = lib.hap_moe_combine_chunked(y.data_ptr(), dst_of_row.data_ptr(), topk_w.data_ptr(), T, k, h,
+                                     _ptr(residual), int(res_row0), int(res_rows or 0), _ptr(shared_y),
+                                     _ptr(shared_gate), dst_tab.data_ptr(), int(chunk_rows), int(slot), _stream())
+    check(st, "hap_moe_combine_chunked")
+    _count(1 if T else 0)
+
+
+def rmsnorm_multi(x: torch.Tensor, w: torch.Tensor, eps: float, dst_tab: torch.Tensor, ldo: int) -> None:
+    """RMSNorm storing every row to each base of dst_tab (the pushed all-gather)."""
+    lib = _lib.load()
+    _need(x, "x", BF16); _need(w, "w", BF16); _need(dst_tab, "dst_tab", torch.int64)
+    _rowmajor(x, "x")
+    st = lib.hap_rmsnorm_multi(x.data_ptr(), x.shape[0], x.shape[1], x.stride(0), w.data_ptr(), float(eps),
+                               dst_tab.data_ptr(), dst_tab.numel(), int(ldo), _stream())
+    check(st, "hap_rmsnorm_multi")
+    _count(1 if x.shape[0] else 0)
+
+
+def peer_barrier(sig_tab: torch.Tensor, epoch: torch.Tensor, n_ranks: int, rank: int) -> None:
+    """Device-side barrier of a peer group (no host synchronisation)."""
+    lib = _lib.load()
+    _need(sig_tab, "sig_tab", torch.int64); _need(epoch, "epoch", torch.int32)
+    check(lib.hap_peer_barrier(sig_tab.data_ptr(), epoch.data_ptr(), n_ranks, rank, _stream()), "hap_peer_barrier")
+    _count(1)
+
+
+def reduce_slots(slots: torch.Tensor, n_slots: int, rows: int, out: torch.Tensor) -> torch.Tensor:
+    """out = sum over n_slots row blocks of slots (slot order, fp32, one bf16 rounding)."""
+    lib = _lib.load()
+    _need(slots, "slots", BF16); _need(out, "out", BF16)
+    if not (slots.is_contiguous() and out.is_contiguous()):
+        raise ValueError("slots and out must be contiguous")
+    h = out.shape[1]
+    check(lib.hap_reduce_slots_bf16(slots.data_ptr(), n_slots, rows, h, out.data_ptr(), _stream()),
+          "hap_reduce_slots_bf16")
+    _count(1 if rows else 0)
+    return out
+
+
+def peer_broadcast_i32(src: torch.Tensor, dst_tab: torch.Tensor, dst_offset_bytes: int) -> None:
+    """Push src (int32) to dst_tab[p] + dst_offset_bytes for every base p."""
+    lib = _lib.load()
+    _need(src, "src", torch.int32); _need(dst_tab, "dst_tab", torch.int64)
+    check(lib.hap_peer_broadcast_i32(src.data_ptr(), src.numel(), dst_tab.data_ptr(), dst_tab.numel(),
+                                     int(dst_offset_bytes), _stream()), "hap_peer_broadcast_i32")
+    _count(1 if src.numel() else 0)
+
+
+def ep_exchange_plan(segs: torch.Tensor, ep: int, experts_local: int, me: int, dst_row0: torch.Tensor,
+                     seg_r: torch.Tensor, seg_dst_row0: torch.Tensor) -> None:
+    """Device-side EP dispatch / combine offsets from the gathered segment offsets."""
+    lib = _lib.load()
+    _need(segs, "segs", torch.int32); _need(dst_row0, "dst_row0", torch.int64)
+    _need(seg_r, "seg_r", torch.int32); _need(seg_dst_row0, "seg_dst_row0", torch.int32)
+    check(lib.hap_ep_exchange_plan(segs.data_ptr(), ep, experts_local, me, dst_row0.data_ptr(), seg_r.data_ptr(),
+                                   seg_dst_row0.data_ptr(), _stream()), "hap_ep_exchange_plan")
+    _count(1)
+
+
 def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     lib = _lib.load()
     _need(x, "x", BF16); _need(w, "w", BF16)

@@ -94,3 +94,101 @@ class PeerAllReduce:
     def close(self) -> None:
         self.data.close()
         self.sig.close()
+
+
+class PeerBoundary:
+    """The DP<->TP boundary of one expert-TP group over peer memory
+    (HAP_BOUNDARY_PEER=1): for plans whose gather group is the expert-TP group
+    and attention is pure DP (e.g. the reference's roofline pick
+    attn(dp=N) + exp(tp=N)).
+
+    * all-gather: the RMSNorm that produces a replica's normalised rows stores
+      them into that replica's row block of every rank's ``gath`` buffer
+      (hap_rmsnorm_multi), then a device barrier;
+    * reduce-scatter: the combine stores chunk q of its partial sums into slot
+      ``me`` of rank q's ``slots`` buffer (hap_moe_combine_chunked), a device
+      barrier, then each owner sums its slots in rank order
+      (hap_reduce_slots_bf16).
+
+    Both exchanges are stores issued by the kernels that produce the data (the
+    NVLink transfer overlaps the norm / combine), and nothing synchronises the
+    host, so a decode step under such a plan is CUDA-graph capturable.  One
+    flag row per group serves every barrier (epochs only grow); single buffers
+    are safe because each exchange is separated from the next write into the
+    same buffer by the other exchange's barrier."""
+
+    def __init__(self, rows: int, h: int, device, group, group_ranks: List[int]):
+        self.rows, self.h = rows, h
+        self.n = len(group_ranks)
+        self.me = group_ranks.index(dist.get_rank())
+        self.gath = PeerBuffer(self.n * rows, h, torch.bfloat16, device, group, group_ranks)
+        self.slots = PeerBuffer(self.n * rows, h, torch.bfloat16, device, group, group_ranks)
+        self.sig = PeerBuffer(1, self.n, torch.int32, device, group, group_ranks)
+        self.sig.local.zero_()
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # every flag row is zero before anyone publishes
+        dev = self.epoch.device
+        row_bytes = h * 2
+        self.ag_tab = torch.tensor([p + self.me * rows * row_bytes for p in self.gath.ptrs], dtype=torch.int64,
+                                   device=dev)
+        self.rs_tab = torch.tensor(self.slots.ptrs, dtype=torch.int64, device=dev)
+        self.sig_tab = torch.tensor(self.sig.ptrs, dtype=torch.int64, device=dev)
+
+    def barrier(self) -> None:
+        from . import ops
+
+        ops.peer_barrier(self.sig_tab, self.epoch, self.n, self.me)
+
+    def close(self) -> None:
+        for b in (self.gath, self.slots, self.sig):
+            b.close()
+
+
+class PeerEP:
+    """EP dispatch / combine over peer memory with the exchange planned on the
+    device (HAP_EP_PEER=1): every rank pushes its permute segment offsets into
+    every rank's ``segs`` table (hap_peer_broadcast_i32), a device barrier, then
+    hap_ep_exchange_plan derives the receive offsets, the dispatch destinations
+    and the combine targets on the device; hap_peer_copy_rows stores the rows
+    into the owners' ``recv`` buffers, and the down GEMM's scatter epilogue
+    stores the expert outputs back into the sources' ``y`` buffers.  Buffers are
+    sized for the worst case (every row of every source routed here), so no
+    count ever reaches the host: three device barriers per call and no host
+    synchronisation (graph capturable)."""
+
+    def __init__(self, rows: int, h: int, inter_local: int, n_experts: int, device, group,
+                 group_ranks: List[int]):
+        self.n = len(group_ranks)
+        self.me = group_ranks.index(dist.get_rank())
+        self.rows, self.E = rows, n_experts
+        self.El = n_experts // self.n
+        cap = self.n * rows
+        self.segs = PeerBuffer(self.n, n_experts + 1, torch.int32, device, group, group_ranks)
+        self.recv = PeerBuffer(cap, h, torch.bfloat16, device, group, group_ranks)
+        self.y = PeerBuffer(rows, h, torch.bfloat16, device, group, group_ranks)
+        self.sig = PeerBuffer(1, self.n, torch.int32, device, group, group_ranks)
+        self.sig.local.zero_()
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
+        self.H = torch.empty(cap, inter_local, dtype=torch.bfloat16, device=device)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # flags zero everywhere before anyone publishes
+        dev = self.epoch.device
+        i64 = dict(dtype=torch.int64, device=dev)
+        self.segs_tab = torch.tensor(self.segs.ptrs, **i64)
+        self.sig_tab = torch.tensor(self.sig.ptrs, **i64)
+        self.dst_base = torch.tensor([self.recv.ptrs[e // self.El] for e in range(n_experts)], **i64)
+        self.seg_dst = torch.tensor([self.y.ptrs[s] for s in range(self.n) for _ in range(self.El)], **i64)
+        self.grp = torch.arange(self.El, dtype=torch.int32, device=dev).repeat(self.n)
+        self.dst_row0 = torch.zeros(n_experts, **i64)
+        self.seg_r = torch.zeros(n_experts + 1, dtype=torch.int32, device=dev)
+        self.seg_dst_row0 = torch.zeros(n_experts, dtype=torch.int32, device=dev)
+
+    def barrier(self) -> None:
+        from . import ops
+
+        ops.peer_barrier(self.sig_tab, self.epoch, self.n, self.me)
+
+    def close(self) -> None:
+        for b in (self.segs, self.recv, self.y, self.sig):
+            b.close()

@@ -1,5 +1,5 @@
 """Time hap_attn_prefill on the Mixtral-8x7B prefill shape, causal and non-causal (dev script).
-HAP_ATTN_POLY=<n> selects how many of every 8 exp2 pairs run on the FMA pipe."""
+HAP_ATTN_EMU=0|1 selects all exponentials on the SFU | one pair in four on the FMA pipe."""
 import os
 import sys
 from pathlib import Path
@@ -22,4 +22,4 @@ for causal in (True, False):
     ms = s.elapsed_time(e) / 20
     fl = 4 * B * S * S * nq * d / (2 if causal else 1)  # causal: useful half
     res.append(f"{'causal' if causal else 'full'} {ms*1e3:.1f} us {fl/ms/1e9:.0f} TF/s")
-print(f"poly={os.environ.get('HAP_ATTN_POLY', 'default')}: " + "; ".join(res))
+print(f"emu={os.environ.get("HAP_ATTN_EMU", "default")}: " + "; ".join(res))

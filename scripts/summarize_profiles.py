@@ -72,18 +72,47 @@ def main(tag: str) -> None:
                 summ[name] = {"total_us": round(sum(t for _, t in s), 1), "kernels": s}
         (prof / f"{tag}_summary.json").write_text(json.dumps(summ, indent=1))
     rep = OUT / "full_block.ncu-rep"
+    raw_csv = OUT / "full_block_raw.csv"  # written on the GPU box when the .ncu-rep is too big to bring back
+    raw = None
     if rep.exists():
         raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-        rows = list(csv.reader(io.StringIO(raw)))
+    elif raw_csv.exists():
+        raw = raw_csv.read_text()
+    if raw:
+        rows = list(csv.reader(io.StringIO(raw[raw.find('"ID"'):])))
         hdr, units, data = rows[0], rows[1], rows[2:]
         out = []
+        gemm_phase = iter(["qkv", "o_proj", "gate_up", "down"])  # grouped_gemm launches of one prefill forward
         for r in data:
             d = dict(zip(hdr, r))
             u = dict(zip(hdr, units))
-            out.append({k: (d.get(k, "") + (" " + u[k] if u.get(k) else "")).strip() for k in FULL_KEYS if k in d})
+            e = {k: (d.get(k, "") + (" " + u[k] if u.get(k) else "")).strip() for k in FULL_KEYS if k in d}
+            if "grouped_gemm_kernel" in d.get("Kernel Name", ""):
+                e["phase"] = next(gemm_phase, "?")
+            out.append(e)
         (prof / f"{tag}_ncu_full.json").write_text(json.dumps(
             {"source": "ncu --set full --clock-control none --import-source on, scripts/profile_block.py 1 0 "
                        "(Mixtral-8x7B prefill 8x2048, one block forward)", "launches": out}, indent=1))
+        # DRAM traffic of the expert GEMMs against their algorithmic bytes (bench.py reads this file)
+        T, h, I, E, k = 8 * 2048, 4096, 14336, 8, 2
+        algo = {"gate_up": T * k * h * 2 + E * 2 * I * h * 2 + T * k * I * 2,
+                "down": T * k * I * 2 + E * h * I * 2 + T * k * h * 2}
+        tr = {"source": f"profiles/{tag}_ncu_full.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
+              "kernel": "hap::gemm::grouped_gemm_kernel (Mixtral-8x7B, 32768 routed rows)"}
+        for e in out:
+            ph = e.get("phase")
+            if ph in algo:
+                def num(key):
+                    v, _, unit = e[key].partition(" ")
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+                    return float(v.replace(",", "")) * scale
+                dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+                tr[ph] = {"dram_bytes_per_launch": dram, "algorithmic_bytes": algo[ph],
+                          "traffic_over_algorithmic": dram / algo[ph]}
+        if "gate_up" in tr:
+            tr["dram_bytes_per_launch"] = tr["gate_up"]["dram_bytes_per_launch"]
+            tr["algorithmic_bytes"] = tr["gate_up"]["algorithmic_bytes"]
+            (prof / f"{tag}_gemm_traffic.json").write_text(json.dumps(tr, indent=1))
 
 
 if __name__ == "__main__":
