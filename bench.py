@@ -228,8 +228,8 @@ def bench_decode(block, cfg, steps, warmup):
     if block.graph_capturable():
         g, _ = block.capture_graph(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos)
         return time_loop(g.replay, steps, warmup), "cuda_graph"
-    return time_loop(lambda: block.forward(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos), steps,
-                     warmup), "eager"
+    return time_loop(lambda: block.forward(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos,
+                                           max_position=DECODE_KV - 1), steps, warmup), "eager"
 
 
 def decode_bytes(cfg, block_routing_idx) -> float:

@@ -36,6 +36,7 @@ from .layout import PlanDegrees, RankLayout, replica_sequences, tokens_per_repli
 from .weights import RankWeights, pack_rank_weights, synthetic_weights
 
 BF16 = torch.bfloat16
+_SHARED_SIDE_STREAM_MAX_T = 512  # decode-size batches: shared expert on a side stream
 
 
 def _maybe_peer_allreduce(comm) -> None:
@@ -89,6 +90,11 @@ class CudaOps:
     moe_combine = staticmethod(K.moe_combine)
     grouped_gemm_scatter = staticmethod(K.grouped_gemm_scatter)
     peer_copy_rows = staticmethod(K.peer_copy_rows)
+    rmsnorm_multi = staticmethod(K.rmsnorm_multi)
+    moe_combine_chunked = staticmethod(K.moe_combine_chunked)
+    reduce_slots = staticmethod(K.reduce_slots)
+    peer_broadcast_i32 = staticmethod(K.peer_broadcast_i32)
+    ep_exchange_plan = staticmethod(K.ep_exchange_plan)
     permute_workspace_bytes = staticmethod(K.permute_workspace_bytes)
     attn_decode_workspace_bytes = staticmethod(K.attn_decode_workspace_bytes)
 
@@ -115,17 +121,18 @@ class KVCache:
     def max_len(self) -> int:
         return int(self.k.shape[2])
 
-    def check_positions(self, positions: torch.Tensor) -> None:
+    def check_positions(self, positions: torch.Tensor) -> int:
         """Raise ValueError unless every decode position is inside the cache
         (0 <= pos < max_len).  Reads device positions back (one sync), so the
         graph-captured decode path validates on the host side instead
         (HapModel.capture_decode callers own their position counter); the
         kernels themselves never write or read outside a sequence's rows."""
         if positions.numel() == 0:
-            return
+            return 0
         lo, hi = int(positions.min()), int(positions.max())
         if lo < 0 or hi >= self.max_len:
             raise ValueError(f"decode positions [{lo}, {hi}] outside the KV cache (max_len {self.max_len})")
+        return hi
 
 
 class HapMoEBlock:
@@ -212,17 +219,24 @@ class HapMoEBlock:
 
     # ------------------------------------------------------------ forward --
     def forward(self, x_local: torch.Tensor, stage: str, batch: int, seq_len: int = 1,
-                kv_cache: Optional[KVCache] = None, positions: Optional[torch.Tensor] = None) -> torch.Tensor:
+                kv_cache: Optional[KVCache] = None, positions: Optional[torch.Tensor] = None,
+                max_position: Optional[int] = None) -> torch.Tensor:
         """x_local: this attention replica's tokens [n_seqs_local * seq_len, h]
         (prefill) or [n_seqs_local, h] (decode); returns the block output in
         the same layout.  positions (decode): int32 [n_seqs_local] current
-        lengths (the new token's position)."""
+        lengths (the new token's position).  Positions are validated against
+        the cache on the host: from ``max_position`` (the caller's own bound,
+        no device read-back) when given, else from a host ``positions``
+        tensor, else by reading the device tensor back (one sync; skipped
+        under graph capture — the kernels never touch rows outside a
+        sequence's cache either way)."""
         if stage == "prefill":
             return self._forward(x_local, batch, seq_len, decode=False, kv_cache=kv_cache)
         if stage == "decode":
             if kv_cache is None or positions is None:
                 raise ValueError("decode needs a kv_cache and positions")
-            return self._forward(x_local, batch, 1, decode=True, kv_cache=kv_cache, positions=positions)
+            return self._forward(x_local, batch, 1, decode=True, kv_cache=kv_cache, positions=positions,
+                                 max_position=max_position)
         raise ValueError(f"unknown stage {stage!r}")
 
     def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor, batch: int, seq_len: int,
@@ -308,7 +322,7 @@ class HapMoEBlock:
             out = self.forward(x_static, stage, batch, seq_len, kv_cache=kv_cache, positions=positions)
         return g, out
 
-    def _forward(self, x_local, batch, S, decode, kv_cache=None, positions=None):
+    def _forward(self, x_local, batch, S, decode, kv_cache=None, positions=None, max_position=None):
         cfg, w, lay, ops = self.cfg, self.w, self.lay, self.ops
         dev = self.device
         h, d = cfg.hidden, cfg.head_dim
@@ -327,8 +341,14 @@ class HapMoEBlock:
             xn = ops.rmsnorm(x, w.ln1, cfg.rms_eps)
         nq, nkv = w.n_q_local, w.n_kv_local
         if decode:
-            if not positions.is_cuda or not torch.cuda.is_current_stream_capturing():
+            if max_position is not None:  # the caller's host-side length: no device read-back
+                if n_seq and not 0 <= max_position < kv_cache.max_len:
+                    raise ValueError(f"decode position {max_position} outside the KV cache "
+                                     f"(max_len {kv_cache.max_len})")
+            elif not positions.is_cuda or not torch.cuda.is_current_stream_capturing():
                 kv_cache.check_positions(positions[:n_seq])
+            if not positions.is_cuda:
+                positions = positions.to(dev, non_blocking=True)
             if rows == n_seq and positions.dtype == torch.int32 and positions.is_contiguous():
                 pos = positions
             else:
@@ -423,6 +443,12 @@ class HapMoEBlock:
             out = chunk
         return out[:T_real]
 
+    def _side_stream(self):
+        st = getattr(self, "_side", None)
+        if st is None or st.device != self.device:
+            st = self._side = torch.cuda.Stream(device=self.device)
+        return st
+
     def _uses_peer_boundary(self) -> bool:
         """Peer-memory boundary: pure attention DP, and the expert shard gathers
         exactly the expert-TP group (gather group == expert-TP group)."""
@@ -474,6 +500,19 @@ class HapMoEBlock:
         dev = self.device
         T, h = hn_s.shape
         E, k = cfg.n_experts, cfg.top_k
+        # shared expert (Qwen): independent of the routed path; on small (decode)
+        # batches its weight-streaming GEMMs run on a side stream, concurrently
+        # with router -> permute -> grouped GEMMs, so neither path's launch ramp
+        # and tail idle the HBM (fork/join by events: CUDA-graph capturable)
+        ys, side = None, None
+        if cfg.n_shared:
+            if hn_s.is_cuda and T <= _SHARED_SIDE_STREAM_MAX_T:
+                side = self._side_stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    ys = ops.gemm(ops.gemm(hn_s, w.ws13, swiglu_half=w.hw_s), w.ws2)
+            else:
+                ys = ops.gemm(ops.gemm(hn_s, w.ws13, swiglu_half=w.hw_s), w.ws2)
         idx = torch.empty(T, k, device=dev, dtype=torch.int32)
         tw = torch.empty(T, k, device=dev, dtype=torch.float32)
         sg = torch.empty(T, device=dev, dtype=torch.float32) if cfg.n_shared else None
@@ -501,10 +540,10 @@ class HapMoEBlock:
             Y = self._ep_experts_peer(x_perm, seg)
         else:
             Y = self._ep_experts(x_perm, seg)
-        ys = None
-        if cfg.n_shared:
-            hs = ops.gemm(hn_s, w.ws13, swiglu_half=w.hw_s)
-            ys = ops.gemm(hs, w.ws2)
+        if side is not None:  # join the shared expert's stream before the combine reads ys
+            main = torch.cuda.current_stream()
+            main.wait_stream(side)
+            ys.record_stream(main)
         if push is not None:  # chunk q of the partial sums straight into slot `me` of rank q
             with self._timed("combine"):
                 ops.moe_combine_chunked(Y, dst, tw, T, k, h, push.rs_tab, push.rows, push.me, residual=residual,

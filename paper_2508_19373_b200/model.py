@@ -106,10 +106,15 @@ class HapModel:
         return h
 
     def decode_step(self, x_local: torch.Tensor, batch: int, caches: List[KVCache],
-                    positions: torch.Tensor) -> torch.Tensor:
+                    positions: torch.Tensor, max_position: Optional[int] = None) -> torch.Tensor:
+        """One decode step through every layer.  ``max_position`` (the caller's
+        host-side bound on ``positions``) is checked against the caches once,
+        without reading the device tensor back."""
         h = x_local
+        if max_position is None and positions.is_cuda and not torch.cuda.is_current_stream_capturing() and caches:
+            max_position = caches[0].check_positions(positions)  # one read-back for the whole step
         for blk, cache in zip(self.blocks, caches):
-            h = blk.forward(h, "decode", batch, kv_cache=cache, positions=positions)
+            h = blk.forward(h, "decode", batch, kv_cache=cache, positions=positions, max_position=max_position)
         return h
 
     def capture_decode(self, x_static: torch.Tensor, batch: int, caches: List[KVCache], positions: torch.Tensor):

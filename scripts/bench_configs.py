@@ -30,8 +30,11 @@ mpl = import_moeplan()
 
 
 def peaks():
-    p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"])
+    """MEASURED_PEAKS.json when the driver wrote one on this box, else bench.py's stated fallback."""
+    from bench import load_peaks
+
+    p = load_peaks()
+    return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"]
 
 
 def timed(fn, steps, warmup):

@@ -21,6 +21,6 @@ cache = KVCache.empty(64, cfg.n_kv_heads, 2048, cfg.head_dim, "cuda", random=Tru
 pos = torch.full((64,), 2047, device="cuda", dtype=torch.int32)
 xd = torch.randn(64, cfg.hidden, device="cuda").to(torch.bfloat16)
 for _ in range(n_d):
-    blk.forward(xd, "decode", 64, kv_cache=cache, positions=pos)
+    blk.forward(xd, "decode", 64, kv_cache=cache, positions=pos, max_position=2047)
 torch.cuda.synchronize()
 print("done")
