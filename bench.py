@@ -225,11 +225,47 @@ def bench_decode(block, cfg, steps, warmup):
     loop keeps the contract's K)."""
     x, cache, pos = make_decode_state(block, cfg)
     steps, warmup = max(steps, DECODE_MIN_STEPS), max(warmup, 20)
-    if block.graph_capturable():
+    if block.graph_capturable(DECODE_BATCH):
         g, _ = block.capture_graph(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos)
         return time_loop(g.replay, steps, warmup), "cuda_graph"
     return time_loop(lambda: block.forward(x, "decode", DECODE_BATCH, kv_cache=cache, positions=pos,
                                            max_position=DECODE_KV - 1), steps, warmup), "eager"
+
+
+def bench_peer_variant(cfg, hap_p, hap_d, rank, weights, x_global, steps, warmup):
+    """N > 1: the HAP plan again with every exchange that has a peer-memory form
+    switched to it (EP dispatch/combine planned on the device, the DP<->TP
+    boundary pushed by the norm / combine, one-shot decode all-reduces).  These
+    paths are opt-in in the executor until timed on an NVLink box; this is that
+    timing.  Barrier waits trap after ~20 s rather than hang, so a failure here
+    is reported in the line instead of stalling the run."""
+    from paper_2508_19373_b200.executor import HapMoEBlock
+
+    out = {}
+    blocks = []
+    try:
+        for stage, sp in (("prefill", hap_p), ("decode", hap_d)):
+            blk = HapMoEBlock(cfg, sp.degrees, None, rank=rank, weights=weights)
+            blocks.append(blk)
+            blk.ep_peer = blk.boundary_peer = True
+            if blk.comm is not None:
+                blk.comm.enable_peer_allreduce(["attn_tp_group", "exp_tp_group"])
+            if stage == "prefill":
+                ms = bench_prefill(blk, cfg, steps, warmup, x_global)
+                out.update({"plan": sp.label(), "prefill_ms": ms,
+                            "prefill_tokens_per_s": PREFILL_BATCH * PREFILL_SEQ / (ms / 1e3)})
+            else:
+                ms, mode = bench_decode(blk, cfg, steps, warmup)
+                out.update({"decode_plan": sp.label(), "decode_ms": ms, "decode_mode": mode,
+                            "decode_tokens_per_s": DECODE_BATCH / (ms / 1e3)})
+    except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+        out["error"] = f"{type(exc).__name__}: {str(exc)[:300]}"
+    for b in blocks:
+        try:
+            b.close()
+        except Exception:  # noqa: BLE001
+            pass
+    return out
 
 
 def decode_bytes(cfg, block_routing_idx) -> float:
@@ -370,6 +406,7 @@ def main():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-tp", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-peer", action="store_true", help="N>1: skip the peer-memory exchange variant of the HAP plan")
     ap.add_argument("--cpu-sample-tokens", type=int, default=256)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -572,6 +609,11 @@ def main():
     e2e = {"value": T / (e2e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": h2d, "api": api}
 
+    # N > 1, last (its failure must not cost the other numbers): the HAP plan over peer memory
+    peer = None
+    if world > 1 and not args.no_peer:
+        peer = bench_peer_variant(cfg, hap_p, hap_d, rank, weights, x_global, args.steps, args.warmup)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg, args.cpu_sample_tokens)
@@ -590,7 +632,8 @@ def main():
                        "planner": f"moeplan solve_ilp (reference ILP) on {plan_src}",
                        "planner_ms": plan_ms,
                        "l2": "no flush: every step streams > L2 (2.8 GB expert weights + 128 MB activations)"},
-            "plans": results, "decode": decode, "roofline": roofline, "roofline_block": roofline_block,
+            "plans": results, "hap_peer_exchanges": peer, "decode": decode, "roofline": roofline,
+            "roofline_block": roofline_block,
             "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": TIMED_LAUNCHES.get(f"prefill:{hap_p.degrees.label()}"),
             "gpu_launches_note": "kernels of libhap_kernels.so launched in the headline timed region (this rank)",

@@ -486,7 +486,10 @@ extern "C" int hap_attn_prefill(const void* q, int64_t ldq, const void* k, int64
 
 // Key-split size for the warp-pipelined decode: items = B * n_kv * ceil(len/split)
 // spread round-robin over 148 x kDecWarps warp workers; minimise
-// rounds x (chunks per item + ~1 chunk of per-item overhead).
+// rounds x (chunks per item + ~1 chunk of per-item overhead), with at most 32
+// splits per (sequence, head) so the merge is the one-split-per-lane kernel
+// (small batches otherwise cut the keys into 16-key splits whose merge reads
+// more partials than the cache holds: Qwen2-57B B=1, 128 splits, merge 12 us).
 static void plan_decode(int64_t B, int64_t n_kv, int64_t max_len, int* split, int* ns) {
   const int64_t workers = (int64_t)kNumSMs * kDecWarps;
   const int64_t cps = (max_len + kDecChunk - 1) / kDecChunk;
@@ -494,6 +497,7 @@ static void plan_decode(int64_t B, int64_t n_kv, int64_t max_len, int* split, in
   for (int64_t sc = 1; sc <= cps; ++sc) {
     const int64_t n = (cps + sc - 1) / sc;
     if (sc > 1 && (cps + sc - 2) / (sc - 1) == n) continue;  // same split count as a smaller sc
+    if (n > 32) continue;
     const int64_t rounds = (B * n_kv * n + workers - 1) / workers;
     const int64_t cost = rounds * (sc + 1);
     if (cost < best_cost) {

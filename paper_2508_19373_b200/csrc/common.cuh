@@ -175,6 +175,22 @@ __device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until *flag >= e (system-scope acquire).  A peer that never arrives
+// (crashed rank, broken mapping) must not hang the GPU: after ~20 s the
+// kernel traps, which surfaces as a CUDA error on every rank's next sync.
+__device__ __forceinline__ void wait_flag_sys(const int32_t* flag, int32_t e) {
+  if (ld_acquire_sys(flag) >= e) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_sys(flag) < e)
+    if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+}
+
 template <uint32_t R>
 __device__ __forceinline__ void setmaxnreg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R));

@@ -57,9 +57,7 @@ __global__ void __launch_bounds__(kThreads) allreduce_kernel(const int64_t* __re
     for (int p = 0; p < n_ranks; ++p)
       st_release_sys(reinterpret_cast<int32_t*>(sig_ptrs[p]) + (int64_t)c * n_ranks + r, e);
     const int32_t* my_sig = reinterpret_cast<const int32_t*>(sig_ptrs[r]) + (int64_t)c * n_ranks;
-    for (int p = 0; p < n_ranks; ++p)
-      while (ld_acquire_sys(my_sig + p) < e) {
-      }
+    for (int p = 0; p < n_ranks; ++p) wait_flag_sys(my_sig + p, e);
   }
   __syncthreads();
   uint4* out = reinterpret_cast<uint4*>(out_ptrs[r]);

@@ -32,9 +32,7 @@ __global__ void barrier_kernel(const int64_t* __restrict__ sig_tab, int32_t* __r
   __threadfence_system();  // this rank's earlier stores (previous kernels) before the flag
   for (int p = 0; p < n_ranks; ++p) st_release_sys(reinterpret_cast<int32_t*>(sig_tab[p]) + rank, e);
   const int32_t* mine = reinterpret_cast<const int32_t*>(sig_tab[rank]);
-  for (int p = 0; p < n_ranks; ++p)
-    while (ld_acquire_sys(mine + p) < e) {
-    }
+  for (int p = 0; p < n_ranks; ++p) wait_flag_sys(mine + p, e);
   epoch[0] = e;
 }
 

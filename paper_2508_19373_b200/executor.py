@@ -309,8 +309,9 @@ class HapMoEBlock:
         (graph, out_static).  Replaying the graph re-runs every kernel of the
         block with no host work (decode is launch-bound otherwise).  Only for
         plans without host synchronisation (no EP count exchange) on one GPU."""
-        if not self.graph_capturable():
-            raise RuntimeError("graph capture needs one device, or a non-EP plan on peer all-reduces (HAP_PEER_AR=1)")
+        if not self.graph_capturable(batch, seq_len):
+            raise RuntimeError("graph capture needs one device, a peer-memory boundary / EP plan, or a non-EP plan "
+                               "whose all-reduces fit the one-shot peer all-reduce (HAP_PEER_AR=1)")
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
@@ -479,10 +480,12 @@ class HapMoEBlock:
                 and c.groups["exp_tp_group"][0] == c.groups["attn_tp_group"][0]
                 and c.uses_peer_allreduce("attn_tp_group") and c.peer_ar["attn_tp_group"].fits(y))
 
-    def graph_capturable(self) -> bool:
+    def graph_capturable(self, batch: Optional[int] = None, seq_len: int = 1) -> bool:
         """True when a forward issues no host synchronisation and no NCCL call:
-        one device, or a non-EP plan whose collectives all run through the
-        one-shot peer all-reduce (HAP_PEER_AR=1)."""
+        one device; the DP<->TP boundary or attention-DP x EP over peer memory;
+        or a non-EP plan whose collectives all run through the one-shot peer
+        all-reduce (HAP_PEER_AR=1) — which needs the call's tensors to fit the
+        all-reduce buffer, so that case is only claimed for a known ``batch``."""
         if self.lay.n == 1:
             return True
         if self._uses_peer_boundary():
@@ -491,9 +494,19 @@ class HapMoEBlock:
         if (self.deg.e_ep > 1 and self.ep_peer and self.deg.a_tp == 1 and self.deg.e_tp == 1
                 and self.lay.n_shards == self.deg.a_dp):
             return True  # attention DP x expert EP: every exchange is a peer store + device barrier
-        return (self.deg.e_ep == 1 and self.lay.n_shards == self.deg.a_dp and c is not None
-                and all(c.size(k) == 1 or c.uses_peer_allreduce(k) for k in ("attn_tp_group", "exp_tp_group"))
-                and c.size("gather_group") == 1)
+        if not (self.deg.e_ep == 1 and self.lay.n_shards == self.deg.a_dp and c is not None
+                and c.size("gather_group") == 1):
+            return False
+        if batch is None:
+            return False
+        _, rows, _ = self._attn_rows(batch, seq_len)
+        n_elems = rows * self.cfg.hidden
+        for k in ("attn_tp_group", "exp_tp_group"):
+            if c.size(k) > 1 and not (c.uses_peer_allreduce(k) and c.peer_ar[k].n_max >= n_elems):
+                return False
+        # the expert side must close with the one-shot all-reduce, not RS + AG over NCCL
+        return self.deg.e_tp == 1 or (self.deg.a_tp == self.deg.e_tp
+                                      and c.groups["exp_tp_group"][0] == c.groups["attn_tp_group"][0])
 
     def _experts(self, hn_s, residual, res_row0, res_rows, push=None):
         cfg, w, lay, ops = self.cfg, self.w, self.lay, self.ops

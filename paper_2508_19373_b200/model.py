@@ -86,6 +86,10 @@ class HapModel:
             e.record()
             torch.cuda.synchronize()
             seconds = s.elapsed_time(e) / 1e3
+        if cuda:
+            torch.cuda.synchronize()
+        for blk in self.blocks:  # release the old layout's peer mappings / symmetric buffers
+            blk.close()
         self.blocks, self.deg, self.lay = new_blocks, new_deg, new_blocks[0].lay
         return seconds
 

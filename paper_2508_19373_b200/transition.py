@@ -110,14 +110,35 @@ def reshard_expert_weights(cfg, w, lay_src, lay_dst, group=None):
     all-to-all that carries exactly the (unit, slice) pieces each rank is
     missing (the per-device volume the reference charges in reshard_volume,
     transition.py:153-177).  Attention weights are unchanged (a plan has one
-    attention strategy).  Returns a new RankWeights packed for lay_dst."""
-    import dataclasses
-    from math import gcd
+    attention strategy).  Returns a new RankWeights packed for lay_dst.
 
+    Three phases (timed separately by scripts/measure_reshard.py): pack the
+    pieces other ranks need (reshard_pack), one all_to_all_single, and
+    re-pack the destination layout from local + received pieces
+    (reshard_unpack)."""
     import torch.distributed as dist
 
+    send, in_splits, out_splits, ctx = reshard_pack(cfg, w, lay_src, lay_dst)
+    recv = torch.empty(sum(out_splits), dtype=send.dtype, device=send.device)
+    if lay_src.n > 1:
+        if recv.is_cuda and dist.get_backend(group) == "gloo":
+            # single-GPU validation (ranks sharing one device): gloo stages through host memory
+            rh = torch.empty(recv.shape, dtype=recv.dtype)
+            dist.all_to_all_single(rh, send.cpu(), output_split_sizes=out_splits, input_split_sizes=in_splits,
+                                   group=group)
+            recv.copy_(rh)
+        else:
+            dist.all_to_all_single(recv, send, output_split_sizes=out_splits, input_split_sizes=in_splits,
+                                   group=group)
+    return reshard_unpack(ctx, recv)
+
+
+def reshard_pack(cfg, w, lay_src, lay_dst):
+    """Phase 1 of the reshard: the send buffer (pieces this rank ships, grouped by
+    destination) and the all-to-all splits; ctx carries what reshard_unpack needs."""
+    from math import gcd
+
     from .layout import RankLayout
-    from .weights import interleave_gate_up, swiglu_half_width
 
     n = lay_src.n
     tp_i, tp_j = lay_src.deg.e_tp, lay_dst.deg.e_tp
@@ -147,9 +168,21 @@ def reshard_expert_weights(cfg, w, lay_src, lay_dst, group=None):
     out_splits = [len(sends[q][me]) * piece_elems for q in range(n)]
     dev, dt = w.w13.device, w.w13.dtype
     send = torch.cat([c.reshape(-1) for c in send_chunks]) if send_chunks else torch.empty(0, dtype=dt, device=dev)
-    recv = torch.empty(sum(out_splits), dtype=dt, device=dev)
-    if n > 1:
-        dist.all_to_all_single(recv, send, output_split_sizes=out_splits, input_split_sizes=in_splits, group=group)
+    ctx = dict(cfg=cfg, w=w, lay_dst=lay_dst, n=n, me=me, per=per, h=h, own_src=own_src, sends=sends,
+               local_piece=local_piece, piece_elems=piece_elems)
+    return send, in_splits, out_splits, ctx
+
+
+def reshard_unpack(ctx, recv):
+    """Phase 3 of the reshard: the destination layout's RankWeights from this
+    rank's own pieces plus the received buffer."""
+    import dataclasses
+
+    from .weights import interleave_gate_up, swiglu_half_width
+
+    cfg, w, n, me, per = ctx["cfg"], ctx["w"], ctx["n"], ctx["me"], ctx["per"]
+    own_src, sends, local_piece, piece_elems, h = (ctx["own_src"], ctx["sends"], ctx["local_piece"],
+                                                  ctx["piece_elems"], ctx["h"])
     received = {}
     off = 0
     for q in range(n):
@@ -160,7 +193,7 @@ def reshard_expert_weights(cfg, w, lay_src, lay_dst, group=None):
     def piece(key):
         return local_piece(*key) if key in own_src[me] else received[key]
 
-    d = lay_dst
+    d = ctx["lay_dst"]
     de0, de1 = d.experts
     ds0, ds1 = d.inter_slice[0] // per, d.inter_slice[1] // per
     il = (ds1 - ds0) * per

@@ -47,7 +47,7 @@ def main(rank, world, port, out_path):
         torch.cuda.synchronize()
         res[peer] = out.float().cpu()
         if peer == "1":
-            assert blk.graph_capturable()
+            assert blk.graph_capturable(B)
             xs = x.clone()
             graph, gout = blk.capture_graph(xs, "decode", B, kv_cache=cache, positions=pos)
             for _ in range(3):
