@@ -335,6 +335,25 @@ int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, void* v_cache
                     float scale, void* out, int64_t ldo, void* workspace, size_t ws_bytes, void* stream);
 
 /*
+ * Paged KV cache: k_pool / v_pool hold n_pages pages [n_kv, page_size, d]
+ * (page_size a multiple of 16); int32 block_table[b * max_pages + j] is the
+ * page of sequence b's keys [j*page_size, (j+1)*page_size) (< 0: none; the
+ * caller allocates the pages covering [0, pos[b]] before the call).  Same
+ * arithmetic as the contiguous entry points with max_len = max_pages *
+ * page_size (identical split plan, bit-identical outputs); workspace:
+ * hap_attn_decode_workspace_bytes(B, n_q, d, max_pages * page_size).
+ * Replaces: the KV bytes the reference grows per decode step
+ * (arch.py:193-201, simulate.py:78-114) with a non-contiguous cache.
+ */
+int hap_kv_cache_fill_paged(const void* qkv, int64_t ldqkv, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
+                            int64_t n_kv_heads, int64_t head_dim, void* k_pool, void* v_pool,
+                            const int32_t* block_table, int64_t max_pages, int64_t page_size, void* stream);
+int hap_attn_decode_paged(const void* qkv, int64_t ldqkv, void* k_pool, void* v_pool, int64_t n_pages,
+                          int64_t page_size, const int32_t* block_table, int64_t max_pages, const int32_t* pos,
+                          int64_t B, int64_t n_q_heads, int64_t n_kv_heads, int64_t head_dim, float scale, void* out,
+                          int64_t ldo, void* workspace, size_t ws_bytes, void* stream);
+
+/*
  * INT4 per-group dequantization of a GQI4 tensor (reference quant.py:19-22,
  * 61-116): codes packed low-nibble-first (4-byte aligned), float64 scale and
  * zero point per group of group_size elements, n original elements.

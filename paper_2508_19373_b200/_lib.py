@@ -131,6 +131,16 @@ SIGNATURES = {
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int32, c_void_p],
     ),
     "hap_attn_decode_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int64]),
+    "hap_kv_cache_fill_paged": (
+        ctypes.c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
+         c_int64, c_void_p],
+    ),
+    "hap_attn_decode_paged": (
+        ctypes.c_int,
+        [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
+         c_int64, c_int64, c_float, c_void_p, c_int64, c_void_p, c_size_t, c_void_p],
+    ),
     "hap_attn_decode": (
         ctypes.c_int,
         [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64,

@@ -24,20 +24,36 @@ namespace attn {
 // ------------------------------------------------------------------ decode --
 constexpr int kMaxG = 8;
 
+// Cache row of key position k of (sequence b, kv head h).  Contiguous cache
+// [B, n_kv, max_len, D]: (b*n_kv + h)*max_len + k.  Paged cache (block_table
+// != nullptr): a pool of pages [n_pages, n_kv, page, D] and int32
+// block_table[b][k / page] = page id (< 0: not allocated, returns -1); a
+// 16-key decode chunk never crosses a page (page is a multiple of 16).
+struct KvLayout {
+  const int32_t* block_table;
+  int max_pages, page;
+};
+__device__ __forceinline__ int64_t kv_row(const KvLayout& L, int b, int h, int n_kv, int max_len, int k) {
+  if (L.block_table == nullptr) return ((int64_t)b * n_kv + h) * max_len + k;
+  const int pg = L.block_table[(int64_t)b * L.max_pages + k / L.page];
+  return pg < 0 ? -1 : ((int64_t)pg * n_kv + h) * L.page + k % L.page;
+}
+
 // Copy the new token's k and v (from the fused qkv row, after RoPE) into the cache.
 template <int D>
 __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, int n_q, int n_kv,
                                  __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int max_len,
-                                 const int32_t* __restrict__ pos) {
+                                 const int32_t* __restrict__ pos, KvLayout L) {
   pdl_trigger();
   pdl_wait();
   const int b = blockIdx.x;
   const int p = pos[b];
   if (p < 0 || p >= max_len) return;  // outside the cache: nothing is written
+  if (kv_row(L, b, 0, n_kv, max_len, p) < 0) return;  // page not allocated
   const __nv_bfloat16* row = qkv + (int64_t)b * ld;
   for (int i = threadIdx.x; i < n_kv * D / 8; i += blockDim.x) {
     const int hh = i / (D / 8), c = (i % (D / 8)) * 8;
-    const int64_t dst = (((int64_t)b * n_kv + hh) * max_len + p) * D + c;
+    const int64_t dst = kv_row(L, b, hh, n_kv, max_len, p) * D + c;
     *reinterpret_cast<uint4*>(kc + dst) = *reinterpret_cast<const uint4*>(row + (int64_t)(n_q + hh) * D + c);
     *reinterpret_cast<uint4*>(vc + dst) = *reinterpret_cast<const uint4*>(row + (int64_t)(n_q + n_kv + hh) * D + c);
   }
@@ -99,7 +115,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
     decode_mma_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                       const __nv_bfloat16* __restrict__ qkv, int64_t ld, int max_len, const int32_t* __restrict__ pos,
                       int B, int n_q, int n_kv, float scale_log2, float* __restrict__ ws_o,
-                      float* __restrict__ ws_ml, int ns, int split) {
+                      float* __restrict__ ws_ml, int ns, int split, KvLayout L) {
   pdl_trigger();
   pdl_wait();
   constexpr int H = D / 64;                        // 128-byte column halves of a row
@@ -134,7 +150,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
   auto issue = [&](int stage) {
     if (l_item >= n_items) return;
     if (lane == 0) {
-      const int row = (li.b * n_kv + li.kvh) * max_len + li.k0 + l_c * kDecChunk;
+      const int row = (int)kv_row(L, li.b, li.kvh, n_kv, max_len, li.k0 + l_c * kDecChunk);
       uint8_t* dst = ring + stage * kStageBytes;
       mbar_arrive_expect_tx(&full[stage], kStageBytes);
 #pragma unroll
@@ -422,14 +438,16 @@ namespace attn {
 // the head-major cache rows [0, seq_len) of its sequence.
 template <int D>
 __global__ void kv_fill_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, int n_q, int n_kv, int S,
-                               __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int max_len) {
+                               __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int max_len,
+                               KvLayout L) {
   pdl_trigger();
   pdl_wait();
   const int i = blockIdx.x, b = blockIdx.y;
+  if (kv_row(L, b, 0, n_kv, max_len, i) < 0) return;  // page not allocated
   const __nv_bfloat16* row = qkv + ((int64_t)b * S + i) * ld;
   for (int v = threadIdx.x; v < n_kv * D / 8; v += blockDim.x) {
     const int hh = v / (D / 8), c = (v % (D / 8)) * 8;
-    const int64_t dst = (((int64_t)b * n_kv + hh) * max_len + i) * D + c;
+    const int64_t dst = kv_row(L, b, hh, n_kv, max_len, i) * D + c;
     *reinterpret_cast<uint4*>(kc + dst) = *reinterpret_cast<const uint4*>(row + (int64_t)(n_q + hh) * D + c);
     *reinterpret_cast<uint4*>(vc + dst) = *reinterpret_cast<const uint4*>(row + (int64_t)(n_q + n_kv + hh) * D + c);
   }
@@ -440,9 +458,9 @@ __global__ void kv_fill_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld
 using namespace hap;
 using namespace hap::attn;
 
-extern "C" int hap_kv_cache_fill(const void* qkv, int64_t ldqkv, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
-                                 int64_t n_kv_heads, int64_t head_dim, void* k_cache, void* v_cache, int64_t max_len,
-                                 void* stream) {
+static int kv_cache_fill(const void* qkv, int64_t ldqkv, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
+                         int64_t n_kv_heads, int64_t head_dim, void* k_cache, void* v_cache, int64_t max_len,
+                         KvLayout L, void* stream) {
   if (!qkv || !k_cache || !v_cache || n_seqs < 0 || seq_len < 0 || n_q_heads < 1 || n_kv_heads < 1)
     return HAP_ERR_INVALID_ARG;
   if (seq_len > max_len) return HAP_ERR_INVALID_ARG;
@@ -457,11 +475,31 @@ extern "C" int hap_kv_cache_fill(const void* qkv, int64_t ldqkv, int64_t n_seqs,
   auto* kc = reinterpret_cast<__nv_bfloat16*>(k_cache);
   auto* vc = reinterpret_cast<__nv_bfloat16*>(v_cache);
   if (head_dim == 128)
-    { if (hap::launch_k(kv_fill_kernel<128>, dim3(grid), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len) != cudaSuccess) return HAP_ERR_LAUNCH; }
+    { if (hap::launch_k(kv_fill_kernel<128>, dim3(grid), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len, L) != cudaSuccess) return HAP_ERR_LAUNCH; }
   else
-    { if (hap::launch_k(kv_fill_kernel<64>, dim3(grid), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len) != cudaSuccess) return HAP_ERR_LAUNCH; }
+    { if (hap::launch_k(kv_fill_kernel<64>, dim3(grid), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, (int)seq_len, kc, vc, (int)max_len, L) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
+}
+
+extern "C" int hap_kv_cache_fill(const void* qkv, int64_t ldqkv, int64_t n_seqs, int64_t seq_len, int64_t n_q_heads,
+                                 int64_t n_kv_heads, int64_t head_dim, void* k_cache, void* v_cache, int64_t max_len,
+                                 void* stream) {
+  return kv_cache_fill(qkv, ldqkv, n_seqs, seq_len, n_q_heads, n_kv_heads, head_dim, k_cache, v_cache, max_len,
+                       KvLayout{nullptr, 0, 0}, stream);
+}
+
+static bool paged_ok(const int32_t* block_table, int64_t max_pages, int64_t page_size) {
+  return block_table && max_pages >= 1 && page_size >= kDecChunk && page_size % kDecChunk == 0;
+}
+
+extern "C" int hap_kv_cache_fill_paged(const void* qkv, int64_t ldqkv, int64_t n_seqs, int64_t seq_len,
+                                       int64_t n_q_heads, int64_t n_kv_heads, int64_t head_dim, void* k_pool,
+                                       void* v_pool, const int32_t* block_table, int64_t max_pages,
+                                       int64_t page_size, void* stream) {
+  if (!paged_ok(block_table, max_pages, page_size)) return HAP_ERR_INVALID_ARG;
+  return kv_cache_fill(qkv, ldqkv, n_seqs, seq_len, n_q_heads, n_kv_heads, head_dim, k_pool, v_pool,
+                       max_pages * page_size, KvLayout{block_table, (int)max_pages, (int)page_size}, stream);
 }
 
 extern "C" size_t hap_attn_prefill_workspace_bytes(void) { return hap::attn_prefill_tc_workspace_bytes(); }
@@ -526,14 +564,14 @@ extern "C" size_t hap_attn_decode_workspace_bytes(int64_t B, int64_t n_q_heads, 
 template <int D>
 static int launch_decode(const __nv_bfloat16* q, int64_t ldqkv, __nv_bfloat16* kc, __nv_bfloat16* vc, int64_t max_len,
                          const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads, float scale,
-                         float* ws_o, float* ws_ml, int* ns_out, cudaStream_t st) {
+                         float* ws_o, float* ws_ml, int* ns_out, KvLayout L, uint64_t cache_rows, cudaStream_t st) {
   const int G = (int)(n_q_heads / n_kv_heads);
-  { if (hap::launch_k(kv_append_kernel<D>, dim3((unsigned)B), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, kc, vc, (int)max_len, pos) != cudaSuccess) return HAP_ERR_LAUNCH; }
+  { if (hap::launch_k(kv_append_kernel<D>, dim3((unsigned)B), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, kc, vc, (int)max_len, pos, L) != cudaSuccess) return HAP_ERR_LAUNCH; }
   const float sl2 = scale * 1.4426950408889634f;
   int split, ns;
   plan_decode(B, n_kv_heads, max_len, &split, &ns);
   *ns_out = ns;  // <= the count hap_attn_decode_workspace_bytes provisions for
-  const uint64_t rows = (uint64_t)(B * n_kv_heads * max_len);
+  const uint64_t rows = cache_rows;
   CUtensorMap tmK, tmV;
   if (!encode_tmap_2d_bf16(&tmK, kc, D, rows, D * 2, 64, kDecChunk, true) ||
       !encode_tmap_2d_bf16(&tmV, vc, D, rows, D * 2, 64, kDecChunk, true))
@@ -551,7 +589,7 @@ static int launch_decode(const __nv_bfloat16* q, int64_t ldqkv, __nv_bfloat16* k
     }                                                                                                             \
     { if (hap::launch_k(decode_mma_kernel<D, GG>, dim3(grid), dim3(kDecWarps * 32), smem, st, tmK, tmV, q, ldqkv, (int)max_len, pos, (int)B,   \
                                                                  (int)n_q_heads, (int)n_kv_heads, sl2, ws_o,      \
-                                                                 ws_ml, ns, split) != cudaSuccess) return HAP_ERR_LAUNCH; }                               \
+                                                                 ws_ml, ns, split, L) != cudaSuccess) return HAP_ERR_LAUNCH; }                            \
     break;                                                                                                        \
   }
   switch (G) {
@@ -570,10 +608,10 @@ static int launch_decode(const __nv_bfloat16* q, int64_t ldqkv, __nv_bfloat16* k
   return HAP_OK;
 }
 
-extern "C" int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, void* v_cache, int64_t max_len,
-                               const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads,
-                               int64_t head_dim, float scale, void* out, int64_t ldo, void* workspace,
-                               size_t ws_bytes, void* stream) {
+static int attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, void* v_cache, int64_t max_len,
+                       const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads, int64_t head_dim,
+                       float scale, void* out, int64_t ldo, void* workspace, size_t ws_bytes, KvLayout L,
+                       uint64_t cache_rows, void* stream) {
   if (!qkv || !k_cache || !v_cache || !pos || !out || B < 0 || max_len < 1 || n_q_heads < 1 || n_kv_heads < 1)
     return HAP_ERR_INVALID_ARG;
   if (n_q_heads % n_kv_heads) return HAP_ERR_INVALID_ARG;
@@ -595,8 +633,8 @@ extern "C" int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, vo
   const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(qkv);
   __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(k_cache);
   __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(v_cache);
-  const int rc = head_dim == 128 ? launch_decode<128>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st)
-                                 : launch_decode<64>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, st);
+  const int rc = head_dim == 128 ? launch_decode<128>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, L, cache_rows, st)
+                                 : launch_decode<64>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, L, cache_rows, st);
   if (rc != HAP_OK) return rc;
   if (ns > 32) {
     if (hap::launch_k(decode_merge_wide_kernel, dim3((unsigned)(B * n_q_heads)), dim3(kWideMergeWarps * 32), 0, st,
@@ -611,4 +649,23 @@ extern "C" int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, vo
   }
   HAP_CHECK_LAUNCH();
   return HAP_OK;
+}
+
+extern "C" int hap_attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, void* v_cache, int64_t max_len,
+                               const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads,
+                               int64_t head_dim, float scale, void* out, int64_t ldo, void* workspace,
+                               size_t ws_bytes, void* stream) {
+  return attn_decode(qkv, ldqkv, k_cache, v_cache, max_len, pos, B, n_q_heads, n_kv_heads, head_dim, scale, out, ldo,
+                     workspace, ws_bytes, KvLayout{nullptr, 0, 0}, (uint64_t)(B * n_kv_heads * max_len), stream);
+}
+
+extern "C" int hap_attn_decode_paged(const void* qkv, int64_t ldqkv, void* k_pool, void* v_pool, int64_t n_pages,
+                                     int64_t page_size, const int32_t* block_table, int64_t max_pages,
+                                     const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads,
+                                     int64_t head_dim, float scale, void* out, int64_t ldo, void* workspace,
+                                     size_t ws_bytes, void* stream) {
+  if (!paged_ok(block_table, max_pages, page_size) || n_pages < 1) return HAP_ERR_INVALID_ARG;
+  return attn_decode(qkv, ldqkv, k_pool, v_pool, max_pages * page_size, pos, B, n_q_heads, n_kv_heads, head_dim,
+                     scale, out, ldo, workspace, ws_bytes, KvLayout{block_table, (int)max_pages, (int)page_size},
+                     (uint64_t)(n_pages * n_kv_heads * page_size), stream);
 }

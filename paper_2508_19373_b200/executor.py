@@ -85,6 +85,8 @@ class CudaOps:
     attn_prefill = staticmethod(K.attn_prefill)
     attn_decode = staticmethod(K.attn_decode)
     kv_cache_fill = staticmethod(K.kv_cache_fill)
+    kv_cache_fill_paged = staticmethod(K.kv_cache_fill_paged)
+    attn_decode_paged = staticmethod(K.attn_decode_paged)
     router_topk = staticmethod(K.router_topk)
     moe_permute = staticmethod(K.moe_permute)
     moe_combine = staticmethod(K.moe_combine)
@@ -133,6 +135,78 @@ class KVCache:
         if lo < 0 or hi >= self.max_len:
             raise ValueError(f"decode positions [{lo}, {hi}] outside the KV cache (max_len {self.max_len})")
         return hi
+
+
+class PagedKV:
+    """Paged KV cache for a stack of layers (the full-model loop, SURVEY §8(f)
+    row 3): per layer a pool of pages [n_pages, Hkv_l, page, d] for k and for v,
+    and ONE int32 block table [B, max_pages] shared by every layer (a sequence's
+    j-th page has the same id in every layer's pool).  Pages are handed out on
+    the host as sequences grow (``ensure``) and returned by ``release``; the
+    device table is refreshed by one small copy only when it changed, so a
+    captured decode graph stays valid while the table rows it reads are updated
+    in place."""
+
+    def __init__(self, n_layers: int, batch: int, n_kv_local: int, head_dim: int, max_len: int, device,
+                 page: int = 64, n_pages: Optional[int] = None):
+        if page % 16:
+            raise ValueError("page size must be a multiple of 16 (the decode kernel's key chunk)")
+        self.page, self.batch = page, batch
+        self.max_pages = -(-max_len // page)
+        self.n_pages = n_pages if n_pages is not None else batch * self.max_pages
+        shape = (self.n_pages, n_kv_local, page, head_dim)
+        self.k = [torch.zeros(shape, device=device, dtype=BF16) for _ in range(n_layers)]
+        self.v = [torch.zeros(shape, device=device, dtype=BF16) for _ in range(n_layers)]
+        self.table_host = torch.full((batch, self.max_pages), -1, dtype=torch.int32)
+        self.table = self.table_host.to(device)
+        self.free = list(range(self.n_pages - 1, -1, -1))
+        self.held = [0] * batch  # pages held per sequence
+
+    @property
+    def max_len(self) -> int:
+        return self.max_pages * self.page
+
+    def ensure(self, length: int, seqs=None) -> None:
+        """Pages for keys [0, length) of every sequence in `seqs` (default: all)."""
+        need = -(-length // self.page)
+        if need > self.max_pages:
+            raise ValueError(f"length {length} exceeds the paged cache (max_len {self.max_len})")
+        changed = False
+        for b in (range(self.batch) if seqs is None else seqs):
+            while self.held[b] < need:
+                if not self.free:
+                    raise RuntimeError("paged KV cache out of pages")
+                self.table_host[b, self.held[b]] = self.free.pop()
+                self.held[b] += 1
+                changed = True
+        if changed:
+            self.table.copy_(self.table_host, non_blocking=False)
+
+    def release(self, b: int) -> None:
+        """Return sequence b's pages to the pool (its rows become unallocated)."""
+        self.free.extend(int(x) for x in self.table_host[b, :self.held[b]].tolist())
+        self.table_host[b] = -1
+        self.held[b] = 0
+        self.table.copy_(self.table_host)
+
+    def layer(self, i: int) -> "PagedKVCache":
+        return PagedKVCache(self.k[i], self.v[i], self)
+
+
+@dataclass
+class PagedKVCache:
+    """One layer's view of a PagedKV (what HapMoEBlock.forward takes as kv_cache)."""
+
+    k: torch.Tensor
+    v: torch.Tensor
+    state: PagedKV
+
+    @property
+    def max_len(self) -> int:
+        return self.state.max_len
+
+    def check_positions(self, positions: torch.Tensor) -> int:
+        return KVCache.check_positions(self, positions)
 
 
 class HapMoEBlock:
@@ -362,14 +436,21 @@ class HapMoEBlock:
             qkv = ops.gemm_qkv_rope(xn, w.wqkv, pos, nq + nkv, d, cfg.rope_theta, bias=w.bqkv)
         attn = torch.zeros(rows, nq * d, device=dev, dtype=BF16) if rows != T_real else \
             torch.empty(rows, nq * d, device=dev, dtype=BF16)
+        paged = isinstance(kv_cache, PagedKVCache)
         if decode:
-            ws = torch.empty(ops.attn_decode_workspace_bytes(max(n_seq, 1), nq, d, kv_cache.k.shape[2]),
+            ws = torch.empty(ops.attn_decode_workspace_bytes(max(n_seq, 1), nq, d, kv_cache.max_len),
                              device=dev, dtype=torch.uint8)
-            if n_seq:
+            if n_seq and paged:
+                ops.attn_decode_paged(qkv[:n_seq], kv_cache.k, kv_cache.v, kv_cache.state.table[:n_seq],
+                                      pos[:n_seq], nq, nkv, d, attn[:n_seq], ws)
+            elif n_seq:
                 ops.attn_decode(qkv[:n_seq], kv_cache.k[:n_seq], kv_cache.v[:n_seq], pos[:n_seq], nq, nkv, d,
                                 attn[:n_seq], ws)
         elif n_seq:
-            if kv_cache is not None:  # keep this prefill's k/v for the decode steps that follow
+            if paged:  # keep this prefill's k/v in the sequences' pages
+                ops.kv_cache_fill_paged(qkv, nq, nkv, d, n_seq, S, kv_cache.k, kv_cache.v,
+                                        kv_cache.state.table[:n_seq])
+            elif kv_cache is not None:  # keep this prefill's k/v for the decode steps that follow
                 ops.kv_cache_fill(qkv, nq, nkv, d, n_seq, S, kv_cache.k, kv_cache.v)
             with self._timed("attn"):
                 ops.attn_prefill(qkv, nq, nkv, d, n_seq, S, attn)

@@ -20,7 +20,7 @@ from typing import List, Optional
 import torch
 
 from .config import BlockConfig
-from .executor import HapMoEBlock, KVCache
+from .executor import HapMoEBlock, KVCache, PagedKV, PagedKVCache
 from .layout import PlanDegrees, replica_sequences
 from .weights import synthetic_weights
 
@@ -97,14 +97,25 @@ class HapModel:
         exp = getattr(self, "_expert_decode", None)
         return 0.0 if exp is None else self.switch_expert_layout(exp)
 
-    def new_caches(self, batch: int, max_len: int) -> List[KVCache]:
+    def new_caches(self, batch: int, max_len: int, paged: bool = False, page: int = 64,
+                   n_pages: Optional[int] = None) -> List[KVCache]:
+        """Per-layer KV caches for this rank's sequences: contiguous
+        [B_l, Hkv_l, max_len, d], or (paged) views of one PagedKV whose pages
+        are allocated as the sequences grow (prefill / decode_step call
+        ``ensure``)."""
         s0, s1 = replica_sequences(batch, self.deg.a_dp, self.lay.a_rep)
         nkv = self.blocks[0].w.n_kv_local
+        if paged:
+            state = PagedKV(self.n_layers, max(s1 - s0, 1), nkv, self.cfg.head_dim, max_len, self.device, page=page,
+                            n_pages=n_pages)
+            return [state.layer(i) for i in range(self.n_layers)]
         return [KVCache.empty(max(s1 - s0, 1), nkv, max_len, self.cfg.head_dim, self.device)
                 for _ in range(self.n_layers)]
 
     def prefill(self, x_local: torch.Tensor, batch: int, seq_len: int, caches: List[KVCache]) -> torch.Tensor:
         h = x_local
+        if caches and isinstance(caches[0], PagedKVCache):
+            caches[0].state.ensure(seq_len)
         for blk, cache in zip(self.blocks, caches):
             h = blk.forward(h, "prefill", batch, seq_len, kv_cache=cache)
         return h
@@ -117,6 +128,8 @@ class HapModel:
         h = x_local
         if max_position is None and positions.is_cuda and not torch.cuda.is_current_stream_capturing() and caches:
             max_position = caches[0].check_positions(positions)  # one read-back for the whole step
+        if caches and isinstance(caches[0], PagedKVCache) and max_position is not None:
+            caches[0].state.ensure(max_position + 1)  # the new token's page
         for blk, cache in zip(self.blocks, caches):
             h = blk.forward(h, "decode", batch, kv_cache=cache, positions=positions, max_position=max_position)
         return h

@@ -455,3 +455,39 @@ def attn_decode(qkv: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     check(st, "hap_attn_decode")
     _count(3 if B else 0)
     return out
+
+
+def kv_cache_fill_paged(qkv: torch.Tensor, n_q: int, n_kv: int, head_dim: int, n_seqs: int, seq_len: int,
+                        k_pool: torch.Tensor, v_pool: torch.Tensor, block_table: torch.Tensor) -> None:
+    """Prefill k/v into a paged cache: pools [n_pages, n_kv, page, d], int32 block_table [B, max_pages]."""
+    lib = _lib.load()
+    _need(qkv, "qkv", BF16); _need(k_pool, "k_pool", BF16); _need(v_pool, "v_pool", BF16)
+    _need(block_table, "block_table", torch.int32)
+    _rowmajor(qkv, "qkv")
+    if k_pool.dim() != 4 or not (k_pool.is_contiguous() and v_pool.is_contiguous() and block_table.is_contiguous()):
+        raise ValueError("pools must be contiguous [n_pages, n_kv, page, d], block_table contiguous [B, max_pages]")
+    st = lib.hap_kv_cache_fill_paged(qkv.data_ptr(), qkv.stride(0), n_seqs, seq_len, n_q, n_kv, head_dim,
+                                     k_pool.data_ptr(), v_pool.data_ptr(), block_table.data_ptr(),
+                                     block_table.shape[1], k_pool.shape[2], _stream())
+    check(st, "hap_kv_cache_fill_paged")
+    _count(1 if n_seqs * seq_len else 0)
+
+
+def attn_decode_paged(qkv: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor, block_table: torch.Tensor,
+                      pos: torch.Tensor, n_q: int, n_kv: int, head_dim: int, out: torch.Tensor,
+                      workspace: torch.Tensor) -> torch.Tensor:
+    """Append + split-KV decode over a paged cache (see hap_attn_decode_paged)."""
+    lib = _lib.load()
+    _need(qkv, "qkv", BF16); _need(k_pool, "k_pool", BF16); _need(v_pool, "v_pool", BF16)
+    _need(block_table, "block_table", torch.int32); _need(pos, "pos", torch.int32); _need(out, "out", BF16)
+    if k_pool.dim() != 4 or not (k_pool.is_contiguous() and v_pool.is_contiguous() and block_table.is_contiguous()):
+        raise ValueError("pools must be contiguous [n_pages, n_kv, page, d], block_table contiguous [B, max_pages]")
+    B = pos.numel()
+    st = lib.hap_attn_decode_paged(qkv.data_ptr(), qkv.stride(0), k_pool.data_ptr(), v_pool.data_ptr(),
+                                   k_pool.shape[0], k_pool.shape[2], block_table.data_ptr(), block_table.shape[1],
+                                   pos.data_ptr(), B, n_q, n_kv, head_dim, float(head_dim ** -0.5), out.data_ptr(),
+                                   out.stride(0), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                                   _stream())
+    check(st, "hap_attn_decode_paged")
+    _count(3 if B else 0)
+    return out
