@@ -427,9 +427,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 a0 = f2split(ls2[0]), a1 = f2split(ls2[1]);
           l_run += (a0.x + a0.y) + (a1.x + a1.y);
         }
-        // rescale O in TMEM when the running max moved (PV_t,j-1 must have landed)
+        // PV_t,j-1 has landed (S_t,j, already in TMEM, was issued after it);
+        // every o_done phase is waited so the barrier protocol stays explicit
+        if (j > 0) WAIT(&o_done[t], (sc - 1) & 1);
+        // rescale O in TMEM when the running max moved
         if (__any_sync(0xffffffffu, j > 0 && alpha != 1.f)) {
-          WAIT(&o_done[t], (sc - 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D; c += 32) {
@@ -447,6 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // epilogue: O row / l -> bf16 -> global, then release O_t
       WAIT(&o_final[t], ic & 1);
+      WAIT(&o_done[t], (sc - 1) & 1);  // the item's last PV (same completion as o_final)
       ++ic;
       tc_fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;

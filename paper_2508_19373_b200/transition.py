@@ -87,6 +87,27 @@ def _unpack(cfg, w):
     return units
 
 
+def _unit_views(cfg, w):
+    """Per-unit (w13-like [.., 2I, h] interleaved tensor, row offset of the unit
+    inside it, hw, w2-like [h, I_unit] view) for the routed experts then the
+    shared units, without copying."""
+    El, Il = w.n_experts_local, w.inter_local
+    out = [(w.w13[e], 0, w.hw, w.w2[e]) for e in range(El)]
+    if cfg.n_shared:
+        out += [(w.ws13, u * Il, w.hw_s, w.ws2[:, u * Il:(u + 1) * Il]) for u in range(cfg.n_shared)]
+    return out
+
+
+def _gu_rows(t13, hw, r0, n, part):
+    """Rows [r0, r0+n) of the gate (part 0) or up (part 1) half of an
+    interleaved [2I, h] tensor as a strided [n/hw, hw, h] view (None when the
+    rows do not align with the hw blocks)."""
+    if r0 % hw or n % hw:
+        return None
+    v = t13.view(t13.shape[0] // (2 * hw), 2, hw, t13.shape[-1])
+    return v[r0 // hw:(r0 + n) // hw, part]
+
+
 def reshard_plan(lay_src_list, lay_dst_list, n_slices: int):
     """Deterministic transfer plan: for every destination rank, each (unit,
     slice) it needs and does not hold is fetched from one holder under the
@@ -150,11 +171,14 @@ def reshard_pack(cfg, w, lay_src, lay_dst):
     dsts = [mk(lay_dst.deg, r) for r in range(n)]
     own_src, own_dst, sends = reshard_plan(srcs, dsts, n_slices)
     me = lay_src.rank
-    units = _unpack(cfg, w)
     e0 = lay_src.experts[0]
     s0 = lay_src.inter_slice[0] // per
+    unpacked = []  # per-unit contiguous (gate, up, down^T), built only if a piece misses the fast path
 
     def local_piece(unit, s):
+        if not unpacked:
+            unpacked.append(_unpack(cfg, w))
+        units = unpacked[0]
         if unit < cfg.n_experts:
             u = units[unit - e0]
         else:
@@ -163,13 +187,30 @@ def reshard_pack(cfg, w, lay_src, lay_dst):
         return torch.stack([t[k * per:(k + 1) * per] for t in u])  # [3, per, h]
 
     piece_elems = 3 * per * h
-    send_chunks = [local_piece(uu, s) for r in range(n) for (uu, s) in sends[me][r]]
+    order = [(uu, s) for r in range(n) for (uu, s) in sends[me][r]]
     in_splits = [len(sends[me][r]) * piece_elems for r in range(n)]
     out_splits = [len(sends[q][me]) * piece_elems for q in range(n)]
     dev, dt = w.w13.device, w.w13.dtype
-    send = torch.cat([c.reshape(-1) for c in send_chunks]) if send_chunks else torch.empty(0, dtype=dt, device=dev)
+    send = torch.empty(len(order) * piece_elems, dtype=dt, device=dev)
+    src_views = _unit_views(cfg, w)
+
+    def unit_index(unit):
+        return unit - e0 if unit < cfg.n_experts else (lay_src.experts[1] - e0) + (unit - cfg.n_experts)
+
+    sv = send.view(len(order), 3, per, h)
+    for i, (uu, sl) in enumerate(order):
+        # each piece is written once, straight from the packed source layout
+        t13, base, hw_u, t2 = src_views[unit_index(uu)]
+        r0 = base + (sl - s0) * per
+        g, u_ = _gu_rows(t13, hw_u, r0, per, 0), _gu_rows(t13, hw_u, r0, per, 1)
+        if g is None:
+            sv[i].copy_(local_piece(uu, sl))
+        else:
+            sv[i, 0].view(per // hw_u, hw_u, h).copy_(g)
+            sv[i, 1].view(per // hw_u, hw_u, h).copy_(u_)
+            sv[i, 2].copy_(t2[:, (sl - s0) * per:(sl - s0 + 1) * per].t())
     ctx = dict(cfg=cfg, w=w, lay_dst=lay_dst, n=n, me=me, per=per, h=h, own_src=own_src, sends=sends,
-               local_piece=local_piece, piece_elems=piece_elems)
+               local_piece=local_piece, piece_elems=piece_elems, src_views=src_views, unit_index=unit_index, s0=s0)
     return send, in_splits, out_splits, ctx
 
 
@@ -197,13 +238,52 @@ def reshard_unpack(ctx, recv):
     de0, de1 = d.experts
     ds0, ds1 = d.inter_slice[0] // per, d.inter_slice[1] // per
     il = (ds1 - ds0) * per
+    hw = swiglu_half_width(il)
+    El_d = de1 - de0
+    dev, dt = w.w13.device, w.w13.dtype
+    units_d = list(range(de0, de1)) + [cfg.n_experts + u for u in range(cfg.n_shared)]
+    sil = cfg.n_shared * il
+    hw_s = swiglu_half_width(sil) if cfg.n_shared else 0
+    # fast path: every destination slice lands on whole hw blocks of its tensor
+    fast = per % hw == 0 and (not cfg.n_shared or (per % hw_s == 0 and il % hw_s == 0))
+    if fast:
+        w13 = torch.empty(El_d, 2 * il, h, dtype=dt, device=dev)
+        w2 = torch.empty(El_d, h, il, dtype=dt, device=dev)
+        ws13 = torch.empty(2 * sil, h, dtype=dt, device=dev) if cfg.n_shared else None
+        ws2 = torch.empty(h, sil, dtype=dt, device=dev) if cfg.n_shared else None
+        src_views, unit_index, s0 = ctx["src_views"], ctx["unit_index"], ctx["s0"]
+        for j, unit in enumerate(units_d):
+            if unit < cfg.n_experts:
+                t13, base, hw_u, t2 = w13[j], 0, hw, w2[j]
+            else:
+                u = unit - cfg.n_experts
+                t13, base, hw_u, t2 = ws13, u * il, hw_s, ws2[:, u * il:(u + 1) * il]
+            for sl in range(ds0, ds1):
+                r0 = base + (sl - ds0) * per
+                gd, ud = _gu_rows(t13, hw_u, r0, per, 0), _gu_rows(t13, hw_u, r0, per, 1)
+                dcols = t2[:, (sl - ds0) * per:(sl - ds0 + 1) * per]
+                key = (unit, sl)
+                if key in own_src[me]:  # straight from this rank's own packed weights
+                    st13, sbase, shw, st2 = src_views[unit_index(unit)]
+                    sr0 = sbase + (sl - s0) * per
+                    sg, su = _gu_rows(st13, shw, sr0, per, 0), _gu_rows(st13, shw, sr0, per, 1)
+                    if sg is not None:
+                        gd.copy_(sg)
+                        ud.copy_(su)
+                        dcols.copy_(st2[:, (sl - s0) * per:(sl - s0 + 1) * per])
+                        continue
+                pc = piece(key)
+                gd.copy_(pc[0].view(per // hw_u, hw_u, h))
+                ud.copy_(pc[1].view(per // hw_u, hw_u, h))
+                dcols.copy_(pc[2].t())
+        return dataclasses.replace(w, w13=w13, w2=w2, hw=hw, ws13=ws13, ws2=ws2, hw_s=hw_s,
+                                   n_experts_local=El_d, inter_local=il, shared_inter_local=sil)
 
     def assemble(unit):
         p = torch.cat([piece((unit, s)) for s in range(ds0, ds1)], dim=1)  # [3, il, h]
         return p[0], p[1], p[2]
 
     rout = [assemble(e) for e in range(de0, de1)]
-    hw = swiglu_half_width(il)
     w13 = interleave_gate_up(torch.stack([g for g, _, _ in rout]), torch.stack([u for _, u, _ in rout]), hw)
     w2 = torch.stack([dn.t() for _, _, dn in rout]).contiguous()
     ws13 = ws2 = None

@@ -1,0 +1,54 @@
+"""Expert reshard phases without a process group (CPU): every rank's
+reshard_pack is routed to its receivers by hand (what all_to_all_single does)
+and reshard_unpack must reproduce the destination layout's packed weights
+exactly — for the direct-copy fast path (slices on whole SwiGLU blocks) and
+the generic path alike, at N = 2, 4, 8."""
+
+import pytest
+import torch
+
+from paper_2508_19373_b200.config import BlockConfig
+from paper_2508_19373_b200.layout import PlanDegrees, RankLayout
+from paper_2508_19373_b200.transition import reshard_pack, reshard_unpack
+from paper_2508_19373_b200.weights import pack_rank_weights, synthetic_weights
+
+FAST = dict(name="rs-fast", n_layers=1, n_q_heads=2, n_kv_heads=2, head_dim=64, hidden=128, n_experts=8,
+            n_shared=0, top_k=2, inter=2048)
+SHARED = dict(name="rs-shared", n_layers=1, n_q_heads=2, n_kv_heads=2, head_dim=64, hidden=128, n_experts=8,
+              n_shared=2, top_k=4, inter=1024, norm_topk_prob=False, qkv_bias=True)
+GENERIC = dict(name="rs-generic", n_layers=1, n_q_heads=2, n_kv_heads=2, head_dim=64, hidden=128, n_experts=8,
+               n_shared=1, top_k=2, inter=352)
+
+
+def _simulate(cfg, n, src, dst):
+    W = synthetic_weights(cfg, "cpu", seed=0)
+    lay = lambda te, r: RankLayout(PlanDegrees(1, n, te[0], te[1], 1), r, cfg.n_q_heads, cfg.n_kv_heads,  # noqa: E731
+                                   cfg.n_experts, cfg.inter, cfg.n_shared)
+    packs = [reshard_pack(cfg, pack_rank_weights(cfg, W, lay(src, r)), lay(src, r), lay(dst, r)) for r in range(n)]
+    for r in range(n):
+        # the all-to-all: rank r receives, in source order, the chunk each source addressed to it
+        chunks = []
+        for q in range(n):
+            send, ins, _, _ = packs[q]
+            off = sum(ins[:r])
+            chunks.append(send[off:off + ins[r]])
+        got = reshard_unpack(packs[r][3], torch.cat(chunks))
+        want = pack_rank_weights(cfg, W, lay(dst, r))
+        for name in ("w13", "w2", "ws13", "ws2"):
+            a, b = getattr(got, name), getattr(want, name)
+            assert (a is None) == (b is None), name
+            if a is not None:
+                assert a.shape == b.shape and torch.equal(a, b), (cfg.name, n, src, dst, r, name)
+        assert got.hw == want.hw and got.hw_s == want.hw_s and got.inter_local == want.inter_local
+
+
+@pytest.mark.parametrize("cfg_kw", [FAST, SHARED, GENERIC], ids=["fast", "shared", "generic"])
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_reshard_phases_reproduce_destination_layout(cfg_kw, n):
+    cfg = BlockConfig(**cfg_kw)
+    # expert-TP degrees whose slice admits a SwiGLU tile width (a multiple of 8)
+    strat = [(t, n // t) for t in (1, 2, 4, 8) if t <= n and n % t == 0 and (cfg.inter // t) % 8 == 0]
+    for src in strat:
+        for dst in strat:
+            if src != dst:
+                _simulate(cfg, n, src, dst)
