@@ -109,15 +109,11 @@ int hap_gemm_qkv_rope(const void* A, int64_t M, int64_t lda, int64_t K, const vo
  * Split-K variants of the two GEMM entry points (same semantics).  With a
  * workspace, shapes whose tiles cannot cover the 148 SMs (small-M weight
  * streaming: decode projections, TP-sharded layers) cut K into slices run by
- * different CTAs, each writing fp32 partials to the workspace; the CTA that
- * stores a tile's last slice sums the slices in slice order (deterministic) and
- * applies the epilogue (a per-tile arrival counter in the last 256 KB of the
- * workspace; epilogues whose items straddle tiles fall back to a second
- * reduce kernel).  workspace: device scratch of ws_bytes
- * (hap_gemm_splitk_workspace_bytes() is the size the library plans for;
- * smaller => fewer slices), zero-filled once before its first use (every
- * launch leaves the counters zeroed); it must not be shared by GEMMs running
- * concurrently.  NULL workspace == the plain entry points.
+ * different CTAs, each writing fp32 partials to the workspace; a second kernel
+ * sums the slices in slice order (deterministic, no atomics) and applies the
+ * epilogue.  workspace: device scratch of ws_bytes (hap_gemm_splitk_workspace_bytes()
+ * is the size the library plans for; smaller => fewer slices); it must not be
+ * shared by GEMMs running concurrently.  NULL workspace == the plain entry points.
  */
 size_t hap_gemm_splitk_workspace_bytes(void);
 int hap_grouped_gemm_bf16_ex(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,

@@ -178,9 +178,17 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1)
     const int sidx = item % ns;
     const int64_t obase = ((int64_t)it.b * n_q + it.kvh * G + g) * ns + sidx;
     if (it.nk == 0) {
-      if (g < G && (lane & 3) == 0) {
-        ws_ml[obase * 2] = -INFINITY;
-        ws_ml[obase * 2 + 1] = 0.f;
+      // an empty split (past the sequence): weight 0 in the merge, and its o row
+      // zeroed so the merge never multiplies stale workspace bytes (possibly
+      // NaN) by that zero weight
+      if (g < G) {
+        float* dst = ws_o + obase * D;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) *reinterpret_cast<float2*>(dst + n * 8 + q2) = make_float2(0.f, 0.f);
+        if ((lane & 3) == 0) {
+          ws_ml[obase * 2] = -INFINITY;
+          ws_ml[obase * 2 + 1] = 0.f;
+        }
       }
       continue;
     }

@@ -72,12 +72,6 @@ struct Params {
   // epilogue — deterministic, no atomics.
   int32_t ksplit;
   float* part;
-  // fused reduction (fuse_reduce): the CTA finishing a tile's last slice sums
-  // the tile's slices and runs the epilogue itself (no second launch);
-  // tile_cnt = per-tile arrival counters at the end of the workspace (zero
-  // before the first launch; each is re-zeroed by the CTA that reduces)
-  int32_t fuse_reduce;
-  int32_t* tile_cnt;
   // scatter epilogue (EP combine over peer memory): row r of segment s is
   // stored at seg_dst[s] + (r - seg[s] + seg_dst_row0[s]) * ldc, seg_dst[s]
   // being a (possibly peer-mapped) device address; NULL = C
@@ -88,15 +82,6 @@ struct Params {
 constexpr int kEpiRope = 3;     // internal epilogue id (hap_gemm_qkv_rope)
 constexpr int64_t kSplitMax = 16;
 constexpr size_t kSplitWorkspaceBytes = (size_t)32 << 20;
-constexpr size_t kTileCntBytes = (size_t)256 << 10;  // fused-reduction tile counters (end of the workspace)
-
-static bool fused_reduce_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("HAP_GEMM_FUSED_REDUCE");  // A/B switch: 0 = separate reduce launch
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
 constexpr int64_t kRasterL2Bytes = 48ll << 20;  // A rows of one raster group kept L2-resident across n-blocks
 
 struct TileCoord {
@@ -145,8 +130,6 @@ __device__ __forceinline__ TileCoord map_tile(int t, const int32_t* tile_start, 
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
-__device__ __forceinline__ void reduce_row_items(const Params& p, int row, int it0, int it1);
-
 // kPair == 1: one CTA computes a 128 x BN tile (tcgen05 cta_group::1).
 // kPair == 2: a 2-CTA cluster computes a 256 x BN tile with cta_group::2 —
 // each CTA stages its 128 A rows and HALF of the B tile (BN/2 rows), the
@@ -176,7 +159,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ int32_t group_s[kMaxSegs];
   __shared__ int32_t tile_start_s[kMaxSegs + 1];
   __shared__ float inv_freq_s[128];
-  __shared__ int red_last_s;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -369,34 +351,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      __uint_as_float(v[i + 3])));
             }
           }
-        }
-      }
-      if (ksplit > 1 && p.fuse_reduce) {
-        // fused split-K reduction: the CTA that stores a tile's last slice
-        // sums all slices (slice order, as splitk_reduce_kernel) and runs the
-        // epilogue; per-tile counters live at the end of the workspace
-        __threadfence();
-        named_bar_sync(1, 128);  // the four epilogue warps' partial stores are issued + fenced
-        if (q == 0 && lane == 0) red_last_s = atomicAdd(&p.tile_cnt[t], 1) == ksplit - 1;
-        named_bar_sync(1, 128);
-        if (red_last_s) {
-          __threadfence();
-          if (row_ok) {
-            const int n0 = c.n_blk * p.BN, ncols = min(p.BN, p.N - n0);
-            int it0, it1;
-            if (p.epi == HAP_EPI_SWIGLU) {
-              it0 = c.n_blk * (p.hw / 8);
-              it1 = it0 + p.hw / 8;
-            } else if (p.epi == kEpiRope) {
-              it0 = n0 / 16;
-              it1 = (n0 + ncols) / 16;
-            } else {
-              it0 = n0 / 8;
-              it1 = (n0 + ncols) / 8;
-            }
-            reduce_row_items(p, row, it0, it1);
-          }
-          if (q == 0 && lane == 0) p.tile_cnt[t] = 0;  // ready for the next launch
         }
       }
       if (!do_epi) {
@@ -628,11 +582,15 @@ __device__ __forceinline__ void sum_slices8(const float* part, int64_t slice, in
   }
 }
 
-// Sum the slices of output item `it` of row `row` and apply the epilogue
-// (items: 8 columns for the store epilogue, 8 outputs = 16 partial columns
-// for SwiGLU / RoPE).
-__device__ __forceinline__ void reduce_item(const Params& p, int row, int it) {
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(Params p) {
+  pdl_trigger();
+  pdl_wait();
   const int N = p.N;
+  const int items = p.epi == HAP_EPI_SWIGLU ? N / 16 : (p.epi == kEpiRope ? N / 16 : N / 8);
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(idx / items), it = (int)(idx % items);
+  if (row >= p.a_rows) return;
+  if (p.seg && (row < p.seg[0] || row >= p.seg[p.n_segs])) return;
   const int64_t slice = (int64_t)p.a_rows * N;
   const int64_t rbase = (int64_t)row * N;
   __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
@@ -708,23 +666,6 @@ __device__ __forceinline__ void reduce_item(const Params& p, int row, int it) {
     for (int i = 0; i < 4; ++i) o[i] = pack_bf16x2(f[2 * i], f[2 * i + 1]);
     *reinterpret_cast<uint4*>(crow + col) = make_uint4(o[0], o[1], o[2], o[3]);
   }
-}
-
-__device__ __forceinline__ void reduce_row_items(const Params& p, int row, int it0, int it1) {
-#pragma unroll 1
-  for (int it = it0; it < it1; ++it) reduce_item(p, row, it);
-}
-
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(Params p) {
-  pdl_trigger();
-  pdl_wait();
-  const int N = p.N;
-  const int items = p.epi == HAP_EPI_SWIGLU ? N / 16 : (p.epi == kEpiRope ? N / 16 : N / 8);
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = (int)(idx / items), it = (int)(idx % items);
-  if (row >= p.a_rows) return;
-  if (p.seg && (row < p.seg[0] || row >= p.seg[p.n_segs])) return;
-  reduce_item(p, row, it);
 }
 
 // Choose (BN, ksplit) for a single-CTA launch whose tiles cannot cover the
@@ -870,21 +811,12 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
   // over more CTAs when a workspace is supplied, then reduce + epilogue.
   // Only single-m-block launches split; the slice plan depends on (N, K, M) only
   // through the tile bound and the workspace fit, and repeats bit for bit.
-  if (ws && ws_bytes >= kTileCntBytes + 16 && a_rows <= BM) {
-    plan_split(p, a_rows, K, N, n_segs, ws_bytes - kTileCntBytes);
+  if (ws && ws_bytes >= 16 && a_rows <= BM) {
+    plan_split(p, a_rows, K, N, n_segs, ws_bytes);
     p.part = reinterpret_cast<float*>(ws);
-    // fused reduction when every tile holds whole epilogue items: SwiGLU tiles
-    // are one gate|up block pair, RoPE tiles whole heads; at most
-    // kTileCntBytes/4 tiles (the counters at the end of the workspace)
-    const int64_t tiles = (a_rows < n_segs ? a_rows : n_segs) * ((N + p.BN - 1) / p.BN);
-    const bool whole = p.epi == HAP_EPI_STORE || (p.epi == HAP_EPI_SWIGLU && p.BN == 2 * p.hw) ||
-                       (p.epi == kEpiRope && p.BN % p.head_dim == 0);
-    p.fuse_reduce = (fused_reduce_enabled() && p.ksplit > 1 && whole &&
-                     n_segs * ((N + p.BN - 1) / p.BN) <= (int64_t)(kTileCntBytes / 4) && tiles > 0) ? 1 : 0;
-    p.tile_cnt = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(ws) + ws_bytes - kTileCntBytes);
   }
   const int st = launch_impl<1>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
-  if (st != HAP_OK || p.ksplit == 1 || p.fuse_reduce) return st;
+  if (st != HAP_OK || p.ksplit == 1) return st;
   const int items = p.epi == HAP_EPI_STORE ? (int)(N / 8) : (int)(N / 16);
   const int64_t threads = a_rows * items;
   { if (hap::launch_k(splitk_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0,

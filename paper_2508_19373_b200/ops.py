@@ -65,8 +65,8 @@ def stream_workspace(kind: str, device: torch.device) -> torch.Tensor:
     ws = _WS.get(key)
     if ws is None:
         lib = _lib.load()
-        if kind == "splitk":  # zero once: the fused split-K reduction's tile counters live at its end
-            n, zero = int(lib.hap_gemm_splitk_workspace_bytes()), True
+        if kind == "splitk":
+            n, zero = int(lib.hap_gemm_splitk_workspace_bytes()), False
         elif kind == "attn":
             n, zero = int(lib.hap_attn_prefill_workspace_bytes()), True
         elif kind == "router":
