@@ -126,11 +126,14 @@ def scaled(cfg: BlockConfig, **kw) -> BlockConfig:
 
 
 # Measured on this pool's B200s (MEASURED_PEAKS.json: bf16 1652.5 TF/s burst);
-# NVLink: measured 8-rank all-reduce bus bandwidth 725 GB/s (B200_PROFILING.md).
+# NVLink: the pool's measured 8-rank all-reduce bus bandwidth, 725 GB/s at 1 GiB
+# (B200_PROFILING.md; this run's boxes have one GPU, so it is not re-measured
+# here); H2D: pinned host->device copy measured by scripts/measure_transition.py
+# (profiles/r01_transition_measurements.json: 55.2 GB/s).
 B200_PEAK_FLOPS = 1.6525e15
 B200_HBM_BYTES = 180e9
 B200_NVLINK_BW = 725e9
-B200_H2D_BW = 50e9
+B200_H2D_BW = 55.2e9
 
 
 def b200_hardware(n_devices: int, peak_flops: float = B200_PEAK_FLOPS, intra_node_bw: float = B200_NVLINK_BW,

@@ -188,6 +188,75 @@ __global__ void __launch_bounds__(kRanges * NE) router_small_kernel(const __nv_b
   finish_token<NE>(tot, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
 }
 
+// finish_token for one token by a whole warp (the wide router's last CTA):
+// lane l holds logits l, l+32, l+64; the max, the softmax denominator and each
+// of the top_k arg-max rounds are warp reductions (ties -> lower index, as in
+// finish_token) instead of one thread's sequential passes over ~65 logits.
+__device__ __forceinline__ void finish_token_warp(const float* __restrict__ lg, int n_rows, int t, int E, int top_k,
+                                                  int renorm, int has_shared, int32_t* __restrict__ topk_idx,
+                                                  float* __restrict__ topk_w, float* __restrict__ shared_gate,
+                                                  float* __restrict__ logits_out) {
+  const int lane = threadIdx.x & 31;
+  float v[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int e = lane + 32 * i;
+    v[i] = e < n_rows ? __ldcg(lg + e) : 0.f;
+    if (logits_out && e < E) logits_out[(int64_t)t * E + e] = v[i];
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (lane + 32 * i < E) mx = fmaxf(mx, v[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float den = 0.f;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (lane + 32 * i < E) den += expf(v[i] - mx);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+  bool taken[3] = {false, false, false};
+  float wsum = 0.f;
+  for (int s = 0; s < top_k; ++s) {
+    float best = -INFINITY;
+    int bi = INT32_MAX;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && !taken[i] && (bi == INT32_MAX || v[i] > best)) {
+        best = v[i];
+        bi = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oi != INT32_MAX && (bi == INT32_MAX || ob > best || (ob == best && oi < bi))) {
+        best = ob;
+        bi = oi;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (bi == lane + 32 * i) taken[i] = true;
+    const float p = expf(best - mx) / den;
+    wsum += p;
+    if (lane == 0) {
+      topk_idx[(int64_t)t * top_k + s] = bi;
+      topk_w[(int64_t)t * top_k + s] = p;
+    }
+  }
+  if (lane == 0) {
+    if (renorm) {
+      const float inv = 1.f / wsum;
+      for (int s = 0; s < top_k; ++s) topk_w[(int64_t)t * top_k + s] *= inv;
+    }
+    if (has_shared && shared_gate) shared_gate[t] = 1.f / (1.f + expf(-__ldcg(lg + E)));
+  }
+}
+
 // Small T, wide router (rows > 8): one CTA per (token, group of 8 router rows)
 // instead of one per token, so a decode step with few tokens streams the
 // router rows on rows/8 SMs.  Chains and range order are those of
@@ -269,14 +338,11 @@ __global__ void __launch_bounds__(kRanges * kGroupRows) router_group_kernel(
   __syncthreads();
   if (threadIdx.x == 0) last_s = atomicAdd(&cnt_ws[t], 1) == n_groups - 1;
   __syncthreads();
-  if (!last_s || threadIdx.x != 0) return;
+  if (!last_s || threadIdx.x >= 32) return;
   __threadfence();
-  cnt_ws[t] = 0;  // ready for the next launch
-  float tot[NE];
-#pragma unroll
-  for (int ee = 0; ee < NE; ++ee)
-    tot[ee] = ee < n_rows_w ? __ldcg(&logits_ws[(int64_t)t * kMaxRouterRows + ee]) : 0.f;
-  finish_token<NE>(tot, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
+  if (threadIdx.x == 0) cnt_ws[t] = 0;  // ready for the next launch
+  finish_token_warp(logits_ws + (int64_t)t * kMaxRouterRows, n_rows_w, t, E, top_k, renorm, has_shared, topk_idx,
+                    topk_w, shared_gate, logits_out);
 }
 
 template <int NE>

@@ -31,7 +31,8 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--input-len", type=int, default=2048)
     ap.add_argument("--output-len", type=int, default=64)
-    ap.add_argument("--out", default="gpurun_out/r01_e2e_model.json")
+    ap.add_argument("--out", default="gpurun_out/r02_e2e_model.json")
+    ap.add_argument("--page", type=int, default=64, help="also run the decode steps over a paged KV cache")
     args = ap.parse_args()
     cfg = get_config(args.config)
     L = args.layers or cfg.n_layers
@@ -66,6 +67,30 @@ def main():
     decode_s = ev[2].elapsed_time(ev[3]) / 1e3
     measured_total = prefill_s + decode_s
 
+    # the same decode steps over a paged KV cache (pages handed out as the
+    # sequences grow: one host-side ensure per step, a table copy at page edges)
+    paged = None
+    if args.page:
+        pcaches = model.new_caches(B, S + O, paged=True, page=args.page)
+        model.prefill(x, B, S, pcaches)
+        st = pcaches[0].state
+        st.ensure(S + 1)
+        pos.fill_(S)
+        pgraph, _ = model.capture_decode(xd, B, pcaches, pos)
+        pos.fill_(S)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(O):
+            st.ensure(S + i + 1)
+            pgraph.replay()
+            pos.add_(1)
+        e1.record()
+        torch.cuda.synchronize()
+        pd = e0.elapsed_time(e1) / 1e3
+        paged = {"page_tokens": args.page, "decode_s": pd, "decode_ms_per_token_step": pd / O * 1e3,
+                 "pages_held": sum(st.held), "vs_contiguous": pd / decode_s}
+
     # predictions: reference simulate() on roofline tensors and on measured module tables
     spec = cfg.to_model_spec()
     scen = mp.InferenceScenario(B, S, O)
@@ -81,6 +106,7 @@ def main():
         "measured": {"prefill_s": prefill_s, "decode_s": decode_s, "decode_ms_per_token_step": decode_s / O * 1e3,
                      "total_s": measured_total, "prefill_tokens_per_s": B * S / prefill_s,
                      "decode_tokens_per_s": B * O / decode_s},
+        "measured_paged_kv": paged,
         "predicted_roofline": {"prefill_s": roof.prefill_s * scale, "decode_s": roof.decode_s * scale,
                                "total_s": (roof.prefill_s + roof.decode_s) * scale},
         "predicted_measured_tables": {"prefill_s": cal.prefill_s * scale, "decode_s": cal.decode_s * scale,
