@@ -66,6 +66,27 @@ def _events_time(fn, reps: int, warmup: int = 2) -> float:
     return statistics.median(ts)
 
 
+def _graph_time(fn, reps: int, warmup: int = 2) -> float:
+    """Time fn as CUDA-graph replays — how the executor runs a decode step, so a
+    decode cell carries no per-launch host overhead the model does not pay."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(warmup):
+            fn()
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    t = _events_time(g.replay, reps, warmup=warmup)
+    del g
+    return t
+
+
+def _stage_time(fn, stage: str, reps: int) -> float:
+    return _graph_time(fn, reps) if stage == "decode" else _events_time(fn, reps)
+
+
 def _rand(shape, std=1.0):
     t = torch.randn(shape, device="cuda", dtype=BF16)
     return t.mul_(std) if std != 1.0 else t
@@ -104,7 +125,7 @@ def measure_attention(cfg: BlockConfig, tp: int, b_rep: int, S: int, stage: str,
             qkv = K.gemm_qkv_rope(xn, wqkv, pos, nq + nkv, d, cfg.rope_theta, bias=bqkv)
             K.attn_decode(qkv, kc, vc, pos, nq, nkv, d, attn, ws)
             K.gemm(attn, wo, residual=x)
-    t = _events_time(fn, reps)
+    t = _stage_time(fn, stage, reps)
     del x, wqkv, wo, attn
     return t
 
@@ -198,7 +219,7 @@ def measure_experts(cfg: BlockConfig, tp: int, ep: int, dp: int, B: int, S: int,
             hs = K.gemm(x_own, ws13, swiglu_half=hws)
             ys = K.gemm(hs, ws2)
         K.moe_combine(y_back, dst, tw, T_own, k, out, residual=x_own, shared_y=ys, shared_gate=sg)
-    t = _events_time(fn, reps)
+    t = _stage_time(fn, stage, reps)
     del x_all, x_rep, w13, w2, x_recv, H, Y
     torch.cuda.empty_cache()
     return t
