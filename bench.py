@@ -345,6 +345,27 @@ def cpu_decode_baseline(cfg, batch: int = DECODE_BATCH, kv: int = DECODE_KV):
             "sample": f"one {cfg.name} decode step B={batch} @ kv {kv} through oracle decode_forward (fp32)"}
 
 
+def planner_baseline(cfg, world: int, reps: int = 20):
+    """The reference's own CPU path on this workload:
+    moeplan plan() for the prefill and decode scenarios, roofline tables and
+    the B200-measured tables, median of `reps` calls on the host."""
+    from paper_2508_19373_b200.plan import calibrated_plan, plan_for
+
+    out = {}
+    for name, args in (("prefill_8x2048", (PREFILL_BATCH, PREFILL_SEQ, 0)),
+                       ("decode_b64", (DECODE_BATCH, DECODE_KV // 2, DECODE_KV))):
+        for kind, fn in (("roofline", plan_for), ("measured_tables", calibrated_plan)):
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                fn(cfg, world, *args)
+                ts.append(time.perf_counter() - t0)
+            out[f"{name}_{kind}_ms"] = statistics.median(ts) * 1e3
+    out.update({"reps": reps, "cores": 1, "what": "moeplan.plan / solve_ilp on the host (reference CPU path), "
+                                                  "median of reps"})
+    return out
+
+
 def cpu_baseline(cfg, sample_tokens: int, reps: int = 2, decode: bool = True):
     fn = cpu_reference_setup(cfg, sample_tokens)
     fn()
@@ -357,6 +378,7 @@ def cpu_baseline(cfg, sample_tokens: int, reps: int = 2, decode: bool = True):
                      f"dims), 1 sequence x {sample_tokens} tokens prefill, mean of {reps}"}
     if decode:
         out["decode"] = cpu_decode_baseline(cfg)
+    out["planner"] = planner_baseline(cfg, 8)  # the 8-GPU plan search the reference exists for
     return out
 
 
