@@ -447,7 +447,7 @@ struct RouterTmaGeo {
 };
 
 template <int NE, int TPL, int CH>
-__global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
+__global__ void __launch_bounds__(kThreads, NE <= 8 ? (TPL == 1 ? 4 : 2) : 1)
     router_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int T,
                       int h, int E, int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx,
                       float* __restrict__ topk_w, float* __restrict__ shared_gate, float* __restrict__ logits_out) {
@@ -564,6 +564,29 @@ __global__ void __launch_bounds__(kThreads, NE <= 8 ? 2 : 1)
   finish_token<NE>(tot, t, E, top_k, renorm, has_shared, topk_idx, topk_w, shared_gate, logits_out);
 }
 
+template <int NE, int TPL, int CH>
+static int launch_router_tma(const void* x, int64_t T, int64_t h, const void* w, int64_t E, int has_shared,
+                             int64_t k, int renorm, int32_t* idx, float* tw, float* sg, float* logits,
+                             cudaStream_t st) {
+  using G = RouterTmaGeo<NE, TPL, CH>;
+  static_assert(G::kSmem <= 227 * 1024, "router smem");
+  auto kern = router_tma_kernel<NE, TPL, CH>;
+  static int configured_tma = 0;
+  if (!configured_tma) {
+    if (configure_smem((const void*)kern, G::kSmem)) return HAP_ERR_LAUNCH;
+    configured_tma = 1;
+  }
+  CUtensorMap tmX, tmW;
+  if (!encode_tmap_2d_bf16_sw(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, CH, G::kTB, CH * 2) ||
+      !encode_tmap_2d_bf16_sw(&tmW, w, (uint64_t)h, (uint64_t)(E + has_shared), (uint64_t)h * 2, CH, NE, 0))
+    return HAP_ERR_DRIVER;
+  if (hap::launch_k(kern, dim3((unsigned)((T + G::kTB - 1) / G::kTB)), dim3(kThreads), G::kSmem, st, tmX, tmW,
+                    (int)T, (int)h, (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess)
+    return HAP_ERR_LAUNCH;
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
+}
+
 template <int NE>
 static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E, int64_t k, int renorm,
                   int has_shared, int32_t* idx, float* tw, float* sg, float* logits, void* ws, size_t ws_bytes,
@@ -617,30 +640,19 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
     HAP_CHECK_LAUNCH();
     return HAP_OK;
   }
-  {
-    // TMA-staged variant: 2 tokens per lane, 32-element chunks
-    constexpr int TPL = 2;
-    constexpr int CH = 32;
-    using G = RouterTmaGeo<NE, TPL, CH>;
-    static_assert(G::kSmem <= 227 * 1024, "router smem");
-    auto kern = router_tma_kernel<NE, TPL, CH>;
-    const int smem_tma = G::kSmem;
-    if (h % (kRanges * CH) == 0) {
-      static int configured_tma = 0;
-      if (!configured_tma) {
-        if (configure_smem((const void*)kern, smem_tma)) return HAP_ERR_LAUNCH;
-        configured_tma = 1;
-      }
-      CUtensorMap tmX, tmW;
-      if (!encode_tmap_2d_bf16_sw(&tmX, x, (uint64_t)h, (uint64_t)T, (uint64_t)h * 2, CH, G::kTB, CH * 2) ||
-          !encode_tmap_2d_bf16_sw(&tmW, w, (uint64_t)h, (uint64_t)(E + has_shared), (uint64_t)h * 2, CH, NE, 0))
-        return HAP_ERR_DRIVER;
-      { if (hap::launch_k(kern, dim3((unsigned)((T + G::kTB - 1) / G::kTB)), dim3(kThreads),
-                          smem_tma, st, tmX, tmW, (int)T, (int)h, (int)E, (int)k, renorm, has_shared, idx, tw, sg,
-                          logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
-      HAP_CHECK_LAUNCH();
-      return HAP_OK;
-    }
+  if (h % (kRanges * 32) == 0) {
+    // TMA-staged variant, 32-element chunks, 2 tokens per lane (64-token CTAs,
+    // 2 per SM).  1 token per lane (32-token CTAs, 4 per SM: twice the CTAs in
+    // flight) measured slower, 59 vs 41 us at Mixtral prefill: the kernel is
+    // issue-bound on the weight re-expansion and operand moves, which the
+    // 2-token layout amortises over twice the tokens (HAP_ROUTER_TPL A/B switch)
+    static const int tpl = [] {
+      const char* e = getenv("HAP_ROUTER_TPL");
+      return e ? atoi(e) : 2;
+    }();
+    if (NE <= 8 && tpl == 1)
+      return launch_router_tma<NE, 1, 32>(x, T, h, w, E, has_shared, k, renorm, idx, tw, sg, logits, st);
+    return launch_router_tma<NE, 2, 32>(x, T, h, w, E, has_shared, k, renorm, idx, tw, sg, logits, st);
   }
   const int grid = (int)((T + 31) / 32);
   { if (hap::launch_k(router_kernel<NE>, dim3(grid), dim3(kThreads), smem, st, 
