@@ -147,7 +147,8 @@ template <int D, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out, int64_t ldo, int S,
-                     int n_q, int n_kv, int n_seqs, float scale_log2, int causal, int st32, int* __restrict__ sched) {
+                     int n_q, int n_kv, int n_seqs, float scale_log2, int causal, int st32, int* __restrict__ sched,
+                     int opt) {
   pdl_trigger();
   pdl_wait();
   constexpr int kTile = PairSmem<D>::kTile;
@@ -382,51 +383,72 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int c = 0; c < BN; ++c) sv[c] = c < lim ? sv[c] : __float_as_uint(-INFINITY);
         }
-        float pm[8];
+        // P = 2^(s*scale - m) into TMEM over S (bf16 pairs) and the row sum, in
+        // packed fp32 pairs (FFMA2/FADD2); with EMU a fraction of the pairs takes
+        // 2^x on the FMA pipe (exp2_poly2).  track: also reduce the raw row max.
+        float pm[4];
+        auto pass = [&](float msub, bool track) -> float {
+          const uint64_t sc2 = f2dup(scale_log2), nm2 = f2dup(-msub);
+          uint64_t ls2[2] = {0ull, 0ull};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) pm[i] = __uint_as_float(sv[i]);
+          for (int i = 0; i < 4; ++i) pm[i] = -INFINITY;
 #pragma unroll
-        for (int c = 8; c < BN; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sv[c]));
-        const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                               fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) *
-                         scale_log2;
-        float alpha = 1.f;
-        if (mx > m_run + kRescaleThreshold || m_run == -INFINITY) {
-          alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mx);
-          m_run = mx;
-          l_run *= alpha;
-        }
-        const float msub = (m_run == -INFINITY) ? 0.f : m_run;
-        // x = s*scale - m and the row sums in packed fp32 pairs (FFMA2/FADD2);
-        // with EMU one pair in four takes 2^x on the FMA pipe (exp2_poly2), so
-        // the SFU queue of the two softmax warpgroups sharing an SMSP is 3/4 as
-        // long as the tensor pipe's S+PV work per K/V step
-        const uint64_t sc2 = f2dup(scale_log2), nm2 = f2dup(-msub);
-        uint64_t ls2[2] = {0ull, 0ull};
+          for (int h = 0; h < BN / 64; ++h) {
+            uint32_t pk[32];
 #pragma unroll
-        for (int h = 0; h < BN / 64; ++h) {
-          uint32_t pk[32];
-#pragma unroll
-          for (int c2 = 0; c2 < 32; ++c2) {
-            const uint64_t x01 =
-                ffma2r(f2pack(__uint_as_float(sv[64 * h + 2 * c2]), __uint_as_float(sv[64 * h + 2 * c2 + 1])), sc2, nm2);
-            uint64_t p01;
-            if ((EMU == 1 && (c2 & 3) == 3) || (EMU == 2 && (c2 & 7) == 7)) {
-              p01 = exp2_poly2(x01);
-            } else {
-              const float2 xx = f2split(x01);
-              p01 = f2pack(fast_exp2(xx.x), fast_exp2(xx.y));
+            for (int c2 = 0; c2 < 32; ++c2) {
+              const float s0 = __uint_as_float(sv[64 * h + 2 * c2]), s1 = __uint_as_float(sv[64 * h + 2 * c2 + 1]);
+              if (track) pm[c2 & 3] = fmaxf(pm[c2 & 3], fmaxf(s0, s1));
+              const uint64_t x01 = ffma2r(f2pack(s0, s1), sc2, nm2);
+              uint64_t p01;
+              if ((EMU == 1 && (c2 & 3) == 3) || (EMU == 2 && (c2 & 7) == 7)) {
+                p01 = exp2_poly2(x01);
+              } else {
+                const float2 xx = f2split(x01);
+                p01 = f2pack(fast_exp2(xx.x), fast_exp2(xx.y));
+              }
+              fadd2(ls2[c2 & 1], p01);
+              const float2 pp = f2split(p01);
+              pk[c2] = pack_bf16x2(pp.x, pp.y);
             }
-            fadd2(ls2[c2 & 1], p01);
-            const float2 pp = f2split(p01);
-            pk[c2] = pack_bf16x2(pp.x, pp.y);
+            tmem_st_x32(tS(t) + lane_off + 32 * h, pk);
           }
-          tmem_st_x32(tS(t) + lane_off + 32 * h, pk);
-        }
-        {
           const float2 a0 = f2split(ls2[0]), a1 = f2split(ls2[1]);
-          l_run += (a0.x + a0.y) + (a1.x + a1.y);
+          return (a0.x + a0.y) + (a1.x + a1.y);
+        };
+        float alpha = 1.f;
+        float lsum;
+        if (opt && m_run != -INFINITY) {
+          // optimistic: exponentials against the running max while the tile max
+          // is reduced alongside (off the critical path); a row whose max grew
+          // past the threshold redoes its pass with the new max — the same
+          // values the max-first order produces
+          lsum = pass(m_run, true);
+          const float mx =
+              fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])) * scale_log2;
+          if (mx > m_run + kRescaleThreshold) {
+            alpha = fast_exp2(m_run - mx);
+            m_run = mx;
+            l_run *= alpha;
+            lsum = pass(m_run, false);
+          }
+        } else {
+          float pq[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pq[i] = __uint_as_float(sv[i]);
+#pragma unroll
+          for (int c = 8; c < BN; ++c) pq[c & 7] = fmaxf(pq[c & 7], __uint_as_float(sv[c]));
+          const float mx = fmaxf(fmaxf(fmaxf(pq[0], pq[1]), fmaxf(pq[2], pq[3])),
+                                 fmaxf(fmaxf(pq[4], pq[5]), fmaxf(pq[6], pq[7]))) *
+                           scale_log2;
+          if (mx > m_run + kRescaleThreshold || m_run == -INFINITY) {
+            alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mx);
+            m_run = mx;
+            l_run *= alpha;
+          }
+          lsum = pass((m_run == -INFINITY) ? 0.f : m_run, false);
         }
+        l_run += lsum;
         // PV_t,j-1 has landed (S_t,j, already in TMEM, was issued after it);
         // every o_done phase is waited so the barrier protocol stays explicit
         if (j > 0) WAIT(&o_done[t], (sc - 1) & 1);
@@ -493,6 +515,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+static int attn_opt() {
+  static const int on = [] {
+    // A/B switch, default off: exponentials against the running max with the
+    // tile max reduced alongside (+ a redo for rows whose max moved) measured
+    // bit-identical and no faster (causal 328-329 vs 325-327 us): the softmax
+    // is bound by the SFU and issue slots, not by the max's latency
+    const char* e = getenv("HAP_ATTN_OPT");
+    return e ? atoi(e) : 0;
+  }();
+  return on;
+}
+
 template <int D, int EMU>
 static int launch_pair(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* out,
                        int64_t ldo, int64_t n_seqs, int64_t S, int64_t n_q, int64_t n_kv, float scale, int32_t causal,
@@ -515,7 +549,8 @@ static int launch_pair(const void* q, int64_t ldq, const void* k, int64_t ldk, c
   if (hap::launch_k(kern, dim3(grid), dim3(kThreads), PairSmem<D>::kTotal, st, mq, mk, mv,
                     reinterpret_cast<__nv_bfloat16*>(out), ldo, (int)S, (int)n_q, (int)n_kv, (int)n_seqs,
                     scale * 1.4426950408889634f, causal,
-                    (int)(((reinterpret_cast<uintptr_t>(out) | (uintptr_t)(ldo * 2)) & 31) == 0), sched) != cudaSuccess)
+                    (int)(((reinterpret_cast<uintptr_t>(out) | (uintptr_t)(ldo * 2)) & 31) == 0), sched,
+                    attn_opt()) != cudaSuccess)
     return HAP_ERR_LAUNCH;
   HAP_CHECK_LAUNCH();
   return HAP_OK;
