@@ -166,6 +166,22 @@ int hap_peer_copy_rows(const void* src, int64_t rows_max, int64_t h, const int32
  * Replaces: the AllReduce rows of comm_volume (strategies.py:314-322, 341-342)
  * on the decode path.
  */
+/*
+ * One-shot all-reduce through NVLink SHARP (NVSwitch multicast memory): the
+ * caller binds one physical allocation per device to a multicast object and
+ * passes this rank's unicast (uc_base) and multicast (mc_base) views of it,
+ * hap_nvls_allreduce_bytes(n_max, n_ctas) bytes, zero-filled before the first
+ * call, and an int32 epoch[n_ctas] (zero).  Each CTA copies its slice into
+ * its own buffer, arrives with one multimem.red on a per-CTA counter, waits
+ * for all ranks and reads its slice with multimem.ld_reduce (in-switch sum,
+ * fp32 accumulation, one bf16 rounding).  No host work: graph capturable.
+ * Replaces: the decode-size AllReduce rows of comm_volume (strategies.py:314-322,
+ * 341-342).
+ */
+size_t hap_nvls_allreduce_bytes(int64_t n_max, int32_t n_ctas);
+int hap_nvls_allreduce_bf16(const void* in, void* out, void* uc_base, void* mc_base, int32_t* epoch, int64_t n,
+                            int64_t n_max, int32_t n_ranks, int32_t n_ctas, void* stream);
+
 size_t hap_peer_allreduce_sig_bytes(int32_t n_ranks, int32_t n_ctas);
 int hap_peer_allreduce_bf16(const int64_t* in_ptrs, const int64_t* out_ptrs, const int64_t* epoch_ptrs,
                             const int64_t* data_ptrs, const int64_t* sig_ptrs, int64_t n, int64_t n_max,

@@ -70,6 +70,11 @@ SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p],
     ),
     "hap_peer_allreduce_sig_bytes": (c_size_t, [ctypes.c_int32, ctypes.c_int32]),
+    "hap_nvls_allreduce_bytes": (c_size_t, [c_int64, ctypes.c_int32]),
+    "hap_nvls_allreduce_bf16": (
+        ctypes.c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, ctypes.c_int32, ctypes.c_int32, c_void_p],
+    ),
     "hap_peer_allreduce_bf16": (
         ctypes.c_int,
         [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, ctypes.c_int32, ctypes.c_int32,

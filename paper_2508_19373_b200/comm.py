@@ -60,17 +60,20 @@ class Comm:
     def _g(self, kind):
         return self.groups[kind][1]
 
-    def enable_peer_allreduce(self, kinds, n_max: int = 1 << 20) -> None:
+    def enable_peer_allreduce(self, kinds, n_max: int = 1 << 20, mode: str = "peer") -> None:
         """Route all-reduces of bf16 tensors up to n_max elements on these groups
-        through the one-shot peer-memory kernel (peer.PeerAllReduce)."""
-        from .peer import PeerAllReduce
+        through a one-shot kernel: "peer" = peer-memory reads (peer.PeerAllReduce),
+        "nvls" = in-switch reduction over NVSwitch multicast memory
+        (peer.NvlsAllReduce)."""
+        from .peer import NvlsAllReduce, PeerAllReduce
 
+        cls = NvlsAllReduce if mode == "nvls" else PeerAllReduce
         if not hasattr(self, "peer_ar"):
             self.peer_ar = {}
         for kind in kinds:
             if self.size(kind) > 1 and kind not in self.peer_ar:
-                self.peer_ar[kind] = PeerAllReduce(n_max, torch.device("cuda", torch.cuda.current_device()),
-                                                   self._g(kind), self.groups[kind][0])
+                self.peer_ar[kind] = cls(n_max, torch.device("cuda", torch.cuda.current_device()), self._g(kind),
+                                         self.groups[kind][0])
 
     def uses_peer_allreduce(self, kind: str) -> bool:
         return kind in getattr(self, "peer_ar", {})

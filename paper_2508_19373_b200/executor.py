@@ -40,12 +40,16 @@ _SHARED_SIDE_STREAM_MAX_T = 512  # decode-size batches: shared expert on a side 
 
 
 def _maybe_peer_allreduce(comm) -> None:
-    """HAP_PEER_AR=1: decode-size all-reduces of this block's groups go through the
-    one-shot peer-memory kernel (graph capturable); opt-in until measured on a
-    multi-GPU box."""
+    """HAP_PEER_AR=1 / HAP_NVLS_AR=1: decode-size all-reduces of this block's
+    groups go through the one-shot peer-memory kernel or the NVLS in-switch
+    reduction (both graph capturable); opt-in until measured on a multi-GPU box."""
     import os
 
-    if comm is not None and comm.lay.n > 1 and os.environ.get("HAP_PEER_AR", "0") == "1":
+    if comm is None or comm.lay.n == 1:
+        return
+    if os.environ.get("HAP_NVLS_AR", "0") == "1":  # in-switch reduction (NVSwitch multicast)
+        comm.enable_peer_allreduce(["attn_tp_group", "exp_tp_group"], mode="nvls")
+    elif os.environ.get("HAP_PEER_AR", "0") == "1":
         comm.enable_peer_allreduce(["attn_tp_group", "exp_tp_group"])
 
 

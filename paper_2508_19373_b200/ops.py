@@ -491,3 +491,16 @@ def attn_decode_paged(qkv: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Ten
     check(st, "hap_attn_decode_paged")
     _count(3 if B else 0)
     return out
+
+
+def nvls_allreduce(inp: torch.Tensor, out: torch.Tensor, uc_base: int, mc_base: int, epoch: torch.Tensor,
+                   n_max: int, n_ranks: int, n_ctas: int) -> torch.Tensor:
+    """In-switch (NVLS multimem) all-reduce of a bf16 tensor; see hap_nvls_allreduce_bf16."""
+    lib = _lib.load()
+    _need(inp, "inp", BF16); _need(out, "out", BF16); _need(epoch, "epoch", torch.int32)
+    if not (inp.is_contiguous() and out.is_contiguous()):
+        raise ValueError("inp and out must be contiguous")
+    check(lib.hap_nvls_allreduce_bf16(inp.data_ptr(), out.data_ptr(), uc_base, mc_base, epoch.data_ptr(),
+                                      inp.numel(), n_max, n_ranks, n_ctas, _stream()), "hap_nvls_allreduce_bf16")
+    _count(1 if inp.numel() else 0)
+    return out

@@ -192,3 +192,142 @@ class PeerEP:
     def close(self) -> None:
         for b in (self.segs, self.recv, self.y, self.sig):
             b.close()
+
+
+def _drv_check(res):
+    """cuda.bindings.driver calls return (CUresult, *values)."""
+    from cuda.bindings import driver as drv
+
+    err, *vals = res if isinstance(res, tuple) else (res,)
+    if err != drv.CUresult.CUDA_SUCCESS:
+        raise RuntimeError(f"CUDA driver call failed: {err}")
+    return vals[0] if len(vals) == 1 else (tuple(vals) if vals else None)
+
+
+def nvls_supported(device: int, n_devices: int = 1) -> bool:
+    """True when a multicast object can actually be created here: the device
+    attribute alone is not enough — a B200 without an NVSwitch fabric reports
+    CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 1 yet cuMulticastCreate fails
+    with CUDA_ERROR_INVALID_VALUE (this run's one-GPU boxes)."""
+    try:
+        from cuda.bindings import driver as drv
+
+        _drv_check(drv.cuInit(0))
+        dev = _drv_check(drv.cuDeviceGet(device))
+        attr = drv.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED
+        if not _drv_check(drv.cuDeviceGetAttribute(attr, dev)):
+            return False
+        prop = drv.CUmulticastObjectProp()
+        prop.numDevices = n_devices
+        prop.handleTypes = drv.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_FABRIC
+        prop.flags = 0
+        prop.size = 2 << 20
+        prop.size = _drv_check(drv.cuMulticastGetGranularity(
+            prop, drv.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED))
+        handle = _drv_check(drv.cuMulticastCreate(prop))
+        drv.cuMemRelease(handle)
+        return True
+    except Exception:  # noqa: BLE001 - no driver bindings / no multicast fabric: not supported
+        return False
+
+
+class NvlsAllReduce:
+    """One-shot all-reduce through NVLink SHARP (HAP_NVLS_AR=1): one physical
+    allocation per device bound to an NVSwitch multicast object
+    (cuMulticastCreate / AddDevice / BindMem; the object travels between the
+    ranks as a fabric handle), a unicast and a multicast mapping of it, and
+    hap_nvls_allreduce_bf16 reducing in the switch (multimem.ld_reduce).  The
+    caller (not the kernel library) owns every allocation, as the C ABI asks."""
+
+    def __init__(self, n_max: int, device, group, group_ranks: List[int], n_ctas: int = 32):
+        from cuda.bindings import driver as drv
+
+        from . import _lib
+
+        if n_max % 8:
+            raise ValueError("n_max must be a multiple of 8")
+        self.n_max, self.n_ctas = n_max, n_ctas
+        self.n = len(group_ranks)
+        self.me = group_ranks.index(dist.get_rank()) if dist.is_initialized() else 0
+        dev_idx = torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device()
+        _drv_check(drv.cuInit(0))
+        cu_dev = _drv_check(drv.cuDeviceGet(dev_idx))
+        need = int(_lib.load().hap_nvls_allreduce_bytes(n_max, n_ctas))
+        fabric = drv.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_FABRIC
+        mcprop = drv.CUmulticastObjectProp()
+        mcprop.numDevices = self.n
+        # the object crosses processes as a fabric handle; a one-device group
+        # never exports it (a handle type is still required)
+        mcprop.handleTypes = fabric if self.n > 1 else \
+            drv.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+        mcprop.flags = 0
+        mcprop.size = need
+        gran = _drv_check(drv.cuMulticastGetGranularity(
+            mcprop, drv.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED))
+        size = (need + gran - 1) // gran * gran
+        mcprop.size = size
+        # the multicast object: created by the group's first rank, imported by the others
+        if self.me == 0:
+            self.mc_handle = _drv_check(drv.cuMulticastCreate(mcprop))
+            blob = bytes(_drv_check(drv.cuMemExportToShareableHandle(self.mc_handle, fabric, 0)).data) \
+                if self.n > 1 else b""
+        else:
+            blob = None
+        if self.n > 1:
+            objs = [blob]
+            dist.broadcast_object_list(objs, src=group_ranks[0], group=group)
+            if self.me != 0:
+                fh = drv.CUmemFabricHandle()
+                fh.data = objs[0]
+                self.mc_handle = _drv_check(drv.cuMemImportFromShareableHandle(fh, fabric))
+        _drv_check(drv.cuMulticastAddDevice(self.mc_handle, cu_dev))
+        if self.n > 1:
+            dist.barrier(group=group)  # every device joined before memory is bound
+        prop = drv.CUmemAllocationProp()
+        prop.type = drv.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+        prop.location.type = drv.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        prop.location.id = dev_idx
+        ugran = _drv_check(drv.cuMemGetAllocationGranularity(
+            prop, drv.CUmemAllocationGranularity_flags.CU_MEM_ALLOC_GRANULARITY_RECOMMENDED))
+        size = (size + ugran - 1) // ugran * ugran
+        self.size = size
+        self.mem = _drv_check(drv.cuMemCreate(size, prop, 0))
+        _drv_check(drv.cuMulticastBindMem(self.mc_handle, 0, self.mem, 0, size, 0))
+        access = drv.CUmemAccessDesc()
+        access.location.type = drv.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        access.location.id = dev_idx
+        access.flags = drv.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+        self.uc = _drv_check(drv.cuMemAddressReserve(size, max(gran, ugran), 0, 0))
+        _drv_check(drv.cuMemMap(self.uc, size, 0, self.mem, 0))
+        _drv_check(drv.cuMemSetAccess(self.uc, size, [access], 1))
+        self.mc = _drv_check(drv.cuMemAddressReserve(size, max(gran, ugran), 0, 0))
+        _drv_check(drv.cuMemMap(self.mc, size, 0, self.mc_handle, 0))
+        _drv_check(drv.cuMemSetAccess(self.mc, size, [access], 1))
+        _drv_check(drv.cuMemsetD8(self.uc, 0, size))  # flag counters start at zero
+        torch.cuda.synchronize()
+        if self.n > 1:
+            dist.barrier(group=group)
+        self.epoch = torch.zeros(n_ctas, dtype=torch.int32, device=torch.device("cuda", dev_idx))
+
+    def fits(self, t: torch.Tensor) -> bool:
+        return t.dtype == torch.bfloat16 and t.is_contiguous() and t.numel() % 8 == 0 and t.numel() <= self.n_max
+
+    def __call__(self, t: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
+        from . import ops
+
+        out = t if out is None else out
+        return ops.nvls_allreduce(t, out, int(self.uc), int(self.mc), self.epoch, self.n_max, self.n, self.n_ctas)
+
+    def close(self) -> None:
+        from cuda.bindings import driver as drv
+
+        if getattr(self, "mem", None) is None:
+            return
+        torch.cuda.synchronize()
+        for va in (self.uc, self.mc):
+            drv.cuMemUnmap(va, self.size)
+            drv.cuMemAddressFree(va, self.size)
+        drv.cuMulticastUnbind(self.mc_handle, drv.cuDeviceGet(self.epoch.device.index)[1], 0, self.size)
+        drv.cuMemRelease(self.mem)
+        drv.cuMemRelease(self.mc_handle)
+        self.mem = None
