@@ -64,6 +64,8 @@ struct Params {
   float theta;
   int32_t group_m;  // raster group (m-blocks; < 0: -group_m n-blocks, n fastest)
   uint64_t hint_a, hint_b;  // L2 cache policies of the A / B TMA loads
+  int32_t noload;           // diagnostics only (HAP_GEMM_NOLOAD): after the first ring fill, stages
+                            // complete without TMA loads (MMAs re-read stale smem; results invalid)
   int32_t st32;     // C rows 32-byte aligned: 32-byte stores in the store epilogue
   // split-K (small-M, weight-streaming shapes): each tile's K range is cut in
   // ksplit slices computed by different CTAs; slice ks writes its fp32
@@ -249,12 +251,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = tile0; u < total_units; u += tile_step) {
         const int t = u / ksplit, ks = u - t * ksplit;
         const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
-        const int b_row = c.g * p.N + c.n_blk * p.BN + (int)crank * bn_half;
-        const int a_row = c.m0 + (int)crank * BM;
+        // diagnostics (noload == 2): every tile streams the first tile's panels, so
+        // the operand traffic stays on L2 and DRAM is idle (results invalid)
+        const int b_row = p.noload == 2 ? (int)crank * bn_half : c.g * p.N + c.n_blk * p.BN + (int)crank * bn_half;
+        const int a_row = p.noload == 2 ? (int)crank * BM : c.m0 + (int)crank * BM;
         const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
         for (int kb = kb0; kb < kb1; ++kb) {
           const bool pre = u == tile0 && kb - kb0 < npre;  // B already in flight
           if (!pre) mbar_wait_spin(&empty_bar[stage], phase ^ 1);
+          if (p.noload == 1 && !(u == tile0 && kb - kb0 < kStages)) {  // diagnostics: tensor work without loads
+            if (kPair == 1 || leader) mbar_arrive(&full_bar[stage]);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (kPair == 1) {
             if (!pre) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
             tma_load_2d(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, p.hint_a);
@@ -764,6 +773,11 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
   }();
   p.hint_a = hints[0];
   p.hint_b = hints[1];
+  static const int noload = [] {
+    const char* e = getenv("HAP_GEMM_NOLOAD");  // diagnostics only: results are invalid
+    return e ? atoi(e) : 0;
+  }();
+  p.noload = noload;
   int64_t gm = l2_budget / (K * 2 * (raster_n ? (int64_t)p.BN : (int64_t)TM));
   p.group_m = (int32_t)(gm < 1 ? 1 : (gm > 1024 ? 1024 : gm));
   if (raster_n) p.group_m = -p.group_m;
