@@ -257,6 +257,19 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorM
 }
 
 // ---------------------------------------------------------------- cluster --
+// Pair-mode TMA load multicast to the CTAs in cta_mask: every destination
+// CTA's pair leader (peer bit cleared) receives the complete_tx bytes.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                                    int32_t c0, int32_t c1, uint16_t cta_mask,
+                                                    uint64_t cache_hint) {
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_leader), "h"(cta_mask), "r"(c0), "r"(c1), "l"(cache_hint)
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

@@ -19,6 +19,8 @@
 // projection term of attention_flops (arch.py:157-160).
 #include <cstdlib>
 
+#include <cstdio>
+
 #include "common.cuh"
 
 namespace hap {
@@ -138,19 +140,29 @@ __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x));
 // leader CTA issues the M=256 MMAs and multicasts the commits, each CTA's
 // epilogue drains its own 128 TMEM lanes.  Halving B per SM halves the
 // L2->SM operand traffic per FLOP for B.
-template <int kPair>
+// kMc == 2 (pair mode only): a cluster of two CTA pairs computes the tiles
+// (m, 2j) and (m, 2j+1) of one m-block; the pairs share the A rows, so each
+// CTA loads half of its 128-row A slice and multicasts it to the CTA of the
+// same pair rank in the other pair (A traffic from L2 halves: 25 % less
+// operand traffic per tile).  A stage is reused only after both pairs' MMAs
+// consumed it (empty barriers count one commit per pair leader).
+template <int kPair, int kMc>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
   constexpr int kStages = Geo<kPair>::kStages;
   constexpr int kBBytes = Geo<kPair>::kBBytes;
   constexpr int TM = BM * kPair;  // rows per tile
+  constexpr int kCl = kPair * kMc;  // CTAs per cluster
+  static_assert(kMc == 1 || kPair == 2, "A multicast is a pair-mode layout");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* smA = smem;
   uint8_t* smB = smem + kStages * kABytes;
-  const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0;
+  const uint32_t ccta = kCl > 1 ? cluster_ctarank() : 0;
+  const uint32_t crank = kPair == 2 ? (ccta & 1) : 0;  // rank inside the CTA pair
+  const int pr = kMc == 2 ? (int)(ccta >> 1) : 0;      // pair index inside the cluster
   const bool leader = crank == 0;
-  const int tile0 = blockIdx.x / kPair, tile_step = gridDim.x / kPair;
+  const int tile0 = blockIdx.x / kCl, tile_step = gridDim.x / kCl;
 
   __shared__ __align__(8) uint64_t full_bar[kStages];
   __shared__ __align__(8) uint64_t empty_bar[kStages];
@@ -166,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const int n_segs = p.n_segs;
   const int n_blocks = (p.N + p.BN - 1) / p.BN;
+  const int n_sblocks = (n_blocks + kMc - 1) / kMc;  // n-block groups a cluster covers (kMc n-blocks each)
   // PDL: a grouped GEMM's tile list comes from the predecessor (permute's seg),
   // so it waits first; a dense GEMM's does not, and its producer streams the
   // first weight stages before waiting (weights are never written).
@@ -190,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], kMc);  // one commit per pair leader reading this stage
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
@@ -208,13 +221,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int g = 0; g < n_segs; ++g) {
       tile_start_s[g] = acc;
       const int rows = seg_s[g + 1] - seg_s[g];
-      acc += ((rows + TM - 1) / TM) * n_blocks;
+      acc += ((rows + TM - 1) / TM) * n_sblocks;
     }
     tile_start_s[n_segs] = acc;
   }
   tc_fence_before();
   __syncthreads();
-  if (kPair == 2) cluster_sync();  // peer barriers initialised, TMEM allocated in both CTAs
+  if (kCl > 1) cluster_sync();  // peer barriers initialised, TMEM allocated in every CTA
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
   const int ksplit = p.ksplit;
@@ -233,8 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int npre = 0;
       if (dense && tile0 < total_units) {
         const int t = tile0 / ksplit, ks = tile0 - t * ksplit;
-        const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
-        const int b_row = c.g * p.N + c.n_blk * p.BN + (int)crank * bn_half;
+        const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_sblocks, p.group_m);
+        const int nb = min(c.n_blk * kMc + pr, n_blocks - 1);
+        const int b_row = c.g * p.N + nb * p.BN + (int)crank * bn_half;
         const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
         npre = min(kStages, kb1 - kb0);
         for (int i = 0; i < npre; ++i) {
@@ -250,11 +264,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (dense) pdl_wait();
       for (int u = tile0; u < total_units; u += tile_step) {
         const int t = u / ksplit, ks = u - t * ksplit;
-        const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
+        const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_sblocks, p.group_m);
+        const int nb = min(c.n_blk * kMc + pr, n_blocks - 1);  // an odd last n-block: pair 1 recomputes it
         // diagnostics (noload == 2): every tile streams the first tile's panels, so
         // the operand traffic stays on L2 and DRAM is idle (results invalid)
-        const int b_row = p.noload == 2 ? (int)crank * bn_half : c.g * p.N + c.n_blk * p.BN + (int)crank * bn_half;
-        const int a_row = p.noload == 2 ? (int)crank * BM : c.m0 + (int)crank * BM;
+        // (noload == 3: only A streams from its real rows; 4: only B)
+        const bool fix_b = p.noload == 2 || p.noload == 3, fix_a = p.noload == 2 || p.noload == 4;
+        const int b_row = fix_b ? (int)crank * bn_half : c.g * p.N + nb * p.BN + (int)crank * bn_half;
+        const int a_row = fix_a ? (int)crank * BM : c.m0 + (int)crank * BM;
         const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
         for (int kb = kb0; kb < kb1; ++kb) {
           const bool pre = u == tile0 && kb - kb0 < npre;  // B already in flight
@@ -270,7 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!pre) tma_load_2d(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, p.hint_b);
           } else {
             if (leader && !pre) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
-            tma_load_2d_pair(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, p.hint_a);
+            if (kMc == 2)  // this CTA's half of the A slice, to itself and its twin in the other pair
+              tma_load_2d_pair_mc(smA + stage * kABytes + pr * (kABytes / 2), &tmA, &full_bar[stage], kb * BK,
+                                  a_row + pr * (BM / 2), (uint16_t)((1u << crank) | (1u << (2 + crank))), p.hint_a);
+            else
+              tma_load_2d_pair(smA + stage * kABytes, &tmA, &full_bar[stage], kb * BK, a_row, p.hint_a);
             if (!pre)
               tma_load_2d_pair(smB + stage * kBBytes, &tmB, &full_bar[stage], kb * BK, b_row, p.hint_b);
           }
@@ -305,11 +326,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             else umma_bf16_ss_pair(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb != kb0) | (k != 0));
           }
           if (kPair == 1) umma_commit(&empty_bar[stage]);
-          else umma_commit_pair_mc(&empty_bar[stage], 0x3);  // frees the stage in both CTAs
+          else umma_commit_pair_mc(&empty_bar[stage], kMc == 2 ? 0xF : 0x3);  // frees the stage in every CTA that
+                                                                             // wrote into this pair's buffers
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         if (kPair == 1) umma_commit(&tfull_bar[acc]);
-        else umma_commit_pair_mc(&tfull_bar[acc], 0x3);
+        else umma_commit_pair_mc(&tfull_bar[acc], (uint16_t)(0x3u << (2 * pr)));
       }
     }
   } else if (warp >= 4) {
@@ -319,13 +341,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;
     for (int u = tile0; u < total_units; u += tile_step, ++it) {
       const int t = u / ksplit, ks = u - t * ksplit;
-      const TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_blocks, p.group_m);
+      TileCoord c = map_tile<TM>(t, tile_start_s, seg_s, group_s, n_segs, n_sblocks, p.group_m);
+      const bool dup = c.n_blk * kMc + pr >= n_blocks;  // pair 1's recomputed odd last n-block: no stores
+      c.n_blk = min(c.n_blk * kMc + pr, n_blocks - 1);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait_spin(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = c.m0 + (int)crank * BM + q * 32 + lane;
-      const bool row_ok = row < c.m_end;
+      const bool row_ok = row < c.m_end && !dup;
       const uint32_t t_row = tmem_base + acc * kAccCols + ((uint32_t)(q * 32) << 16);
       __nv_bfloat16* crow =
           p.seg_dst ? reinterpret_cast<__nv_bfloat16*>(p.seg_dst[c.s]) +
@@ -530,14 +554,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {  // accumulator drained by this warp -> the leader's MMA may reuse it
         if (kPair == 1) mbar_arrive(&tempty_bar[acc]);
-        else mbar_arrive_cluster(&tempty_bar[acc], 0);
+        else mbar_arrive_cluster(&tempty_bar[acc], ccta & ~1u);  // this pair's leader
       }
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (kPair == 2) cluster_sync();
+  if (kCl > 1) cluster_sync();
   if (warp == 2) {
     tc_fence_after();
     if (kPair == 2) tmem_dealloc_pair(tmem_base, 2 * kAccCols);
@@ -731,19 +755,21 @@ static void plan_split(Params& p, int64_t a_rows, int64_t K, int64_t N, int64_t 
   }
 }
 
-template <int kPair>
+template <int kPair, int kMc = 1>
 static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
                        int64_t n_groups, int64_t N, int64_t n_segs, void* stream) {
   constexpr int TM = BM * kPair;
+  constexpr int kCl = kPair * kMc;
   CUtensorMap tmA, tmB;
-  if (!encode_tmap_2d_bf16(&tmA, A, (uint64_t)K, (uint64_t)a_rows, (uint64_t)lda * 2, BK, BM, true))
+  if (!encode_tmap_2d_bf16(&tmA, A, (uint64_t)K, (uint64_t)a_rows, (uint64_t)lda * 2, BK, BM / kMc, true))
     return HAP_ERR_DRIVER;
   if (!encode_tmap_2d_bf16(&tmB, B, (uint64_t)K, (uint64_t)(n_groups * N), (uint64_t)K * 2, BK, p.BN / kPair,
                            true))
     return HAP_ERR_DRIVER;
   static int configured = 0;
   if (!configured) {
-    if (configure_smem((const void*)grouped_gemm_kernel<kPair>, Geo<kPair>::kSmemBytes) != 0) return HAP_ERR_LAUNCH;
+    if (configure_smem((const void*)grouped_gemm_kernel<kPair, kMc>, Geo<kPair>::kSmemBytes) != 0)
+      return HAP_ERR_LAUNCH;
     configured = 1;
   }
   // Upper bound on tiles without reading seg on the host.
@@ -781,10 +807,29 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
   int64_t gm = l2_budget / (K * 2 * (raster_n ? (int64_t)p.BN : (int64_t)TM));
   p.group_m = (int32_t)(gm < 1 ? 1 : (gm > 1024 ? 1024 : gm));
   if (raster_n) p.group_m = -p.group_m;
-  const int64_t max_tiles = ((a_rows + TM - 1) / TM + (n_segs - 1)) * n_blocks;
-  const int64_t max_units = kNumSMs / kPair;
+  const int64_t max_tiles = ((a_rows + TM - 1) / TM + (n_segs - 1)) * ((n_blocks + kMc - 1) / kMc);
+  // persistent grid = the clusters that can be co-resident (4-CTA clusters do
+  // not tile every GPC: 33 of them fit on 148 SMs, not 37)
+  static const int64_t max_units = [] {
+    if (kCl <= 2) return (int64_t)(kNumSMs / kCl);
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(kNumSMs);
+    q.blockDim = dim3(kThreads);
+    q.dynamicSmemBytes = Geo<kPair>::kSmemBytes;
+    cudaLaunchAttribute a{};
+    a.id = cudaLaunchAttributeClusterDimension;
+    a.val.clusterDim.x = kCl;
+    a.val.clusterDim.y = 1;
+    a.val.clusterDim.z = 1;
+    q.attrs = &a;
+    q.numAttrs = 1;
+    int n_cl = 0;
+    if (cudaOccupancyMaxActiveClusters(&n_cl, (void*)grouped_gemm_kernel<kPair, kMc>, &q) != cudaSuccess || n_cl < 1)
+      n_cl = kNumSMs / kCl;
+    return (int64_t)n_cl;
+  }();
   const int64_t units = max_tiles * p.ksplit;
-  const int grid = (int)((units < max_units ? units : max_units) * kPair);
+  const int grid = (int)((units < max_units ? units : max_units) * kCl);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -792,16 +837,31 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
   cfg.stream = reinterpret_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kPair;
+  attr[0].val.clusterDim.x = kCl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (pdl_enabled() || (pdl_mode() == 2 && p.seg == nullptr)) ? 2 : 1;
-  if (cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<kPair>, tmA, tmB, p) != cudaSuccess) return HAP_ERR_LAUNCH;
+  static const bool debug = getenv("HAP_GEMM_DEBUG") != nullptr;
+  if (debug) {
+    int n_cl = -1;
+    cudaOccupancyMaxActiveClusters(&n_cl, (void*)grouped_gemm_kernel<kPair, kMc>, &cfg);
+    fprintf(stderr, "[hap gemm] cluster %d: max active clusters %d, grid %d CTAs\n", kCl, n_cl, grid);
+  }
+  if (cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<kPair, kMc>, tmA, tmB, p) != cudaSuccess) return HAP_ERR_LAUNCH;
   HAP_CHECK_LAUNCH();
   return HAP_OK;
+}
+
+// A multicast across two CTA pairs (kMc = 2): HAP_GEMM_MC=1 (A/B switch)
+static bool a_multicast() {
+  static const bool on = [] {
+    const char* e = getenv("HAP_GEMM_MC");
+    return e && e[0] == '1' && !getenv("HAP_GEMM_NOLOAD");  // the load diagnostics are 1-pair layouts
+  }();
+  return on;
 }
 
 static int pair_mode() {
@@ -819,8 +879,11 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
   // when segments fill 256-row tiles (prefill); weight-streaming decode shapes
   // (a few rows per expert) keep 128-row single-CTA tiles.
   p.ksplit = 1;
-  if (pair_mode() && (p.BN / 2) % 8 == 0 && a_rows >= 256 * n_segs)
+  if (pair_mode() && (p.BN / 2) % 8 == 0 && a_rows >= 256 * n_segs) {
+    if (a_multicast() && (N + p.BN - 1) / p.BN >= 2)
+      return launch_impl<2, 2>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
     return launch_impl<2>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
+  }
   // Small-M weight streaming (decode projections, TP-sharded shapes): split K
   // over more CTAs when a workspace is supplied, then reduce + epilogue.
   // Only single-m-block launches split; the slice plan depends on (N, K, M) only
