@@ -16,13 +16,20 @@ import torch
 from paper_2508_19373_b200 import ops
 
 secs = float(sys.argv[1]) if len(sys.argv) > 1 else 3.0
+which = sys.argv[2] if len(sys.argv) > 2 else "gate_up"
 E, h, I, rows = 8, 4096, 14336, 32768
 x = torch.randn(rows, h, device="cuda").to(torch.bfloat16)
 w13 = (torch.randn(E, 2 * I, h, device="cuda") * 0.02).to(torch.bfloat16)
 seg = torch.arange(0, rows + 1, rows // E, device="cuda", dtype=torch.int32)
 H = torch.empty(rows, I, device="cuda", dtype=torch.bfloat16)
 hw = ops.swiglu_half_width(I)
-fn = lambda: ops.grouped_gemm(x, w13, E, seg, H, swiglu_half=hw)  # noqa: E731
+w2 = (torch.randn(E, h, I, device="cuda") * 0.02).to(torch.bfloat16)
+Y = torch.empty(rows, h, device="cuda", dtype=torch.bfloat16)
+ops.grouped_gemm(x, w13, E, seg, H, swiglu_half=hw)
+if which == "down":
+    fn = lambda: ops.grouped_gemm(H, w2, E, seg, Y)  # noqa: E731
+else:
+    fn = lambda: ops.grouped_gemm(x, w13, E, seg, H, swiglu_half=hw)  # noqa: E731
 for _ in range(5):
     fn()
 torch.cuda.synchronize()
@@ -55,6 +62,7 @@ stop.set()
 th.join()
 ms = s.elapsed_time(e) / n
 late = samples[len(samples) // 3:]
-print(f"noload={os.environ.get('HAP_GEMM_NOLOAD', '0')}: {ms:.3f} ms/GEMM = {2 * rows * 2 * I * h / ms / 1e9:.0f} TF/s, "
+flops = 2 * rows * 2 * I * h if which == "gate_up" else 2 * rows * I * h
+print(f"{which} noload={os.environ.get('HAP_GEMM_NOLOAD', '0')}: {ms:.3f} ms/GEMM = {flops / ms / 1e9:.0f} TF/s, "
       f"SM clock median {statistics.median(c for c, _ in late):.0f} MHz, power median "
       f"{statistics.median(p for _, p in late):.0f} W ({len(late)} samples)")
