@@ -18,6 +18,11 @@ x = torch.randn(rows, h, device="cuda", generator=g).to(torch.bfloat16)
 w13 = (torch.randn(E, 2 * I, h, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
 w2 = (torch.randn(E, h, I, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
 seg = torch.arange(0, rows + 1, rows // E, device="cuda", dtype=torch.int32)
+if os.environ.get("SWEEP_RAGGED") == "1":  # segment sizes of a random top-2 routing (multinomial), not 4096 each
+    cnt = torch.bincount(torch.randint(0, E, (rows,), generator=torch.Generator().manual_seed(3)), minlength=E)
+    seg = torch.zeros(E + 1, dtype=torch.int32)
+    seg[1:] = torch.cumsum(cnt, 0)
+    seg = seg.to("cuda")
 hw = ops.swiglu_half_width(I)
 H = torch.empty(rows, I, device="cuda", dtype=torch.bfloat16)
 Y = torch.empty(rows, h, device="cuda", dtype=torch.bfloat16)
