@@ -271,8 +271,8 @@ constexpr int kGroupRows = 8;
 constexpr int kMaxRouterRows = 80;
 constexpr int64_t kGroupCntBytes = (int64_t)kSmallT * 4;
 
-template <int NE>
-__global__ void __launch_bounds__(kRanges * kGroupRows) router_group_kernel(
+template <int NE, int G>
+__global__ void __launch_bounds__(kRanges * G) router_group_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w, int T, int h, int n_rows_w, int E,
     int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
     float* __restrict__ shared_gate, float* __restrict__ logits_out, uint8_t* __restrict__ scratch) {
@@ -281,13 +281,13 @@ __global__ void __launch_bounds__(kRanges * kGroupRows) router_group_kernel(
   int* cnt_ws = reinterpret_cast<int*>(scratch);
   float* logits_ws = reinterpret_cast<float*>(scratch + kGroupCntBytes);
   extern __shared__ uint4 xs[];  // token row (h/8 vectors), then the group's (row, range) segments
-  __shared__ float part[kRanges][kGroupRows];
+  __shared__ float part[kRanges][G];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int last_s;
   const int t = blockIdx.x, g = blockIdx.y, n_groups = gridDim.y;
-  const int p = threadIdx.x / kGroupRows, el = threadIdx.x % kGroupRows, e = g * kGroupRows + el;
+  const int p = threadIdx.x / G, el = threadIdx.x % G, e = g * G + el;
   const int hr = h / kRanges, nv = hr / 8;
-  const int rows_here = min(kGroupRows, n_rows_w - g * kGroupRows);
+  const int rows_here = min(G, n_rows_w - g * G);
   // token row and this group's router rows arrive by 1D bulk copies in one
   // round trip; segments nv+1 vectors apart keep the threads' reads in
   // different banks
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kRanges * kGroupRows) router_group_kernel(
     bulk_load(xs, x + (int64_t)t * h, (uint32_t)(h * 2), &bar);
     for (int r = 0; r < rows_here * kRanges; ++r) {
       const int rl = r / kRanges, pp = r % kRanges;
-      bulk_load(ws + (rl * kRanges + pp) * (nv + 1), w + (int64_t)(g * kGroupRows + rl) * h + pp * hr,
+      bulk_load(ws + (rl * kRanges + pp) * (nv + 1), w + (int64_t)(g * G + rl) * h + pp * hr,
                 (uint32_t)(hr * 2), &bar);
     }
   }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kRanges * kGroupRows) router_group_kernel(
   }
   part[p][el] = acc;
   __syncthreads();
-  if (threadIdx.x < kGroupRows && e < n_rows_w) {
+  if (threadIdx.x < G && e < n_rows_w) {
     float s2 = part[0][el];
 #pragma unroll
     for (int pp = 1; pp < kRanges; ++pp) s2 = __fadd_rn(s2, part[pp][el]);
@@ -619,13 +619,23 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
     if (!stage && E + has_shared > kGroupRows && E + has_shared <= kMaxRouterRows && gs_bytes <= kStageLimit &&
         ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(ws)) & 15) == 0 &&
         ws && ws_bytes >= (size_t)(kGroupCntBytes + T * kMaxRouterRows * 4)) {
+      // router rows per CTA: 4 (default: twice the CTAs of 8, half the rows
+      // each — Qwen2-57B decode router 12.0 -> 9.7 us per call in a graph) or
+      // 8 (HAP_ROUTER_GROUP=8 A/B switch)
+      static const int grp = [] {
+        const char* e = getenv("HAP_ROUTER_GROUP");
+        return e && atoi(e) == 8 ? 8 : 4;
+      }();
+      auto gkern = grp == 4 ? router_group_kernel<NE, 4> : router_group_kernel<NE, kGroupRows>;
       static int configured_group = 0;
       if (!configured_group) {
-        if (configure_smem((const void*)router_group_kernel<NE>, kStageLimit)) return HAP_ERR_LAUNCH;
+        if (configure_smem((const void*)router_group_kernel<NE, 4>, kStageLimit) ||
+            configure_smem((const void*)router_group_kernel<NE, kGroupRows>, kStageLimit))
+          return HAP_ERR_LAUNCH;
         configured_group = 1;
       }
-      const int n_groups = (int)((E + has_shared + kGroupRows - 1) / kGroupRows);
-      { if (hap::launch_k(router_group_kernel<NE>, dim3((unsigned)T, (unsigned)n_groups), dim3(kRanges * kGroupRows),
+      const int n_groups = (int)((E + has_shared + grp - 1) / grp);
+      { if (hap::launch_k(gkern, dim3((unsigned)T, (unsigned)n_groups), dim3(kRanges * grp),
                           gs_bytes, st, reinterpret_cast<const __nv_bfloat16*>(x),
                           reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared), (int)E,
                           (int)k, renorm, has_shared, idx, tw, sg, logits,
