@@ -885,12 +885,199 @@ static int pair_mode() {
   return mode;
 }
 
+
+// ---- small-M weight streaming (decode) -------------------------------------
+// a_rows <= 8: every weight row is read once by one warp that dots it with all
+// the (<= 8) activation rows held in shared memory, 16-byte loads, 4 chunks in
+// flight per lane, fp32 accumulation per lane in k order then a fixed xor-
+// shuffle tree (deterministic).  A warp item is a PAIR of weight rows so every
+// epilogue closes inside the item: two output columns (store / bias /
+// residual), the gate and up rows of one SwiGLU column, or the columns i and
+// i + d/2 of one rotary head.  Grouped launches: items run over (segment,
+// column pair), rows of segment s dotted with weight group seg_group[s].
+// Replaces the 128-row tensor-core tile + split-K + reduce launches whose
+// fill / drain dominate decode projections (Qwen2-57B B=1 QKV: 15.5 + 6.8 us).
+constexpr int kGvThreads = 256;
+constexpr int kGvMaxRows = 8;
+constexpr int kGvU = 4;  // 16-byte chunks in flight per lane and weight row
+
+__device__ __forceinline__ void gv_dot8(const uint4 w, const uint4 x, float& acc) {
+  const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+  const uint32_t xx[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 a = unpack_bf16x2(ww[q]);
+    const float2 b = unpack_bf16x2(xx[q]);
+    acc = fmaf(a.x, b.x, acc);
+    acc = fmaf(a.y, b.y, acc);
+  }
+}
+
+__global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda,
+                                                          const __nv_bfloat16* __restrict__ B, Params p) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ uint4 xs[];  // [a_rows][K/8]
+  const int kv = p.K / 8;
+  for (int i = threadIdx.x; i < p.a_rows * kv; i += blockDim.x) {
+    const int r = i / kv, c = i - r * kv;
+    xs[i] = *reinterpret_cast<const uint4*>(A + (int64_t)r * lda + (int64_t)c * 8);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_pairs = p.epi == HAP_EPI_SWIGLU ? p.N / 2 : p.N / 2;  // column pairs per segment
+  const int n_items = p.n_segs * n_pairs;
+  const int d = p.head_dim, half = d >> 1;
+  for (int item = blockIdx.x * (kGvThreads / 32) + warp; item < n_items; item += gridDim.x * (kGvThreads / 32)) {
+    const int s = item / n_pairs, c2 = item - s * n_pairs;
+    const int r0 = p.seg ? p.seg[s] : 0, r1 = p.seg ? p.seg[s + 1] : p.a_rows;
+    if (r1 <= r0) continue;
+    const int g = p.seg_group ? p.seg_group[s] : s;
+    int na, nb;  // the two weight rows of this item
+    if (p.epi == HAP_EPI_SWIGLU) {
+      na = (c2 / p.hw) * 2 * p.hw + c2 % p.hw;
+      nb = na + p.hw;
+    } else if (p.epi == kEpiRope) {
+      na = (c2 / half) * d + c2 % half;
+      nb = na + half;
+    } else {
+      na = 2 * c2;
+      nb = na + 1;
+    }
+    const uint4* wa = reinterpret_cast<const uint4*>(B + ((int64_t)g * p.N + na) * p.K);
+    const uint4* wb = reinterpret_cast<const uint4*>(B + ((int64_t)g * p.N + nb) * p.K);
+    const int nr = r1 - r0;
+    float acc_a[kGvMaxRows], acc_b[kGvMaxRows];
+#pragma unroll
+    for (int m = 0; m < kGvMaxRows; ++m) acc_a[m] = acc_b[m] = 0.f;
+    // software-pipelined: the next group of chunks is in flight while this one
+    // is consumed (two groups = 8 KB per warp outstanding)
+    uint4 va[kGvU], vb[kGvU];
+#pragma unroll
+    for (int u = 0; u < kGvU; ++u) {
+      const int c = lane + 32 * u;
+      va[u] = c < kv ? __ldg(wa + c) : make_uint4(0, 0, 0, 0);
+      vb[u] = c < kv ? __ldg(wb + c) : make_uint4(0, 0, 0, 0);
+    }
+    for (int c0 = lane; c0 < kv; c0 += 32 * kGvU) {
+      uint4 na[kGvU], nb[kGvU];
+#pragma unroll
+      for (int u = 0; u < kGvU; ++u) {
+        const int c = c0 + 32 * (kGvU + u);
+        na[u] = c < kv ? __ldg(wa + c) : make_uint4(0, 0, 0, 0);
+        nb[u] = c < kv ? __ldg(wb + c) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kGvU; ++u) {
+        const int c = c0 + 32 * u;
+        if (c >= kv) break;
+#pragma unroll
+        for (int m = 0; m < kGvMaxRows; ++m) {
+          if (m < nr) {
+            const uint4 x = xs[(r0 + m) * kv + c];
+            gv_dot8(va[u], x, acc_a[m]);
+            gv_dot8(vb[u], x, acc_b[m]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kGvU; ++u) {
+        va[u] = na[u];
+        vb[u] = nb[u];
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kGvMaxRows; ++m) {
+      if (m < nr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          acc_a[m] += __shfl_xor_sync(0xffffffffu, acc_a[m], o);
+          acc_b[m] += __shfl_xor_sync(0xffffffffu, acc_b[m], o);
+        }
+      }
+    }
+    // epilogue: lane m writes row r0 + m
+#pragma unroll
+    for (int m = 0; m < kGvMaxRows; ++m) {
+      if (m != lane || m >= nr) continue;
+      const int row = r0 + m;
+      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+      float x1 = acc_a[m], x2 = acc_b[m];
+      if (p.epi == HAP_EPI_SWIGLU) {
+        crow[c2] = __float2bfloat16_rn(silu(x1) * x2);
+        continue;
+      }
+      if (p.bias) {
+        x1 += __bfloat162float(p.bias[na]);
+        x2 += __bfloat162float(p.bias[nb]);
+      }
+      if (p.epi == kEpiRope) {
+        if (na < p.rope_cols) {
+          const int i = c2 % half;
+          const float inv_freq = 1.0f / powf(p.theta, (float)(2 * i) / (float)d);
+          float sn, cs;
+          rope_sincos((float)p.positions[row] * inv_freq, &sn, &cs);
+          const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
+          x1 = y1;
+          x2 = y2;
+        }
+        crow[na] = __float2bfloat16_rn(x1);
+        crow[nb] = __float2bfloat16_rn(x2);
+        continue;
+      }
+      if (p.resid) {
+        x1 += __bfloat162float(p.resid[(int64_t)row * p.ldr + na]);
+        x2 += __bfloat162float(p.resid[(int64_t)row * p.ldr + nb]);
+      }
+      *reinterpret_cast<uint32_t*>(crow + na) = pack_bf16x2(x1, x2);
+    }
+  }
+}
+
+// HAP_GEMV (experiments; default 0 = tensor-core tiles for every M): 1 = GEMV
+// for decode launches streaming <= 64 MB of weights, 2 = for every eligible
+// decode launch.  Off by default: faster per launch at one activation row, but
+// the graph-replayed Qwen2-57B decode block got slower (profiles/r02_gemv_ab.txt)
+static int gemv_mode() {
+  static const int mode = [] {
+    const char* e = getenv("HAP_GEMV");
+    return e ? atoi(e) : 0;
+  }();
+  return mode;
+}
+
+static int launch_gemv(Params& p, const void* A, int64_t lda, const void* B, void* stream) {
+  const int smem = p.a_rows * p.K * 2;
+  static int configured = 0;
+  if (!configured) {
+    if (configure_smem((const void*)gemv_kernel, 200 * 1024)) return HAP_ERR_LAUNCH;
+    configured = 1;
+  }
+  const int64_t items = (int64_t)p.n_segs * (p.N / 2);
+  int64_t ctas = (items + (kGvThreads / 32) - 1) / (kGvThreads / 32);
+  const int per_sm = smem > 0 ? (int)((220 * 1024) / (smem + 1024)) : 8;
+  const int64_t cap = (int64_t)kNumSMs * (per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm));
+  if (ctas > cap) ctas = cap;
+  if (hap::launch_k(gemv_kernel, dim3((unsigned)ctas), dim3(kGvThreads), smem, reinterpret_cast<cudaStream_t>(stream),
+                    reinterpret_cast<const __nv_bfloat16*>(A), lda, reinterpret_cast<const __nv_bfloat16*>(B),
+                    p) != cudaSuccess)
+    return HAP_ERR_LAUNCH;
+  HAP_CHECK_LAUNCH();
+  return HAP_OK;
+}
+
 static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
                   int64_t n_groups, int64_t N, int64_t n_segs, void* ws, size_t ws_bytes, void* stream) {
   // CTA pairs need B split in two whole 8-row swizzle groups, and only pay off
   // when segments fill 256-row tiles (prefill); weight-streaming decode shapes
   // (a few rows per expert) keep 128-row single-CTA tiles.
   p.ksplit = 1;
+  // decode-size launches (<= 8 activation rows in all), HAP_GEMV=1|2: one warp
+  // per weight-row pair, no tensor-core tiles (see gemv_kernel / gemv_mode)
+  if (gemv_mode() > 0 && a_rows <= kGvMaxRows && p.seg_dst == nullptr && p.epi != HAP_EPI_F32 && p.N % 2 == 0 &&
+      a_rows * K * 2 <= 192 * 1024 && (p.epi != HAP_EPI_SWIGLU || p.hw > 0) &&
+      (gemv_mode() == 2 || n_groups * N * K * 2 <= (int64_t)64 << 20))
+    return launch_gemv(p, A, lda, B, stream);
   if (pair_mode() && (p.BN / 2) % 8 == 0 && a_rows >= 256 * n_segs) {
     if (a_multicast() && (N + p.BN - 1) / p.BN >= 2)
       return launch_impl<2, 2>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
