@@ -574,7 +574,7 @@ static int launch_decode(const __nv_bfloat16* q, int64_t ldqkv, __nv_bfloat16* k
                          const int32_t* pos, int64_t B, int64_t n_q_heads, int64_t n_kv_heads, float scale,
                          float* ws_o, float* ws_ml, int* ns_out, KvLayout L, uint64_t cache_rows, cudaStream_t st) {
   const int G = (int)(n_q_heads / n_kv_heads);
-  { if (hap::launch_k(kv_append_kernel<D>, dim3((unsigned)B), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, kc, vc, (int)max_len, pos, L) != cudaSuccess) return HAP_ERR_LAUNCH; }
+  { if (hap::launch_kr(B, kv_append_kernel<D>, dim3((unsigned)B), dim3(128), 0, st, q, ldqkv, (int)n_q_heads, (int)n_kv_heads, kc, vc, (int)max_len, pos, L) != cudaSuccess) return HAP_ERR_LAUNCH; }
   const float sl2 = scale * 1.4426950408889634f;
   int split, ns;
   plan_decode(B, n_kv_heads, max_len, &split, &ns);
@@ -595,7 +595,7 @@ static int launch_decode(const __nv_bfloat16* q, int64_t ldqkv, __nv_bfloat16* k
       if (configure_smem((const void*)decode_mma_kernel<D, GG>, smem) != 0) return HAP_ERR_LAUNCH;                \
       cfg = true;                                                                                                 \
     }                                                                                                             \
-    { if (hap::launch_k(decode_mma_kernel<D, GG>, dim3(grid), dim3(kDecWarps * 32), smem, st, tmK, tmV, q, ldqkv, (int)max_len, pos, (int)B,   \
+    { if (hap::launch_kr(B, decode_mma_kernel<D, GG>, dim3(grid), dim3(kDecWarps * 32), smem, st, tmK, tmV, q, ldqkv, (int)max_len, pos, (int)B,   \
                                                                  (int)n_q_heads, (int)n_kv_heads, sl2, ws_o,      \
                                                                  ws_ml, ns, split, L) != cudaSuccess) return HAP_ERR_LAUNCH; }                            \
     break;                                                                                                        \
@@ -645,12 +645,12 @@ static int attn_decode(const void* qkv, int64_t ldqkv, void* k_cache, void* v_ca
                                  : launch_decode<64>(q, ldqkv, kc, vc, max_len, pos, B, n_q_heads, n_kv_heads, scale, ws_o, ws_ml, &ns, L, cache_rows, st);
   if (rc != HAP_OK) return rc;
   if (ns > 32) {
-    if (hap::launch_k(decode_merge_wide_kernel, dim3((unsigned)(B * n_q_heads)), dim3(kWideMergeWarps * 32), 0, st,
+    if (hap::launch_kr(B, decode_merge_wide_kernel, dim3((unsigned)(B * n_q_heads)), dim3(kWideMergeWarps * 32), 0, st,
                       ws_o, ws_ml, ns, (int)n_q_heads, (int)head_dim, reinterpret_cast<__nv_bfloat16*>(out),
                       ldo) != cudaSuccess)
       return HAP_ERR_LAUNCH;
   } else {
-    if (hap::launch_k(decode_merge_kernel, dim3((unsigned)((B * n_q_heads + kMergeWarps - 1) / kMergeWarps)),
+    if (hap::launch_kr(B, decode_merge_kernel, dim3((unsigned)((B * n_q_heads + kMergeWarps - 1) / kMergeWarps)),
                       dim3(kMergeWarps * 32), 0, st, ws_o, ws_ml, ns, (int)n_q_heads, (int)B, (int)head_dim,
                       reinterpret_cast<__nv_bfloat16*>(out), ldo) != cudaSuccess)
       return HAP_ERR_LAUNCH;

@@ -448,7 +448,14 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 bool pdl_enabled();
-int pdl_mode();  // 0 off, 1 every launch, 2 dense GEMMs only (experiments)
+int pdl_mode();  // 0 off, 1 every launch, 2 dense GEMMs only (experiments), 3 decode-size launches (default)
+// decode-size launches (<= kPdlMaxRows tokens / permuted rows) are the
+// launch-latency-bound ones PDL helps; prefill launches measured slower with it
+constexpr int64_t kPdlMaxRows = 512;
+inline bool pdl_for(int64_t rows) {
+  const int m = pdl_mode();
+  return m == 1 || (m == 3 && rows <= kPdlMaxRows);
+}
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -463,6 +470,23 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// launch_k with PDL decided by the launch's row count (pdl_for)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kr(int64_t rows, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_for(rows) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

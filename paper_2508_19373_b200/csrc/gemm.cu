@@ -855,7 +855,7 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (pdl_enabled() || (pdl_mode() == 2 && p.seg == nullptr)) ? 2 : 1;
+  cfg.numAttrs = (pdl_for(a_rows) || (pdl_mode() == 2 && p.seg == nullptr)) ? 2 : 1;
   static const bool debug = getenv("HAP_GEMM_DEBUG") != nullptr;
   if (debug) {
     int n_cl = -1;
@@ -1058,7 +1058,7 @@ static int launch_gemv(Params& p, const void* A, int64_t lda, const void* B, voi
   const int per_sm = smem > 0 ? (int)((220 * 1024) / (smem + 1024)) : 8;
   const int64_t cap = (int64_t)kNumSMs * (per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm));
   if (ctas > cap) ctas = cap;
-  if (hap::launch_k(gemv_kernel, dim3((unsigned)ctas), dim3(kGvThreads), smem, reinterpret_cast<cudaStream_t>(stream),
+  if (hap::launch_kr(p.a_rows, gemv_kernel, dim3((unsigned)ctas), dim3(kGvThreads), smem, reinterpret_cast<cudaStream_t>(stream),
                     reinterpret_cast<const __nv_bfloat16*>(A), lda, reinterpret_cast<const __nv_bfloat16*>(B),
                     p) != cudaSuccess)
     return HAP_ERR_LAUNCH;
@@ -1095,7 +1095,7 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
   if (st != HAP_OK || p.ksplit == 1) return st;
   const int items = p.epi == HAP_EPI_STORE ? (int)(N / 8) : (int)(N / 16);
   const int64_t threads = a_rows * items;
-  { if (hap::launch_k(splitk_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0,
+  { if (hap::launch_kr(a_rows, splitk_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0,
                reinterpret_cast<cudaStream_t>(stream), p) != cudaSuccess)
     return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();

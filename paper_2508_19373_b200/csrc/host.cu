@@ -40,10 +40,13 @@ bool encode_tmap_2d_bf16_sw(CUtensorMap* map, const void* base, uint64_t inner, 
   return r == CUDA_SUCCESS;
 }
 
-// Off by default: on the graph-replayed Mixtral decode step PDL measured
-// 679 us vs 668 us without (scripts: 3 x 15 windows of 50 replays); the waiting
-// dependents' smem/TMEM reservations cost more than the launch gaps they hide.
-// HAP_PDL=1 turns it on for experiments.
+// HAP_PDL (experiments; default 0 = off): 1 every launch, 3 decode-size
+// launches only (pdl_for).  On every launch it measured +5.6 % on the
+// Mixtral-8x7B prefill block (the waiting dependents' smem/TMEM reservations
+// cost more than the launch gaps they hide there) and -4..-6 % on the Qwen2-57B
+// B=1 decode step before the shared expert moved to a side stream; on the
+// current decode graph the row-gated form measures +2 % at Qwen2-57B B=1 and
+// ±noise elsewhere (profiles/r02_pdl_ab.txt), so it stays off.
 int pdl_mode() {
   static int v = -1;
   if (v < 0) {

@@ -176,7 +176,7 @@ static int rmsnorm_launch(const void* x, int64_t T, int64_t h, int64_t ldx, cons
     const int vpt = (hv + kRowThreads - 1) / kRowThreads;
 #define HAP_ROW_CASE(V)                                                                                          \
   if (vpt <= V) {                                                                                               \
-    { if (hap::launch_k(rmsnorm_row_kernel<V>, dim3((unsigned)T), dim3(kRowThreads), 0, st, xv, (int)T, hv,    \
+    { if (hap::launch_kr(T, rmsnorm_row_kernel<V>, dim3((unsigned)T), dim3(kRowThreads), 0, st, xv, (int)T, hv,    \
                         (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8), dst_tab, n_dst) != cudaSuccess)           \
         return HAP_ERR_LAUNCH; }                                                                                \
     HAP_CHECK_LAUNCH();                                                                                         \
@@ -189,7 +189,7 @@ static int rmsnorm_launch(const void* x, int64_t T, int64_t h, int64_t ldx, cons
 #undef HAP_ROW_CASE
   }
 #define HAP_NORM_CASE(V) \
-  if (vpl <= V) { { if (hap::launch_k(rmsnorm_kernel<V>, dim3(grid), dim3(kThreads), 0, st, xv, (int)T, hv, (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8), dst_tab, n_dst) != cudaSuccess) return HAP_ERR_LAUNCH; } HAP_CHECK_LAUNCH(); return HAP_OK; }
+  if (vpl <= V) { { if (hap::launch_kr(T, rmsnorm_kernel<V>, dim3(grid), dim3(kThreads), 0, st, xv, (int)T, hv, (int)(ldx / 8), wv, eps, ov, (int)(ldo / 8), dst_tab, n_dst) != cudaSuccess) return HAP_ERR_LAUNCH; } HAP_CHECK_LAUNCH(); return HAP_OK; }
   HAP_NORM_CASE(2)
   HAP_NORM_CASE(4)
   HAP_NORM_CASE(8)

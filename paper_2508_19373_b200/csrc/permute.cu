@@ -398,14 +398,14 @@ extern "C" int hap_moe_permute(const int32_t* expert_of_row, int64_t R, int64_t 
     return HAP_OK;
   }
   const int smem = (int)((1 + kWarps) * E * sizeof(int32_t));
-  { if (hap::launch_k(rank_kernel, dim3((int)nb), dim3(kThreads), smem, st, expert_of_row, (int)R, E, local_rank, block_counts, block_base, seg) != cudaSuccess) return HAP_ERR_LAUNCH; }
+  { if (hap::launch_kr(R, rank_kernel, dim3((int)nb), dim3(kThreads), smem, st, expert_of_row, (int)R, E, local_rank, block_counts, block_base, seg) != cudaSuccess) return HAP_ERR_LAUNCH; }
   if (nb > 1) {  // one block computes the prefix itself
-    { if (hap::launch_k(scan_kernel, dim3(1), dim3(256), 0, st, block_counts, (int)nb, E, block_base, seg) != cudaSuccess) return HAP_ERR_LAUNCH; }
+    { if (hap::launch_kr(R, scan_kernel, dim3(1), dim3(256), 0, st, block_counts, (int)nb, E, block_base, seg) != cudaSuccess) return HAP_ERR_LAUNCH; }
   }
   const int64_t warps_needed = R;
   int grid = (int)((warps_needed * 32 + kThreads - 1) / kThreads);
   if (grid > 148 * 16) grid = 148 * 16;
-  { if (hap::launch_k(scatter_kernel, dim3(grid), dim3(kThreads), 0, st, expert_of_row, (int)R, E, local_rank, block_base,
+  { if (hap::launch_kr(R, scatter_kernel, dim3(grid), dim3(kThreads), 0, st, expert_of_row, (int)R, E, local_rank, block_base,
                                             reinterpret_cast<const uint4*>(x), (int)(src_row_div > 0 ? src_row_div : 1),
                                             (int)(h / 8), reinterpret_cast<uint4*>(x_out), dst_of_row) != cudaSuccess) return HAP_ERR_LAUNCH; }
   HAP_CHECK_LAUNCH();
@@ -429,7 +429,7 @@ static int combine_launch(const void* y, const int32_t* dst_of_row, const float*
   if (T >= 148 * kWarps) {  // enough tokens to fill the GPU with one warp per row
     int grid_r = (int)((T + kWarps - 1) / kWarps);
     if (grid_r > 148 * 16) grid_r = 148 * 16;
-    { if (hap::launch_k(combine_row_kernel, dim3(grid_r), dim3(kThreads), 0, st, reinterpret_cast<const uint4*>(y),
+    { if (hap::launch_kr(T, combine_row_kernel, dim3(grid_r), dim3(kThreads), 0, st, reinterpret_cast<const uint4*>(y),
                         dst_of_row, topk_w, (int)T, (int)k, (int)(h / 8), reinterpret_cast<const uint4*>(residual),
                         (int)res_row0, (int)res_rows, reinterpret_cast<const uint4*>(shared_y), shared_gate,
                         reinterpret_cast<uint4*>(out), out_tab, (int)chunk_rows, (int)slot) != cudaSuccess) return HAP_ERR_LAUNCH; }
@@ -439,7 +439,7 @@ static int combine_launch(const void* y, const int32_t* dst_of_row, const float*
   const int64_t items = T * ((h / 8 + 31) / 32);
   int grid = (int)((items * 32 + kThreads - 1) / kThreads);
   if (grid > 148 * 16) grid = 148 * 16;
-  { if (hap::launch_k(combine_kernel, dim3(grid), dim3(kThreads), 0, st, reinterpret_cast<const uint4*>(y), dst_of_row, topk_w, (int)T, (int)k,
+  { if (hap::launch_kr(T, combine_kernel, dim3(grid), dim3(kThreads), 0, st, reinterpret_cast<const uint4*>(y), dst_of_row, topk_w, (int)T, (int)k,
                                             (int)(h / 8), reinterpret_cast<const uint4*>(residual), (int)res_row0,
                                             (int)res_rows, reinterpret_cast<const uint4*>(shared_y), shared_gate,
                                             reinterpret_cast<uint4*>(out), out_tab, (int)chunk_rows, (int)slot) != cudaSuccess) return HAP_ERR_LAUNCH; }

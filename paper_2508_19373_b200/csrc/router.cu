@@ -635,7 +635,7 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
         configured_group = 1;
       }
       const int n_groups = (int)((E + has_shared + grp - 1) / grp);
-      { if (hap::launch_k(gkern, dim3((unsigned)T, (unsigned)n_groups), dim3(kRanges * grp),
+      { if (hap::launch_kr(T, gkern, dim3((unsigned)T, (unsigned)n_groups), dim3(kRanges * grp),
                           gs_bytes, st, reinterpret_cast<const __nv_bfloat16*>(x),
                           reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared), (int)E,
                           (int)k, renorm, has_shared, idx, tw, sg, logits,
@@ -644,7 +644,7 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
       return HAP_OK;
     }
     auto kern = stage ? router_small_kernel<NE, true> : router_small_kernel<NE, false>;
-    { if (hap::launch_k(kern, dim3((int)T), dim3(kRanges * NE), stage ? xs_bytes + ws_bytes : xs_bytes, st,
+    { if (hap::launch_kr(T, kern, dim3((int)T), dim3(kRanges * NE), stage ? xs_bytes + ws_bytes : xs_bytes, st,
         reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h,
         (int)(E + has_shared), (int)E, (int)k, renorm, has_shared, idx, tw, sg, logits) != cudaSuccess) return HAP_ERR_LAUNCH; }
     HAP_CHECK_LAUNCH();

@@ -22,4 +22,4 @@ for B in map(int, sys.argv[2:]):
     x = torch.randn(B, cfg.hidden, device="cuda").to(torch.bfloat16)
     graph, _ = blk.capture_graph(x, "decode", B, kv_cache=cache, positions=pos)
     out.append(f"B={B}: {timed(graph.replay, steps=100, warmup=20) * 1e3:.1f}us")
-print(f"gemv={os.environ.get('HAP_GEMV', '1')} {sys.argv[1]} " + ", ".join(out))
+print(f"gemv={os.environ.get('HAP_GEMV', '0')} pdl={os.environ.get('HAP_PDL', '0')} {sys.argv[1]} " + ", ".join(out))
