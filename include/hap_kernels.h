@@ -124,6 +124,15 @@ int hap_grouped_gemm_bf16_ex(const void* A, int64_t a_rows, int64_t lda, int64_t
 int hap_gemm_qkv_rope_ex(const void* A, int64_t M, int64_t lda, int64_t K, const void* W, int64_t N,
                          const void* bias, void* C, int64_t ldc, const int32_t* positions, int64_t n_rope_heads,
                          int64_t head_dim, float theta, void* workspace, size_t ws_bytes, void* stream);
+/* hap_grouped_gemm_bf16_ex on at most sm_budget SMs (0 = all): the persistent
+ * grid and the split-K plan are sized for that many SMs, leaving the rest to
+ * kernels on other streams — the executor runs the shared expert's decode
+ * GEMMs this way on a side stream beside the routed path (half the SMs). */
+int hap_grouped_gemm_bf16_sms(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                              int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
+                              const int32_t* seg_group, void* C, int64_t ldc, int32_t epilogue,
+                              int64_t swiglu_half, const void* bias, const void* residual, int64_t ldr,
+                              void* workspace, size_t ws_bytes, int32_t sm_budget, void* stream);
 
 /*
  * EP combine over peer memory: hap_grouped_gemm_bf16 with HAP_EPI_STORE whose

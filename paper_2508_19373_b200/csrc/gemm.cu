@@ -66,6 +66,7 @@ struct Params {
   float theta;
   int32_t group_m;  // raster group (m-blocks; < 0: -group_m n-blocks, n fastest)
   uint64_t hint_a, hint_b;  // L2 cache policies of the A / B TMA loads
+  int32_t sms;  // SM budget of the launch (persistent grid cap, split-K plan); 0 = all
   int32_t snake;            // serpentine n order across m-groups (HAP_GEMM_SNAKE)
   int32_t noload;           // diagnostics only (HAP_GEMM_NOLOAD): after the first ring fill, stages
                             // complete without TMA loads (MMAs re-read stale smem; results invalid)
@@ -588,35 +589,29 @@ static int pick_bn(int64_t N) {
 // order, then the same epilogue math as the TMEM path (bias, residual, SwiGLU,
 // RoPE with inv_freq = 1/theta^(2i/d)), one bf16 rounding.
 __device__ __forceinline__ void sum_slices8(const float* part, int64_t slice, int ks, int64_t off, float (&f)[8]) {
-  if (ks <= 4) {
-    // every slice's load in flight before the first add (one memory round
-    // trip instead of ks); the sum order is unchanged
-    float4 a[4], b[4];
+  // slices are loaded 8 at a time with every load in flight before the first
+  // add (ks/8 memory round trips instead of ks); the sum order is slice order
+  constexpr int kB = 8;
+  for (int s0 = 0; s0 < ks; s0 += kB) {
+    float4 a[kB], b[kB];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      if (s < ks) {
-        a[s] = __ldcg(reinterpret_cast<const float4*>(part + s * slice + off));
-        b[s] = __ldcg(reinterpret_cast<const float4*>(part + s * slice + off + 4));
+    for (int s = 0; s < kB; ++s) {
+      if (s0 + s < ks) {
+        a[s] = __ldcg(reinterpret_cast<const float4*>(part + (s0 + s) * slice + off));
+        b[s] = __ldcg(reinterpret_cast<const float4*>(part + (s0 + s) * slice + off + 4));
       }
     }
-    f[0] = a[0].x; f[1] = a[0].y; f[2] = a[0].z; f[3] = a[0].w;
-    f[4] = b[0].x; f[5] = b[0].y; f[6] = b[0].z; f[7] = b[0].w;
 #pragma unroll
-    for (int s = 1; s < 4; ++s) {
-      if (s < ks) {
+    for (int s = 0; s < kB; ++s) {
+      if (s0 + s >= ks) break;
+      if (s0 + s == 0) {
+        f[0] = a[0].x; f[1] = a[0].y; f[2] = a[0].z; f[3] = a[0].w;
+        f[4] = b[0].x; f[5] = b[0].y; f[6] = b[0].z; f[7] = b[0].w;
+      } else {
         f[0] += a[s].x; f[1] += a[s].y; f[2] += a[s].z; f[3] += a[s].w;
         f[4] += b[s].x; f[5] += b[s].y; f[6] += b[s].z; f[7] += b[s].w;
       }
     }
-    return;
-  }
-  float4 a = __ldcg(reinterpret_cast<const float4*>(part + off));
-  float4 b = __ldcg(reinterpret_cast<const float4*>(part + off + 4));
-  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-  for (int s = 1; s < ks; ++s) {
-    a = __ldcg(reinterpret_cast<const float4*>(part + s * slice + off));
-    b = __ldcg(reinterpret_cast<const float4*>(part + s * slice + off + 4));
-    f[0] += a.x; f[1] += a.y; f[2] += a.z; f[3] += a.w; f[4] += b.x; f[5] += b.y; f[6] += b.z; f[7] += b.w;
   }
 }
 
@@ -711,17 +706,18 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(Params p) {
 // preferring the larger tile; partials must fit the workspace.
 static void plan_split(Params& p, int64_t a_rows, int64_t K, int64_t N, int64_t n_segs, size_t ws_bytes) {
   p.ksplit = 1;
+  const int64_t nsm = p.sms > 0 ? p.sms : kNumSMs;
   auto tiles = [&](int64_t bn) { return ((a_rows + BM - 1) / BM + (n_segs - 1)) * ((N + bn - 1) / bn); };
   if (N % 8) return;
   const int64_t num_kb = (K + BK - 1) / BK;
-  if (2 * tiles(p.BN) > kNumSMs) {
+  if (2 * tiles(p.BN) > nsm) {
     // Many tiles, but a badly quantised last wave (e.g. 160 tiles = 1.08 waves
     // on 148 SMs: the weight stream takes two rounds).  A grouped launch has at
     // most min(rows, segments) non-empty segments, one m-block each here
     // (a_rows <= BM), which bounds its real tile count without a host sync.
     const int64_t n_blocks = (N + p.BN - 1) / p.BN;
     const int64_t t = (a_rows < n_segs ? a_rows : n_segs) * n_blocks;
-    auto rounds = [&](int64_t ks) { return (double)((t * ks + kNumSMs - 1) / kNumSMs) / (double)ks; };
+    auto rounds = [&](int64_t ks) { return (double)((t * ks + nsm - 1) / nsm) / (double)ks; };
     int64_t best = 1;
     for (int64_t ks = 2; ks <= 8 && ks <= num_kb / 4; ++ks)
       if ((size_t)ks * a_rows * N * sizeof(float) <= ws_bytes && rounds(ks) < rounds(best)) best = ks;
@@ -740,13 +736,13 @@ static void plan_split(Params& p, int64_t a_rows, int64_t K, int64_t N, int64_t 
   bool best_ok = false;
   for (int c = 0; c < nc; ++c) {
     const int64_t t = tiles(cands[c]);
-    int64_t ks = kNumSMs / t;
+    int64_t ks = nsm / t;
     if (ks > num_kb / 4) ks = num_kb / 4;  // >= 4 k-blocks (256 K) per slice
     if (ks > kSplitMax) ks = kSplitMax;
     while (ks > 1 && (size_t)ks * a_rows * N * sizeof(float) > ws_bytes) --ks;
     if (ks < 1) ks = 1;
     const int64_t units = t * ks;
-    const bool ok = units * 100 >= kNumSMs * 85;
+    const bool ok = units * 100 >= nsm * 85;
     if ((ok && (!best_ok || ks < best_ks)) || (!ok && !best_ok && units > best_units)) {
       best_bn = cands[c];
       best_ks = ks;
@@ -841,7 +837,8 @@ static int launch_impl(Params& p, const void* A, int64_t a_rows, int64_t lda, in
     return (int64_t)n_cl;
   }();
   const int64_t units = max_tiles * p.ksplit;
-  const int grid = (int)((units < max_units ? units : max_units) * kCl);
+  const int64_t cap_units = p.sms > 0 && p.sms / kCl < max_units ? (p.sms / kCl > 0 ? p.sms / kCl : 1) : max_units;
+  const int grid = (int)((units < cap_units ? units : cap_units) * kCl);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -1123,8 +1120,17 @@ extern "C" int hap_grouped_gemm_bf16_ex(const void* A, int64_t a_rows, int64_t l
                                         const int32_t* seg_group, void* C, int64_t ldc, int32_t epilogue,
                                         int64_t swiglu_half, const void* bias, const void* residual, int64_t ldr,
                                         void* workspace, size_t ws_bytes, void* stream) {
+  return hap_grouped_gemm_bf16_sms(A, a_rows, lda, K, B, n_groups, N, seg, n_segs, seg_group, C, ldc, epilogue,
+                                   swiglu_half, bias, residual, ldr, workspace, ws_bytes, 0, stream);
+}
+
+extern "C" int hap_grouped_gemm_bf16_sms(const void* A, int64_t a_rows, int64_t lda, int64_t K, const void* B,
+                                         int64_t n_groups, int64_t N, const int32_t* seg, int64_t n_segs,
+                                         const int32_t* seg_group, void* C, int64_t ldc, int32_t epilogue,
+                                         int64_t swiglu_half, const void* bias, const void* residual, int64_t ldr,
+                                         void* workspace, size_t ws_bytes, int32_t sm_budget, void* stream) {
   using namespace hap::gemm;
-  if (!A || !B || !C || a_rows < 0 || K <= 0 || N <= 0 || n_groups <= 0) return HAP_ERR_INVALID_ARG;
+  if (!A || !B || !C || a_rows < 0 || K <= 0 || N <= 0 || n_groups <= 0 || sm_budget < 0) return HAP_ERR_INVALID_ARG;
   if (!seg) n_segs = 1;
   if (n_segs <= 0 || n_segs > kMaxSegs) return HAP_ERR_INVALID_ARG;
   if (!seg_group && n_segs != n_groups && seg) return HAP_ERR_INVALID_ARG;
@@ -1144,6 +1150,7 @@ extern "C" int hap_grouped_gemm_bf16_ex(const void* A, int64_t a_rows, int64_t l
   p.seg = seg;
   p.C = reinterpret_cast<__nv_bfloat16*>(C);
   p.ldc = ldc;
+  p.sms = sm_budget < kNumSMs ? sm_budget : 0;
   if (epilogue == HAP_EPI_SWIGLU) {
     if (bias || residual) return HAP_ERR_UNSUPPORTED;
     if (swiglu_half <= 0 || swiglu_half > 128 || swiglu_half % 8 || N % (2 * swiglu_half))

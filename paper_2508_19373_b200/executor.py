@@ -23,6 +23,7 @@ collective schedule on gloo (see tests/test_executor_dist.py).
 
 from __future__ import annotations
 
+import os
 from contextlib import contextmanager
 from dataclasses import dataclass
 from typing import Optional
@@ -39,11 +40,18 @@ BF16 = torch.bfloat16
 _SHARED_SIDE_STREAM_MAX_T = 512  # decode-size batches: shared expert on a side stream
 
 
+def _shared_sm_budget(device) -> int:
+    """SMs the side-stream shared expert may use (half; HAP_SHARED_SMS overrides, 0 = all)."""
+    env = os.environ.get("HAP_SHARED_SMS")
+    if env is not None:
+        return int(env)
+    return torch.cuda.get_device_properties(device).multi_processor_count // 2
+
+
 def _maybe_peer_allreduce(comm) -> None:
     """HAP_PEER_AR=1 / HAP_NVLS_AR=1: decode-size all-reduces of this block's
     groups go through the one-shot peer-memory kernel or the NVLS in-switch
     reduction (both graph capturable); opt-in until measured on a multi-GPU box."""
-    import os
 
     if comm is None or comm.lay.n == 1:
         return
@@ -56,7 +64,6 @@ def _maybe_peer_allreduce(comm) -> None:
 def _boundary_peer_default() -> bool:
     """DP<->TP boundary pushed through peer memory (HAP_BOUNDARY_PEER=1) instead of
     NCCL AllGather + ReduceScatter; opt-in until measured on a multi-GPU box."""
-    import os
 
     return os.environ.get("HAP_BOUNDARY_PEER", "0") == "1"
 
@@ -64,7 +71,6 @@ def _boundary_peer_default() -> bool:
 def _ep_peer_default() -> bool:
     """EP dispatch/combine through peer-mapped buffers (HAP_EP_PEER=1) instead of
     NCCL all-to-alls; opt-in until measured on a multi-GPU box."""
-    import os
 
     return os.environ.get("HAP_EP_PEER", "0") == "1"
 
@@ -601,14 +607,18 @@ class HapMoEBlock:
         # shared expert (Qwen): independent of the routed path; on small (decode)
         # batches its weight-streaming GEMMs run on a side stream, concurrently
         # with router -> permute -> grouped GEMMs, so neither path's launch ramp
-        # and tail idle the HBM (fork/join by events: CUDA-graph capturable)
+        # and tail idle the HBM (fork/join by events: CUDA-graph capturable).
+        # They keep to half the SMs: unbounded, their persistent grids take every
+        # SM and the routed path waits for them (Qwen2-57B decode B=1
+        # 249 -> 226 us, B=2 316-348 -> 279-310 us, profiles/r02_shared_sms.txt)
         ys, side = None, None
         if cfg.n_shared:
             if hn_s.is_cuda and T <= _SHARED_SIDE_STREAM_MAX_T:
                 side = self._side_stream()
                 side.wait_stream(torch.cuda.current_stream())
+                sms = _shared_sm_budget(hn_s.device)
                 with torch.cuda.stream(side):
-                    ys = ops.gemm(ops.gemm(hn_s, w.ws13, swiglu_half=w.hw_s), w.ws2)
+                    ys = ops.gemm(ops.gemm(hn_s, w.ws13, swiglu_half=w.hw_s, sm_budget=sms), w.ws2, sm_budget=sms)
             else:
                 ys = ops.gemm(ops.gemm(hn_s, w.ws13, swiglu_half=w.hw_s), w.ws2)
         idx = torch.empty(T, k, device=dev, dtype=torch.int32)

@@ -96,11 +96,13 @@ def swiglu_half_width(inter: int) -> int:
 def grouped_gemm(a: torch.Tensor, b: torch.Tensor, n_groups: int, seg: Optional[torch.Tensor],
                  out: torch.Tensor, *, swiglu_half: int = 0, bias: Optional[torch.Tensor] = None,
                  residual: Optional[torch.Tensor] = None,
-                 seg_group: Optional[torch.Tensor] = None) -> torch.Tensor:
+                 seg_group: Optional[torch.Tensor] = None, sm_budget: int = 0) -> torch.Tensor:
     """out[r] = epi(a[r] @ b[g*N:(g+1)*N]^T) for rows r of segment s, g = seg_group[s] (tcgen05 kernel).
 
     A float32 ``out`` selects HAP_EPI_F32: the unrounded fp32 accumulators
-    (no bias / residual / SwiGLU), the fp32-accumulate parity check."""
+    (no bias / residual / SwiGLU), the fp32-accumulate parity check.
+    ``sm_budget`` > 0 keeps the launch on at most that many SMs
+    (hap_grouped_gemm_bf16_sms), for weight streams running beside others."""
     lib = _lib.load()
     f32 = out.dtype == torch.float32
     _need(a, "a", BF16); _need(b, "b", BF16); _need(out, "out", torch.float32 if f32 else BF16)
@@ -134,12 +136,12 @@ def grouped_gemm(a: torch.Tensor, b: torch.Tensor, n_groups: int, seg: Optional[
     if bias is not None:
         _need(bias, "bias", BF16)
     ws, ws_bytes = splitk_workspace(a.device)
-    st = lib.hap_grouped_gemm_bf16_ex(a.data_ptr(), a.shape[0], a.stride(0), K, b2.data_ptr(), n_groups, N,
-                                      _ptr(seg), n_segs, _ptr(seg_group), out.data_ptr(), out.stride(0), epi,
-                                      int(swiglu_half),
-                                      _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0,
-                                      ws or None, ws_bytes, _stream())
-    check(st, "hap_grouped_gemm_bf16_ex")
+    st = lib.hap_grouped_gemm_bf16_sms(a.data_ptr(), a.shape[0], a.stride(0), K, b2.data_ptr(), n_groups, N,
+                                       _ptr(seg), n_segs, _ptr(seg_group), out.data_ptr(), out.stride(0), epi,
+                                       int(swiglu_half),
+                                       _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0,
+                                       ws or None, ws_bytes, int(sm_budget), _stream())
+    check(st, "hap_grouped_gemm_bf16_sms")
     _count(1 if a.shape[0] else 0)
     return out
 
@@ -198,12 +200,13 @@ def peer_allreduce(in_ptrs: torch.Tensor, out_ptrs: torch.Tensor, epoch_ptrs: to
 
 
 def gemm(a: torch.Tensor, w: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None, residual=None,
-         swiglu_half: int = 0) -> torch.Tensor:
+         swiglu_half: int = 0, sm_budget: int = 0) -> torch.Tensor:
     """Dense a @ w^T (nn.Linear layout) on the tcgen05 kernel."""
     n_out = w.shape[0] // 2 if swiglu_half else w.shape[0]
     if out is None:
         out = torch.empty(a.shape[0], n_out, device=a.device, dtype=BF16)
-    return grouped_gemm(a, w, 1, None, out, swiglu_half=swiglu_half, bias=bias, residual=residual)
+    return grouped_gemm(a, w, 1, None, out, swiglu_half=swiglu_half, bias=bias, residual=residual,
+                        sm_budget=sm_budget)
 
 
 def gemm_qkv_rope(a: torch.Tensor, w: torch.Tensor, positions: torch.Tensor, n_rope_heads: int, head_dim: int,

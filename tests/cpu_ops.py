@@ -32,7 +32,7 @@ class CpuOps:
         return out
 
     @staticmethod
-    def gemm(a, w, out=None, *, bias=None, residual=None, swiglu_half=0):
+    def gemm(a, w, out=None, *, bias=None, residual=None, swiglu_half=0, sm_budget=0):
         acc = a.float() @ w.float().t()
         if swiglu_half:
             acc = _swiglu_cols(acc, swiglu_half)
