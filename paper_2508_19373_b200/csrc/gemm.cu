@@ -1031,14 +1031,18 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
   }
 }
 
-// HAP_GEMV (experiments; default 0 = tensor-core tiles for every M): 1 = GEMV
-// for decode launches streaming <= 64 MB of weights, 2 = for every eligible
-// decode launch.  Off by default: faster per launch at one activation row, but
-// the graph-replayed Qwen2-57B decode block got slower (profiles/r02_gemv_ab.txt)
+// HAP_GEMV: 0 = tensor-core tiles for every M; 1 (default) = GEMV for launches
+// of <= 2 activation rows streaming <= 64 MB of weights (decode QKV / O at
+// batch 1-2); 2 = GEMV for every eligible launch of <= 8 rows (experiments).
+// Per launch from HBM the GEMV wins at 1-2 rows on those streams and loses on
+// the long expert streams and at 4-8 rows; in the graph-replayed decode block
+// it measured Qwen2-57B B=1 226 -> 215 us, Mixtral-8x7B B=1 223 -> 205 us once
+// the shared expert kept to half the SMs (profiles/r02_gemv_ab.txt)
+constexpr int64_t kGvAutoRows = 2;
 static int gemv_mode() {
   static const int mode = [] {
     const char* e = getenv("HAP_GEMV");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
   return mode;
 }
@@ -1073,7 +1077,7 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
   // per weight-row pair, no tensor-core tiles (see gemv_kernel / gemv_mode)
   if (gemv_mode() > 0 && a_rows <= kGvMaxRows && p.seg_dst == nullptr && p.epi != HAP_EPI_F32 && p.N % 2 == 0 &&
       a_rows * K * 2 <= 192 * 1024 && (p.epi != HAP_EPI_SWIGLU || p.hw > 0) &&
-      (gemv_mode() == 2 || n_groups * N * K * 2 <= (int64_t)64 << 20))
+      (gemv_mode() == 2 || (a_rows <= kGvAutoRows && n_groups * N * K * 2 <= (int64_t)64 << 20)))
     return launch_gemv(p, A, lda, B, stream);
   if (pair_mode() && (p.BN / 2) % 8 == 0 && a_rows >= 256 * n_segs) {
     if (a_multicast() && (N + p.BN - 1) / p.BN >= 2)

@@ -13,6 +13,7 @@ from paper_2508_19373_b200.config import get_config
 from paper_2508_19373_b200.executor import HapMoEBlock, KVCache
 from paper_2508_19373_b200.layout import PlanDegrees
 
+torch.manual_seed(0)  # same routing in every process
 cfg = get_config(sys.argv[1])
 blk = HapMoEBlock(cfg, PlanDegrees(1, 1, 1, 1), None)
 out = []
@@ -22,4 +23,4 @@ for B in map(int, sys.argv[2:]):
     x = torch.randn(B, cfg.hidden, device="cuda").to(torch.bfloat16)
     graph, _ = blk.capture_graph(x, "decode", B, kv_cache=cache, positions=pos)
     out.append(f"B={B}: {timed(graph.replay, steps=100, warmup=20) * 1e3:.1f}us")
-print(f"gemv={os.environ.get('HAP_GEMV', '0')} pdl={os.environ.get('HAP_PDL', '0')} {sys.argv[1]} " + ", ".join(out))
+print(f"gemv={os.environ.get('HAP_GEMV', '1')} pdl={os.environ.get('HAP_PDL', '0')} {sys.argv[1]} " + ", ".join(out))

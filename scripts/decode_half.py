@@ -15,6 +15,7 @@ from paper_2508_19373_b200.config import get_config
 from paper_2508_19373_b200.executor import HapMoEBlock, KVCache
 from paper_2508_19373_b200.layout import PlanDegrees
 
+torch.manual_seed(0)  # same routing in every process
 cfg = get_config(sys.argv[1])
 B = int(sys.argv[2])
 blk = HapMoEBlock(cfg, PlanDegrees(1, 1, 1, 1), None)
@@ -42,5 +43,5 @@ with torch.cuda.graph(g):
     blk._experts(hn, x, res_row0=0, res_rows=B)
 res["expert_half"] = timed(g.replay, steps=100, warmup=20)
 tag = os.environ.get("TAG", "")
-print(f"{tag} gemv={os.environ.get('HAP_GEMV', '0')} {sys.argv[1]} B={B}: " +
+print(f"{tag} gemv={os.environ.get('HAP_GEMV', '1')} {sys.argv[1]} B={B}: " +
       ", ".join(f"{k} {v * 1e3:.1f}us" for k, v in res.items()))
