@@ -160,6 +160,86 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const int32_t* __rest
   }
 }
 
+// Decode-size permute (R <= kRowsPerBlock): rank and scatter in ONE launch.
+// Every CTA recomputes the stable ranks of all R rows in shared memory (the
+// same per-warp __match_any_sync ranks combined in row order as rank_kernel,
+// so dst_of_row / seg are identical), CTA 0 writes seg, and the warps of all
+// CTAs then copy their rows.  Saves the rank launch on the decode critical
+// path; R is at most 512 ids (2 KB), so the redundant ranking is cheap.
+__global__ void __launch_bounds__(kThreads) permute_small_kernel(const int32_t* __restrict__ eid, int R, int E,
+                                                                 const uint4* __restrict__ x, int src_div, int hv,
+                                                                 uint4* __restrict__ x_out,
+                                                                 int32_t* __restrict__ dst_of_row,
+                                                                 int32_t* __restrict__ seg) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ int32_t sm[];
+  int32_t* running = sm;                   // [E] -> exclusive bases after the scan
+  int32_t* warp_cnt = sm + E;              // [kWarps][E]
+  int32_t* rank_s = sm + (1 + kWarps) * E;  // [kRowsPerBlock]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < E; i += kThreads) running[i] = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int base = 0; base < R; base += kThreads) {
+    for (int i = threadIdx.x; i < kWarps * E; i += kThreads) warp_cnt[i] = 0;
+    __syncthreads();
+    const int r = base + threadIdx.x;
+    int e = -1;
+    if (r < R) {
+      e = eid[r];
+      if (e < 0 || e >= E) e = -1;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank_in_warp = __popc(peers & lt_mask);
+    if (e >= 0 && rank_in_warp == 0) warp_cnt[warp * E + e] = __popc(peers);
+    __syncthreads();
+    if (e >= 0) {
+      int off = running[e];
+      for (int w2 = 0; w2 < warp; ++w2) off += warp_cnt[w2 * E + e];
+      rank_s[r] = off + rank_in_warp;
+    } else if (r < R) {
+      rank_s[r] = -1;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < E; i += kThreads) {
+      int s2 = 0;
+      for (int w2 = 0; w2 < kWarps; ++w2) s2 += warp_cnt[w2 * E + i];
+      running[i] += s2;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {  // counts -> exclusive bases (and seg from CTA 0)
+    int acc = 0;
+    for (int e2 = 0; e2 < E; ++e2) {
+      const int c = running[e2];
+      running[e2] = acc;
+      if (blockIdx.x == 0) seg[e2] = acc;
+      acc += c;
+    }
+    if (blockIdx.x == 0) seg[E] = acc;
+  }
+  __syncthreads();
+  const int n_warps = (gridDim.x * kThreads) >> 5;
+  for (int r = (blockIdx.x * kThreads + threadIdx.x) >> 5; r < R; r += n_warps) {
+    const int e2 = eid[r];
+    const int dst = (e2 >= 0 && e2 < E) ? running[e2] + rank_s[r] : -1;
+    if (lane == 0) dst_of_row[r] = dst;
+    if (dst >= 0 && x_out) {
+      const uint4* src = x + (int64_t)(r / src_div) * hv;
+      uint4* out = x_out + (int64_t)dst * hv;
+      int i = lane;
+      for (; i + 96 < hv; i += 128) {
+        const uint4 a = __ldg(src + i), b = __ldg(src + i + 32), c = __ldg(src + i + 64), d = __ldg(src + i + 96);
+        out[i] = a;
+        out[i + 32] = b;
+        out[i + 64] = c;
+        out[i + 96] = d;
+      }
+      for (; i < hv; i += 32) out[i] = __ldg(src + i);
+    }
+  }
+}
+
 // Large-T combine: one warp per token row; the k slot rows / weights are read
 // once per token and every lane streams its 16-byte column chunks of the k
 // expert outputs (+ shared output, + residual) with 4 chunks in flight, so a
@@ -373,6 +453,15 @@ extern "C" size_t hap_moe_permute_workspace_bytes(int64_t R, int64_t n_experts) 
   return ws_bytes(R, n_experts, nullptr);
 }
 
+// HAP_PERMUTE_SMALL=0 (A/B): decode-size permutes keep the rank + scatter pair
+static bool small_permute() {
+  static const bool on = [] {
+    const char* e = getenv("HAP_PERMUTE_SMALL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 extern "C" int hap_moe_permute(const int32_t* expert_of_row, int64_t R, int64_t n_experts, const void* x,
                                int64_t src_row_div, int64_t h, void* x_out, int32_t* dst_of_row, int32_t* seg,
                                void* workspace, size_t ws_size, void* stream) {
@@ -394,6 +483,16 @@ extern "C" int hap_moe_permute(const int32_t* expert_of_row, int64_t R, int64_t 
       reinterpret_cast<int32_t*>(w8 + align_up((size_t)R * 4, 256) + align_up((size_t)(nb > 0 ? nb : 1) * E * 4, 256));
   if (R == 0) {
     cudaMemsetAsync(seg, 0, sizeof(int32_t) * (E + 1), st);
+    HAP_CHECK_LAUNCH();
+    return HAP_OK;
+  }
+  if (nb == 1 && small_permute()) {  // decode-size: rank + scatter in one launch
+    const int smem_s = (int)(((1 + kWarps) * E + kRowsPerBlock) * sizeof(int32_t));
+    int grid_s = (int)((R * 32 + kThreads - 1) / kThreads);
+    if (!x_out) grid_s = 1;
+    { if (hap::launch_kr(R, permute_small_kernel, dim3(grid_s), dim3(kThreads), smem_s, st, expert_of_row, (int)R, E,
+                         reinterpret_cast<const uint4*>(x), (int)(src_row_div > 0 ? src_row_div : 1), (int)(h / 8),
+                         reinterpret_cast<uint4*>(x_out), dst_of_row, seg) != cudaSuccess) return HAP_ERR_LAUNCH; }
     HAP_CHECK_LAUNCH();
     return HAP_OK;
   }
