@@ -70,6 +70,26 @@ def test_gemm_splitk(M, N, Kd):
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
 
 
+@pytest.mark.parametrize("M,N,Kd,sms", [(1, 40960, 3584, 74), (8, 40960, 3584, 74), (64, 4096, 4096, 50),
+                                        (300, 1024, 2048, 16)])
+def test_gemm_sm_budget(M, N, Kd, sms):
+    """hap_grouped_gemm_bf16_sms: the persistent grid and the split-K plan sized
+    for a part of the GPU (the side-stream shared expert) give the same
+    product (vs fp64, vs the full-GPU launch; SwiGLU epilogue at the Qwen2-57B
+    shared-expert shape) and repeat bit for bit."""
+    ops = K()
+    a, b = bf16((M, Kd), seed=11), bf16((N, Kd), 0.03, seed=12)
+    hw = ops.swiglu_half_width(N // 2)
+    outs = [ops.gemm(a, b, swiglu_half=hw, sm_budget=sms) for _ in range(2)]
+    full = ops.gemm(a, b, swiglu_half=hw)
+    torch.cuda.synchronize()
+    y = (np32(a).astype(np.float64) @ np32(b).astype(np.float64).T).reshape(M, -1, 2, hw)
+    ref = (y[:, :, 0] / (1 + np.exp(-y[:, :, 0])) * y[:, :, 1]).reshape(M, -1)
+    assert rel_err(np32(outs[0]), ref) < 2e-2
+    assert rel_err(np32(outs[0]), np32(full)) < 1e-2
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_gemm_qkv_rope_splitk_decode_shape():
     """Mixtral decode QKV (64 x 4096 -> 6144, RoPE on 40 heads): split-K vs unsplit."""
     ops = K()
