@@ -10,7 +10,9 @@ MEASURED_PEAKS.json: prefill = the reference's algorithmic FLOPs
 (attention_flops + expert_flops, arch.py:145-178, causal score/value term
 halved) / dense bf16 peak; decode = algorithmic HBM bytes (experts touched,
 attention weights, KV cache, router) / copy bandwidth.  Multi-GPU plans of
-configs 3 and 5 are not measurable on a one-GPU box.
+configs 3 and 5 are not measurable on a one-GPU box; the
+Qwen2-57B decode sweep (config 4) runs B = 1..512 and records the decode plan
+the reference ILP re-selects for 8 GPUs beside each row.
 """
 import json
 import statistics
@@ -98,8 +100,17 @@ def main():
         prefill("qwen1.5-moe-a2.7b", 8, 2048, hbm, bf16, bf16s),
         prefill("mixtral-8x22b", 16, 4096, hbm, bf16, bf16s),
     ]
-    for B in (1, 8, 64, 512):
-        rows.append(decode("qwen2-57b-a14b", B, 2048, hbm, bf16, bf16s))
+    # config 4: the Qwen2-57B decode batch sweep 1-512; beside each row the
+    # decode plan the reference ILP re-selects for 8 B200s (roofline tables)
+    from paper_2508_19373_b200.plan import plan_for, stage_plan
+
+    qcfg = get_config("qwen2-57b-a14b")
+    for B in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512):
+        row = decode("qwen2-57b-a14b", B, 2048, hbm, bf16, bf16s)
+        sp = stage_plan(plan_for(qcfg, 8, B, 2048, 1), "decode")
+        row["plan_n8_roofline"] = (f"attn(tp={sp.attention.tp_degree},dp={sp.attention.dp_degree})"
+                                   f"+exp(tp={sp.expert.tp_degree},ep={sp.expert.ep_degree})")
+        rows.append(row)
     out = {"device": torch.cuda.get_device_name(0),
            "peaks": {"hbm_gbs": hbm, "bf16_tflops": bf16, "bf16_tflops_sustained": bf16s},
            "plan": "single device: attn(tp=1,dp=1)+exp(tp=1,ep=1)", "data": "synthetic, random-init bf16 weights",
