@@ -268,38 +268,53 @@ __device__ __forceinline__ void finish_token_warp(const float* __restrict__ lg, 
 // then float logits[T][kMaxRouterRows].  Concurrent launches need distinct
 // workspaces.
 constexpr int kGroupRows = 8;
+constexpr int kGroupTB = 8;        // tokens per CTA of the blocked wide router
+constexpr int kGroupTBMinT = 32;   // ... from this many tokens on (16: 9.8 -> 13.6 us)
 constexpr int kMaxRouterRows = 80;
 constexpr int64_t kGroupCntBytes = (int64_t)kSmallT * 4;
 
-template <int NE, int G>
-__global__ void __launch_bounds__(kRanges * G) router_group_kernel(
+// TB > 1: one CTA per (block of TB tokens, group of G router rows), warp w
+// taking token w of the block with the same (row, range) thread layout, so the
+// G router rows staged in shared memory serve TB tokens (mid-size decode
+// batches: Qwen2-57B T = 512 had 8704 one-warp CTAs each re-staging its rows;
+// kRanges * G threads per token, the first warp of each finishes it).
+// The block's last CTA finishes its TB tokens, one warp each; the block counter
+// is the workspace slot of its first token.
+template <int NE, int G, int TB>
+__global__ void __launch_bounds__(kRanges * G * TB) router_group_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w, int T, int h, int n_rows_w, int E,
     int top_k, int renorm, int has_shared, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
     float* __restrict__ shared_gate, float* __restrict__ logits_out, uint8_t* __restrict__ scratch) {
+  constexpr int kPer = kRanges * G;  // threads per token (a whole number of warps)
+  static_assert(kPer % 32 == 0, "kRanges * G must be a multiple of the warp size");
   pdl_trigger();
   pdl_wait();
   int* cnt_ws = reinterpret_cast<int*>(scratch);
   float* logits_ws = reinterpret_cast<float*>(scratch + kGroupCntBytes);
-  extern __shared__ uint4 xs[];  // token row (h/8 vectors), then the group's (row, range) segments
-  __shared__ float part[kRanges][G];
+  extern __shared__ uint4 xs[];  // TB token rows (h/8 vectors each), then the group's (row, range) segments
+  __shared__ float part[TB][kRanges][G];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int last_s;
-  const int t = blockIdx.x, g = blockIdx.y, n_groups = gridDim.y;
-  const int p = threadIdx.x / G, el = threadIdx.x % G, e = g * G + el;
+  const int t0 = blockIdx.x * TB, g = blockIdx.y, n_groups = gridDim.y;
+  const int tb = threadIdx.x / kPer, lt = threadIdx.x % kPer;
+  const int p = lt / G, el = lt % G, e = g * G + el;
+  const int t = t0 + tb;
+  const int n_tok = min(TB, T - t0);
   const int hr = h / kRanges, nv = hr / 8;
   const int rows_here = min(G, n_rows_w - g * G);
-  // token row and this group's router rows arrive by 1D bulk copies in one
+  // token rows and this group's router rows arrive by 1D bulk copies in one
   // round trip; segments nv+1 vectors apart keep the threads' reads in
   // different banks
-  uint4* ws = xs + h / 8;
+  uint4* ws = xs + TB * (h / 8);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_barrier_init();
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bar, (uint32_t)(h * 2) * (uint32_t)(1 + rows_here));
-    bulk_load(xs, x + (int64_t)t * h, (uint32_t)(h * 2), &bar);
+    mbar_arrive_expect_tx(&bar, (uint32_t)(h * 2) * (uint32_t)(n_tok + rows_here));
+    for (int i = 0; i < n_tok; ++i)
+      bulk_load(xs + i * (h / 8), x + (int64_t)(t0 + i) * h, (uint32_t)(h * 2), &bar);
     for (int r = 0; r < rows_here * kRanges; ++r) {
       const int rl = r / kRanges, pp = r % kRanges;
       bulk_load(ws + (rl * kRanges + pp) * (nv + 1), w + (int64_t)(g * G + rl) * h + pp * hr,
@@ -308,9 +323,9 @@ __global__ void __launch_bounds__(kRanges * G) router_group_kernel(
   }
   mbar_wait(&bar, 0);
   float acc = 0.f;
-  if (e < n_rows_w) {
+  if (e < n_rows_w && tb < n_tok) {
     const uint4* wr = ws + (el * kRanges + p) * (nv + 1);
-    const uint4* xr = xs + p * nv;
+    const uint4* xr = xs + tb * (h / 8) + p * nv;
 #pragma unroll 4
     for (int v = 0; v < nv; ++v) {
       const uint4 wv = wr[v];
@@ -326,21 +341,21 @@ __global__ void __launch_bounds__(kRanges * G) router_group_kernel(
       }
     }
   }
-  part[p][el] = acc;
+  part[tb][p][el] = acc;
   __syncthreads();
-  if (threadIdx.x < G && e < n_rows_w) {
-    float s2 = part[0][el];
+  if (lt < G && e < n_rows_w && tb < n_tok) {
+    float s2 = part[tb][0][el];
 #pragma unroll
-    for (int pp = 1; pp < kRanges; ++pp) s2 = __fadd_rn(s2, part[pp][el]);
+    for (int pp = 1; pp < kRanges; ++pp) s2 = __fadd_rn(s2, part[tb][pp][el]);
     logits_ws[(int64_t)t * kMaxRouterRows + e] = s2;
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last_s = atomicAdd(&cnt_ws[t], 1) == n_groups - 1;
+  if (threadIdx.x == 0) last_s = atomicAdd(&cnt_ws[t0], 1) == n_groups - 1;
   __syncthreads();
-  if (!last_s || threadIdx.x >= 32) return;
+  if (!last_s || tb >= n_tok || lt >= 32) return;
   __threadfence();
-  if (threadIdx.x == 0) cnt_ws[t] = 0;  // ready for the next launch
+  if (threadIdx.x == 0) cnt_ws[t0] = 0;  // ready for the next launch
   finish_token_warp(logits_ws + (int64_t)t * kMaxRouterRows, n_rows_w, t, E, top_k, renorm, has_shared, topk_idx,
                     topk_w, shared_gate, logits_out);
 }
@@ -597,7 +612,15 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
     if (configure_smem((const void*)router_kernel<NE>, smem)) return HAP_ERR_LAUNCH;
     configured = 1;
   }
-  if (T <= kSmallT) {
+  // wide routers (more rows than one group) leave the per-token kernels for
+  // the TMA-staged token-block kernel above wide_max_t tokens (A/B switch
+  // HAP_ROUTER_WIDE_MAXT; logits are bit-identical across the variants)
+  static const int64_t wide_max_t = [] {
+    const char* e = getenv("HAP_ROUTER_WIDE_MAXT");
+    return e ? (int64_t)atoi(e) : (int64_t)kSmallT;
+  }();
+  const bool wide_to_tma = E + has_shared > kGroupRows && T > wide_max_t && h % (kRanges * 32) == 0;
+  if (T <= kSmallT && !wide_to_tma) {
     const int xs_bytes = (int)(h / 8) * 16;
     const int ws_bytes = (int)((E + has_shared) * kRanges) * (int)(h / kRanges / 8 + 1) * 16;
     constexpr int kStageLimit = 200 * 1024;
@@ -626,17 +649,28 @@ static int launch(const void* x, int64_t T, int64_t h, const void* w, int64_t E,
         const char* e = getenv("HAP_ROUTER_GROUP");
         return e && atoi(e) == 8 ? 8 : 4;
       }();
-      auto gkern = grp == 4 ? router_group_kernel<NE, 4> : router_group_kernel<NE, kGroupRows>;
+      // token blocks of kGroupTB tokens per CTA from kGroupTBMinT tokens on
+      // (HAP_ROUTER_TB=0 A/B switch keeps one token per CTA)
+      static const bool tb_ok = [] {
+        const char* e = getenv("HAP_ROUTER_TB");
+        return !(e && e[0] == '0');
+      }();
+      const int gtb_bytes = kGroupTB * xs_bytes + 4 * kRanges * (int)(h / kRanges / 8 + 1) * 16;
+      const bool blocked = tb_ok && grp == 4 && T >= kGroupTBMinT && gtb_bytes <= kStageLimit;
+      auto gkern = blocked ? router_group_kernel<NE, 4, kGroupTB>
+                           : (grp == 4 ? router_group_kernel<NE, 4, 1> : router_group_kernel<NE, kGroupRows, 1>);
       static int configured_group = 0;
       if (!configured_group) {
-        if (configure_smem((const void*)router_group_kernel<NE, 4>, kStageLimit) ||
-            configure_smem((const void*)router_group_kernel<NE, kGroupRows>, kStageLimit))
+        if (configure_smem((const void*)router_group_kernel<NE, 4, 1>, kStageLimit) ||
+            configure_smem((const void*)router_group_kernel<NE, 4, kGroupTB>, kStageLimit) ||
+            configure_smem((const void*)router_group_kernel<NE, kGroupRows, 1>, kStageLimit))
           return HAP_ERR_LAUNCH;
         configured_group = 1;
       }
       const int n_groups = (int)((E + has_shared + grp - 1) / grp);
-      { if (hap::launch_kr(T, gkern, dim3((unsigned)T, (unsigned)n_groups), dim3(kRanges * grp),
-                          gs_bytes, st, reinterpret_cast<const __nv_bfloat16*>(x),
+      const int tb = blocked ? kGroupTB : 1;
+      { if (hap::launch_kr(T, gkern, dim3((unsigned)((T + tb - 1) / tb), (unsigned)n_groups), dim3(kRanges * grp * tb),
+                          blocked ? gtb_bytes : gs_bytes, st, reinterpret_cast<const __nv_bfloat16*>(x),
                           reinterpret_cast<const __nv_bfloat16*>(w), (int)T, (int)h, (int)(E + has_shared), (int)E,
                           (int)k, renorm, has_shared, idx, tw, sg, logits,
                           reinterpret_cast<uint8_t*>(ws)) != cudaSuccess) return HAP_ERR_LAUNCH; }

@@ -32,4 +32,4 @@ for _ in range(10):
     g.replay()
 e.record()
 torch.cuda.synchronize()
-print(f"group={os.environ.get('HAP_ROUTER_GROUP', '8')} T={T}: {s.elapsed_time(e) / 200 * 1e3:.1f} us per router call (graph)")
+print(f"group={os.environ.get('HAP_ROUTER_GROUP', '4')} wide_maxt={os.environ.get('HAP_ROUTER_WIDE_MAXT', '-')} T={T}: {s.elapsed_time(e) / 200 * 1e3:.1f} us per router call (graph)")
