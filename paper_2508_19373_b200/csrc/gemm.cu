@@ -88,6 +88,7 @@ struct Params {
 constexpr int kEpiRope = 3;     // internal epilogue id (hap_gemm_qkv_rope)
 constexpr int64_t kSplitMax = 16;
 constexpr size_t kSplitWorkspaceBytes = (size_t)32 << 20;
+constexpr int64_t kSplitDenseMaxRows = 512;  // dense launches up to this many rows may split K
 constexpr int64_t kRasterL2Bytes = 48ll << 20;  // A rows of one raster group kept L2-resident across n-blocks
 
 struct TileCoord {
@@ -716,7 +717,8 @@ static void plan_split(Params& p, int64_t a_rows, int64_t K, int64_t N, int64_t 
     // most min(rows, segments) non-empty segments, one m-block each here
     // (a_rows <= BM), which bounds its real tile count without a host sync.
     const int64_t n_blocks = (N + p.BN - 1) / p.BN;
-    const int64_t t = (a_rows < n_segs ? a_rows : n_segs) * n_blocks;
+    const int64_t t = p.seg == nullptr ? ((a_rows + BM - 1) / BM) * n_blocks
+                                       : (a_rows < n_segs ? a_rows : n_segs) * n_blocks;
     auto rounds = [&](int64_t ks) { return (double)((t * ks + nsm - 1) / nsm) / (double)ks; };
     int64_t best = 1;
     for (int64_t ks = 2; ks <= 8 && ks <= num_kb / 4; ++ks)
@@ -1079,7 +1081,24 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
       a_rows * K * 2 <= 192 * 1024 && (p.epi != HAP_EPI_SWIGLU || p.hw > 0) &&
       (gemv_mode() == 2 || (a_rows <= kGvAutoRows && n_groups * N * K * 2 <= (int64_t)64 << 20)))
     return launch_gemv(p, A, lda, B, stream);
-  if (pair_mode() && (p.BN / 2) % 8 == 0 && a_rows >= 256 * n_segs) {
+  // Dense launches of a few hundred rows (decode at large batch: QKV / O at
+  // T = 512 are 36 / 28 pair tiles on 148 SMs) split K over 1-CTA tiles when
+  // that fills the GPU (HAP_GEMM_SPLIT_DENSE=0: A/B switch)
+  static const bool split_dense = [] {
+    const char* e = getenv("HAP_GEMM_SPLIT_DENSE");
+    return !(e && e[0] == '0');
+  }();
+  bool dense_split = false;
+  if (split_dense && ws && ws_bytes >= 16 && p.seg == nullptr && a_rows > BM && a_rows <= kSplitDenseMaxRows &&
+      p.epi != HAP_EPI_F32) {
+    Params q = p;
+    plan_split(q, a_rows, K, N, n_segs, ws_bytes);
+    if (q.ksplit > 1) {
+      p = q;
+      dense_split = true;
+    }
+  }
+  if (!dense_split && pair_mode() && (p.BN / 2) % 8 == 0 && a_rows >= 256 * n_segs) {
     if (a_multicast() && (N + p.BN - 1) / p.BN >= 2)
       return launch_impl<2, 2>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
     return launch_impl<2>(p, A, a_rows, lda, K, B, n_groups, N, n_segs, stream);
@@ -1088,7 +1107,9 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
   // over more CTAs when a workspace is supplied, then reduce + epilogue.
   // Only single-m-block launches split; the slice plan depends on (N, K, M) only
   // through the tile bound and the workspace fit, and repeats bit for bit.
-  if (ws && ws_bytes >= 16 && a_rows <= BM) {
+  if (dense_split) {
+    p.part = reinterpret_cast<float*>(ws);
+  } else if (ws && ws_bytes >= 16 && a_rows <= BM) {
     plan_split(p, a_rows, K, N, n_segs, ws_bytes);
     p.part = reinterpret_cast<float*>(ws);
   }
