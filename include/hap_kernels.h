@@ -391,6 +391,20 @@ int hap_attn_decode_paged(const void* qkv, int64_t ldqkv, void* k_pool, void* v_
 int hap_int4_dequant(const uint8_t* codes, const double* scales, const double* zero_points, int64_t group_size,
                      int64_t n, void* out, int32_t out_bf16, void* stream);
 
+/*
+ * Batched 2-D strided copy, one launch for up to any number of pieces.
+ * descs (HOST memory, read before return): n_descs records of 6 int64 —
+ * {src address, dst address, rows, row_bytes, src_pitch, dst_pitch} (bytes);
+ * row i of a record copies row_bytes from src + i*src_pitch to dst +
+ * i*dst_pitch.  Addresses, row_bytes and (rows > 1) pitches must be 16-byte
+ * aligned (HAP_ERR_MISALIGNED otherwise); source and destination bytes must
+ * not overlap; all records are validated before the first launch.
+ * Replaces: the local pack / unpack phases of the expert reshard whose
+ * volume the reference charges in reshard_volume (transition.py:153-177,
+ * Eq.6 T_reshard transition.py:241-267).
+ */
+int hap_copy2d_batched(const int64_t* descs, int64_t n_descs, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

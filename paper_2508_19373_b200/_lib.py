@@ -141,6 +141,7 @@ SIGNATURES = {
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int32, c_void_p],
     ),
     "hap_attn_decode_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int64]),
+    "hap_copy2d_batched": (ctypes.c_int, [c_void_p, c_int64, c_void_p]),
     "hap_kv_cache_fill_paged": (
         ctypes.c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int64,

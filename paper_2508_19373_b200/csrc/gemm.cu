@@ -1083,10 +1083,13 @@ static int launch(Params& p, const void* A, int64_t a_rows, int64_t lda, int64_t
     return launch_gemv(p, A, lda, B, stream);
   // Dense launches of a few hundred rows (decode at large batch: QKV / O at
   // T = 512 are 36 / 28 pair tiles on 148 SMs) split K over 1-CTA tiles when
-  // that fills the GPU (HAP_GEMM_SPLIT_DENSE=0: A/B switch)
+  // that fills the GPU.  Opt-in (HAP_GEMM_SPLIT_DENSE=1): the K split changes
+  // the fp32 summation order, so a 256-row prefill chunk would no longer be
+  // bit-identical to the same rows inside a larger launch
+  // (test_forward_host_streams_chunks_identically), for a gain within a few %
   static const bool split_dense = [] {
     const char* e = getenv("HAP_GEMM_SPLIT_DENSE");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   bool dense_split = false;
   if (split_dense && ws && ws_bytes >= 16 && p.seg == nullptr && a_rows > BM && a_rows <= kSplitDenseMaxRows &&

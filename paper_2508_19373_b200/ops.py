@@ -507,3 +507,58 @@ def nvls_allreduce(inp: torch.Tensor, out: torch.Tensor, uc_base: int, mc_base: 
                                       inp.numel(), n_max, n_ranks, n_ctas, _stream()), "hap_nvls_allreduce_bf16")
     _count(1 if inp.numel() else 0)
     return out
+
+
+def _rows_split(shape, strides_a, strides_b):
+    """(rows, row_elems, pitch_a, pitch_b) when both strided views of `shape`
+    are `rows` runs of `row_elems` contiguous elements at one uniform pitch
+    each (None otherwise).  Trailing dims merge into the row while both views
+    stay contiguous; the leading dims must collapse to a single stride."""
+    dims = [(s, a, b) for s, a, b in zip(shape, strides_a, strides_b) if s != 1]
+    if not dims:
+        return 1, 1, 1, 1
+    k, inner = len(dims), 1
+    while k > 0 and dims[k - 1][1] == inner and dims[k - 1][2] == inner:
+        inner *= dims[k - 1][0]
+        k -= 1
+    if k == 0:
+        return 1, inner, inner, inner
+    for i in range(k - 1):
+        s_next, a_next, b_next = dims[i + 1]
+        if dims[i][1] != a_next * s_next or dims[i][2] != b_next * s_next:
+            return None
+    rows = 1
+    for s, _, _ in dims[:k]:
+        rows *= s
+    return rows, inner, dims[k - 1][1], dims[k - 1][2]
+
+
+def copy_views(pairs) -> int:
+    """dst.copy_(src) for every (src, dst) pair of same-shape, same-dtype CUDA
+    views in ONE hap_copy2d_batched launch (each pair must be a uniform-pitch
+    stack of contiguous rows, 16-byte aligned; ValueError otherwise — there is
+    no per-pair fallback).  Returns the bytes moved."""
+    import numpy as np
+
+    lib = _lib.load()
+    recs, moved = [], 0
+    for src, dst in pairs:
+        _need(src, "src"); _need(dst, "dst", src.dtype)
+        if src.shape != dst.shape:
+            raise ValueError(f"shape mismatch {tuple(src.shape)} vs {tuple(dst.shape)}")
+        if src.numel() == 0:
+            continue
+        sp = _rows_split(src.shape, src.stride(), dst.stride())
+        if sp is None:
+            raise ValueError(f"views {tuple(src.stride())} / {tuple(dst.stride())} are not uniform-pitch row stacks")
+        rows, inner, ps, pd = sp
+        es = src.element_size()
+        recs.append((src.data_ptr(), dst.data_ptr(), rows, inner * es, ps * es, pd * es))
+        moved += rows * inner * es
+    if not recs:
+        return 0
+    arr = np.ascontiguousarray(np.array(recs, dtype=np.int64))
+    st = lib.hap_copy2d_batched(arr.ctypes.data, len(recs), _stream())
+    check(st, "hap_copy2d_batched")
+    _count(-(-len(recs) // 192))
+    return moved

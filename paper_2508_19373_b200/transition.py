@@ -154,6 +154,29 @@ def reshard_expert_weights(cfg, w, lay_src, lay_dst, group=None):
     return reshard_unpack(ctx, recv)
 
 
+def _piece_views(buf, per: int, h: int):
+    """A (unit, slice) piece on the wire: gate rows [per, h], up rows [per, h],
+    then the down projection's columns as stored in w2, [h, per] (so both
+    reshard phases copy row blocks and nothing is transposed)."""
+    n = per * h
+    return buf[:n].view(per, h), buf[n:2 * n].view(per, h), buf[2 * n:3 * n].view(h, per)
+
+
+def _run_copies(pairs) -> None:
+    """All the copies of one reshard phase: ONE hap_copy2d_batched launch for
+    device tensors; host tensors (the CPU gloo tests of the host logic) copy
+    pair by pair."""
+    if not pairs:
+        return
+    if pairs[0][0].is_cuda:
+        from . import ops
+
+        ops.copy_views(pairs)
+    else:
+        for src, dst in pairs:
+            dst.copy_(src)
+
+
 def reshard_pack(cfg, w, lay_src, lay_dst):
     """Phase 1 of the reshard: the send buffer (pieces this rank ships, grouped by
     destination) and the all-to-all splits; ctx carries what reshard_unpack needs."""
@@ -176,6 +199,7 @@ def reshard_pack(cfg, w, lay_src, lay_dst):
     unpacked = []  # per-unit contiguous (gate, up, down^T), built only if a piece misses the fast path
 
     def local_piece(unit, s):
+        """(gate [per,h], up [per,h], down [h,per]) views of a piece this rank holds."""
         if not unpacked:
             unpacked.append(_unpack(cfg, w))
         units = unpacked[0]
@@ -184,7 +208,8 @@ def reshard_pack(cfg, w, lay_src, lay_dst):
         else:
             u = units[(lay_src.experts[1] - e0) + (unit - cfg.n_experts)]
         k = s - s0
-        return torch.stack([t[k * per:(k + 1) * per] for t in u])  # [3, per, h]
+        g, up, dt = (t[k * per:(k + 1) * per] for t in u)
+        return g, up, dt.t()
 
     piece_elems = 3 * per * h
     order = [(uu, s) for r in range(n) for (uu, s) in sends[me][r]]
@@ -197,18 +222,20 @@ def reshard_pack(cfg, w, lay_src, lay_dst):
     def unit_index(unit):
         return unit - e0 if unit < cfg.n_experts else (lay_src.experts[1] - e0) + (unit - cfg.n_experts)
 
-    sv = send.view(len(order), 3, per, h)
+    pairs = []
     for i, (uu, sl) in enumerate(order):
         # each piece is written once, straight from the packed source layout
+        pg, pu, pd = _piece_views(send[i * piece_elems:(i + 1) * piece_elems], per, h)
         t13, base, hw_u, t2 = src_views[unit_index(uu)]
         r0 = base + (sl - s0) * per
         g, u_ = _gu_rows(t13, hw_u, r0, per, 0), _gu_rows(t13, hw_u, r0, per, 1)
         if g is None:
-            sv[i].copy_(local_piece(uu, sl))
+            lg, lu, ld = local_piece(uu, sl)
+            pairs += [(lg, pg), (lu, pu), (ld, pd)]
         else:
-            sv[i, 0].view(per // hw_u, hw_u, h).copy_(g)
-            sv[i, 1].view(per // hw_u, hw_u, h).copy_(u_)
-            sv[i, 2].copy_(t2[:, (sl - s0) * per:(sl - s0 + 1) * per].t())
+            pairs += [(g, pg.view(per // hw_u, hw_u, h)), (u_, pu.view(per // hw_u, hw_u, h)),
+                      (t2[:, (sl - s0) * per:(sl - s0 + 1) * per], pd)]
+    _run_copies(pairs)
     ctx = dict(cfg=cfg, w=w, lay_dst=lay_dst, n=n, me=me, per=per, h=h, own_src=own_src, sends=sends,
                local_piece=local_piece, piece_elems=piece_elems, src_views=src_views, unit_index=unit_index, s0=s0)
     return send, in_splits, out_splits, ctx
@@ -228,7 +255,7 @@ def reshard_unpack(ctx, recv):
     off = 0
     for q in range(n):
         for key in sends[q][me]:
-            received[key] = recv[off:off + piece_elems].view(3, per, h)
+            received[key] = _piece_views(recv[off:off + piece_elems], per, h)
             off += piece_elems
 
     def piece(key):
@@ -252,6 +279,7 @@ def reshard_unpack(ctx, recv):
         ws13 = torch.empty(2 * sil, h, dtype=dt, device=dev) if cfg.n_shared else None
         ws2 = torch.empty(h, sil, dtype=dt, device=dev) if cfg.n_shared else None
         src_views, unit_index, s0 = ctx["src_views"], ctx["unit_index"], ctx["s0"]
+        pairs = []
         for j, unit in enumerate(units_d):
             if unit < cfg.n_experts:
                 t13, base, hw_u, t2 = w13[j], 0, hw, w2[j]
@@ -268,24 +296,22 @@ def reshard_unpack(ctx, recv):
                     sr0 = sbase + (sl - s0) * per
                     sg, su = _gu_rows(st13, shw, sr0, per, 0), _gu_rows(st13, shw, sr0, per, 1)
                     if sg is not None:
-                        gd.copy_(sg)
-                        ud.copy_(su)
-                        dcols.copy_(st2[:, (sl - s0) * per:(sl - s0 + 1) * per])
+                        pairs += [(sg, gd), (su, ud), (st2[:, (sl - s0) * per:(sl - s0 + 1) * per], dcols)]
                         continue
-                pc = piece(key)
-                gd.copy_(pc[0].view(per // hw_u, hw_u, h))
-                ud.copy_(pc[1].view(per // hw_u, hw_u, h))
-                dcols.copy_(pc[2].t())
+                pg, pu, pd = piece(key)
+                pairs += [(pg.view(per // hw_u, hw_u, h), gd), (pu.view(per // hw_u, hw_u, h), ud), (pd, dcols)]
+        _run_copies(pairs)
         return dataclasses.replace(w, w13=w13, w2=w2, hw=hw, ws13=ws13, ws2=ws2, hw_s=hw_s,
                                    n_experts_local=El_d, inter_local=il, shared_inter_local=sil)
 
     def assemble(unit):
-        p = torch.cat([piece((unit, s)) for s in range(ds0, ds1)], dim=1)  # [3, il, h]
-        return p[0], p[1], p[2]
+        ps = [piece((unit, s)) for s in range(ds0, ds1)]
+        return (torch.cat([p[0] for p in ps]), torch.cat([p[1] for p in ps]),  # [il, h]
+                torch.cat([p[2] for p in ps], dim=1))                          # [h, il]
 
     rout = [assemble(e) for e in range(de0, de1)]
     w13 = interleave_gate_up(torch.stack([g for g, _, _ in rout]), torch.stack([u for _, u, _ in rout]), hw)
-    w2 = torch.stack([dn.t() for _, _, dn in rout]).contiguous()
+    w2 = torch.stack([dn for _, _, dn in rout]).contiguous()
     ws13 = ws2 = None
     hw_s, sil = 0, 0
     if cfg.n_shared:
@@ -295,7 +321,7 @@ def reshard_unpack(ctx, recv):
         sil = sg.shape[0]
         hw_s = swiglu_half_width(sil)
         ws13 = interleave_gate_up(sg, su, hw_s)
-        ws2 = torch.cat([dn for _, _, dn in sh]).t().contiguous()
+        ws2 = torch.cat([dn for _, _, dn in sh], dim=1).contiguous()
     return dataclasses.replace(w, w13=w13, w2=w2, hw=hw, ws13=ws13, ws2=ws2, hw_s=hw_s,
                                n_experts_local=de1 - de0, inter_local=il, shared_inter_local=sil)
 

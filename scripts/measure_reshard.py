@@ -23,6 +23,29 @@ from paper_2508_19373_b200.weights import pack_rank_weights, synthetic_weights
 NVLINK_BPS = 900e9  # NVLink 5, per direction per GPU (guide figure, not measured here: one-GPU box)
 
 
+KERNEL_MS = []
+TIME_KERNEL = [False]
+
+
+def _timed_copies(pairs):
+    """transition._run_copies with CUDA events around the one batched launch."""
+    from paper_2508_19373_b200 import ops
+
+    if not TIME_KERNEL[0]:
+        ORIG_RUN_COPIES(pairs)
+        return
+    if not pairs:
+        KERNEL_MS.append(0.0)
+        return
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(4_000_000)  # keep the GPU busy while the host builds the records: s..e is the kernel alone
+    s.record()
+    ops.copy_views(pairs)
+    e.record()
+    e.synchronize()
+    KERNEL_MS.append(s.elapsed_time(e))
+
+
 def timed(fn, reps=5):
     fn()
     torch.cuda.synchronize()
@@ -36,6 +59,11 @@ def timed(fn, reps=5):
 
 
 def main():
+    global ORIG_RUN_COPIES
+    import paper_2508_19373_b200.transition as tr
+
+    ORIG_RUN_COPIES = tr._run_copies
+    tr._run_copies = _timed_copies
     mpl = import_moeplan()
     cfg = get_config("mixtral-8x7b")
     spec = cfg.to_model_spec()
@@ -52,20 +80,37 @@ def main():
             t_pack, (send, ins, outs, ctx) = timed(lambda: reshard_pack(cfg, wi, li, lj))
             recv = torch.randn(sum(outs), device="cuda").to(torch.bfloat16)
             t_unpack, _ = timed(lambda: reshard_unpack(ctx, recv))
+            TIME_KERNEL[0] = True  # second pass: the batched copy launch alone
+            KERNEL_MS.clear()
+            timed(lambda: reshard_pack(cfg, wi, li, lj))
+            k_pack = sorted(KERNEL_MS)[len(KERNEL_MS) // 2]
+            KERNEL_MS.clear()
+            timed(lambda: reshard_unpack(ctx, recv))
+            k_unpack = sorted(KERNEL_MS)[len(KERNEL_MS) // 2]
+            TIME_KERNEL[0] = False
+            wj = reshard_unpack(ctx, recv)
+            dst_bytes = sum(t.numel() * 2 for t in (wj.w13, wj.w2, wj.ws13, wj.ws2) if t is not None)
             r = {"rank": rank, "pack_ms": t_pack * 1e3, "unpack_ms": t_unpack * 1e3,
-                 "send_bytes": send.numel() * 2, "recv_bytes": recv.numel() * 2}
+                 "send_bytes": send.numel() * 2, "recv_bytes": recv.numel() * 2,
+                 # HBM bytes each phase moves (read + write): the pieces shipped / the whole destination packing
+                 "pack_kernel_ms": k_pack, "unpack_kernel_ms": k_unpack,
+                 "pack_kernel_hbm_gbs": 2 * send.numel() * 2 / k_pack / 1e6 if k_pack else 0.0,
+                 "unpack_kernel_hbm_gbs": 2 * dst_bytes / k_unpack / 1e6}
             worst = r if worst is None or r["pack_ms"] + r["unpack_ms"] > worst["pack_ms"] + worst["unpack_ms"] else worst
         ref = mpl.reshard_volume(mpl.ExpertStrategy(tp_degree=src[0], ep_degree=src[1]),
                                  mpl.ExpertStrategy(tp_degree=dst[0], ep_degree=dst[1]), spec) / spec.n_layers
         rows.append({"switch": f"exp(tp={src[0]},ep={src[1]}) -> exp(tp={dst[0]},ep={dst[1]})", "n_gpus": N,
                      "reference_reshard_bytes_per_layer": ref, "recv_bytes_rank": worst["recv_bytes"],
                      "pack_ms": worst["pack_ms"], "unpack_ms": worst["unpack_ms"],
+                     "pack_kernel_ms": worst["pack_kernel_ms"], "unpack_kernel_ms": worst["unpack_kernel_ms"],
+                     "pack_kernel_hbm_gbs": worst["pack_kernel_hbm_gbs"],
+                     "unpack_kernel_hbm_gbs": worst["unpack_kernel_hbm_gbs"],
                      "transfer_ms_at_nvlink5": worst["recv_bytes"] / NVLINK_BPS * 1e3,
                      "t_reshard_ms_per_layer": worst["pack_ms"] + worst["unpack_ms"]
                      + worst["recv_bytes"] / NVLINK_BPS * 1e3,
                      "reference_t_reshard_ms_per_layer_at_nvlink5": ref / NVLINK_BPS * 1e3})
     out = {"workload": "Mixtral-8x7B, one layer's expert weights (1.41 G params bf16), N=8 layouts, worst of ranks 0/7",
-           "note": "pack/unpack measured on one B200 (CUDA, median of 5); the all-to-all is the reference's volume "
+           "note": "pack/unpack measured on one B200 (pack_ms / unpack_ms: wall clock around each phase incl. its Python planning, median of 5; *_kernel_ms: CUDA events around the phase's one hap_copy2d_batched launch, HBM GB/s = read + write bytes over it); the all-to-all is the reference's volume "
                    "at NVLink 5 900 GB/s (a multi-GPU box is needed to time it)", "rows": rows}
     text = json.dumps(out, indent=1)
     print(text)

@@ -20,8 +20,8 @@ GENERIC = dict(name="rs-generic", n_layers=1, n_q_heads=2, n_kv_heads=2, head_di
                n_shared=1, top_k=2, inter=352)
 
 
-def _simulate(cfg, n, src, dst):
-    W = synthetic_weights(cfg, "cpu", seed=0)
+def _simulate(cfg, n, src, dst, device="cpu"):
+    W = synthetic_weights(cfg, device, seed=0)
     lay = lambda te, r: RankLayout(PlanDegrees(1, n, te[0], te[1], 1), r, cfg.n_q_heads, cfg.n_kv_heads,  # noqa: E731
                                    cfg.n_experts, cfg.inter, cfg.n_shared)
     packs = [reshard_pack(cfg, pack_rank_weights(cfg, W, lay(src, r)), lay(src, r), lay(dst, r)) for r in range(n)]
@@ -52,3 +52,37 @@ def test_reshard_phases_reproduce_destination_layout(cfg_kw, n):
         for dst in strat:
             if src != dst:
                 _simulate(cfg, n, src, dst)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg_kw", [FAST, SHARED, GENERIC], ids=["fast", "shared", "generic"])
+def test_reshard_phases_on_gpu(cfg_kw):
+    """The same phases with the weights on the GPU: pack and unpack run as
+    batched hap_copy2d_batched launches (bit-identical weights)."""
+    from paper_2508_19373_b200 import ops
+
+    cfg = BlockConfig(**cfg_kw)
+    before = ops.LAUNCHES[0]
+    for n in (2, 8):
+        strat = [(t, n // t) for t in (1, 2, 4, 8) if t <= n and n % t == 0 and (cfg.inter // t) % 8 == 0]
+        for src in strat:
+            for dst in strat:
+                if src != dst:
+                    _simulate(cfg, n, src, dst, device="cuda")
+    assert ops.LAUNCHES[0] > before
+
+
+def test_rows_split_views():
+    """The descriptor rule of ops.copy_views: uniform-pitch stacks of
+    contiguous rows are found (merging trailing dims), anything else is None."""
+    from paper_2508_19373_b200.ops import _rows_split
+
+    t = torch.empty(8, 2, 4, 16)
+    v = t[:, 0]                              # [8, 4, 16] blocks, pitch 2*4*16
+    c = torch.empty(8, 4, 16)
+    assert _rows_split(v.shape, v.stride(), c.stride()) == (8, 64, 128, 64)
+    assert _rows_split(c.shape, c.stride(), c.stride()) == (1, 512, 512, 512)
+    w = torch.empty(32, 100)[:, 10:30]       # column block of a row-major matrix
+    d = torch.empty(32, 20)
+    assert _rows_split(w.shape, w.stride(), d.stride()) == (32, 20, 100, 20)
+    assert _rows_split(w.t().shape, w.t().stride(), d.t().contiguous().stride()) is None
