@@ -428,7 +428,11 @@ def main():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-tp", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-peer", action="store_true", help="N>1: skip the peer-memory exchange variant of the HAP plan")
+    ap.add_argument("--peer", action="store_true",
+                    help="N>1: also time the HAP plan with its peer-memory exchanges (CUDA IPC + device barriers). "
+                         "Opt-in: validated only with ranks sharing one B200; a device-side barrier trap on a real "
+                         "NVLink box would poison the CUDA context and cost the NCCL numbers of the same run")
+    ap.add_argument("--no-peer", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--cpu-sample-tokens", type=int, default=256)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -633,7 +637,7 @@ def main():
 
     # N > 1, last (its failure must not cost the other numbers): the HAP plan over peer memory
     peer = None
-    if world > 1 and not args.no_peer:
+    if world > 1 and args.peer and not args.no_peer:
         peer = bench_peer_variant(cfg, hap_p, hap_d, rank, weights, x_global, args.steps, args.warmup)
 
     cpu = None
