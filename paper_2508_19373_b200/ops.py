@@ -533,15 +533,14 @@ def _rows_split(shape, strides_a, strides_b):
     return rows, inner, dims[k - 1][1], dims[k - 1][2]
 
 
-def copy_views(pairs) -> int:
-    """dst.copy_(src) for every (src, dst) pair of same-shape, same-dtype CUDA
-    views in ONE hap_copy2d_batched launch (each pair must be a uniform-pitch
-    stack of contiguous rows, 16-byte aligned; ValueError otherwise — there is
-    no per-pair fallback).  Returns the bytes moved."""
+def view_records(pairs):
+    """hap_copy2d_batched records (int64 [n, 6]: src, dst, rows, row_bytes,
+    src_pitch, dst_pitch) for dst.copy_(src) over same-shape, same-dtype CUDA
+    views; each pair must be a uniform-pitch stack of contiguous rows
+    (ValueError otherwise — there is no per-pair fallback)."""
     import numpy as np
 
-    lib = _lib.load()
-    recs, moved = [], 0
+    recs = []
     for src, dst in pairs:
         _need(src, "src"); _need(dst, "dst", src.dtype)
         if src.shape != dst.shape:
@@ -554,11 +553,25 @@ def copy_views(pairs) -> int:
         rows, inner, ps, pd = sp
         es = src.element_size()
         recs.append((src.data_ptr(), dst.data_ptr(), rows, inner * es, ps * es, pd * es))
-        moved += rows * inner * es
-    if not recs:
+    return np.array(recs, dtype=np.int64).reshape(-1, 6)
+
+
+def copy_records(recs) -> int:
+    """One hap_copy2d_batched call over int64 [n, 6] records on the current
+    stream; returns the bytes moved."""
+    import numpy as np
+
+    lib = _lib.load()
+    recs = np.ascontiguousarray(recs, dtype=np.int64)
+    if len(recs) == 0:
         return 0
-    arr = np.ascontiguousarray(np.array(recs, dtype=np.int64))
-    st = lib.hap_copy2d_batched(arr.ctypes.data, len(recs), _stream())
+    st = lib.hap_copy2d_batched(recs.ctypes.data, len(recs), _stream())
     check(st, "hap_copy2d_batched")
     _count(-(-len(recs) // 192))
-    return moved
+    return int((recs[:, 2] * recs[:, 3]).sum())
+
+
+def copy_views(pairs) -> int:
+    """dst.copy_(src) for every (src, dst) pair in ONE hap_copy2d_batched
+    launch (see view_records).  Returns the bytes moved."""
+    return copy_records(view_records(pairs))

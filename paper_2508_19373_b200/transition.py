@@ -162,28 +162,117 @@ def _piece_views(buf, per: int, h: int):
     return buf[:n].view(per, h), buf[n:2 * n].view(per, h), buf[2 * n:3 * n].view(h, per)
 
 
-def _run_copies(pairs) -> None:
+def _run_copies(pairs, bases=None, plan_key=None) -> None:
     """All the copies of one reshard phase: ONE hap_copy2d_batched launch for
     device tensors; host tensors (the CPU gloo tests of the host logic) copy
-    pair by pair."""
+    pair by pair.  With ``bases`` / ``plan_key`` the launch's records are also
+    kept relative to the phase's base tensors, so the next layer with the same
+    layout pair replays them (``_replay``) without rebuilding any view."""
     if not pairs:
+        if plan_key is not None:
+            _COPY_PLANS[plan_key] = _np_empty_rel()
         return
     if pairs[0][0].is_cuda:
         from . import ops
 
-        ops.copy_views(pairs)
+        recs = ops.view_records(pairs)
+        ops.copy_records(recs)
+        if plan_key is not None:
+            rel = _relativize(recs, bases)
+            if rel is not None:
+                _COPY_PLANS[plan_key] = rel
     else:
         for src, dst in pairs:
             dst.copy_(src)
 
 
-def reshard_pack(cfg, w, lay_src, lay_dst):
-    """Phase 1 of the reshard: the send buffer (pieces this rank ships, grouped by
-    destination) and the all-to-all splits; ctx carries what reshard_unpack needs."""
+# ------------------------------------------------- compiled reshard phases --
+# The reshard plan and its copy records depend only on (model dims, source
+# layout, destination layout, rank, packed weight shapes) — the same for every
+# layer of a stage switch.  The first layer builds them from tensor views; the
+# others replay the records with their own base pointers (one numpy add + one
+# launch per phase).
+_COPY_PLANS: dict = {}
+_STATIC_PLANS: dict = {}
+
+
+def _np_empty_rel():
+    import numpy as np
+
+    return np.zeros((0, 8), dtype=np.int64)
+
+
+def _spans(bases):
+    out = []
+    for t in bases:
+        if t is None:
+            out.append((0, 0))
+        else:
+            p = t.data_ptr()
+            out.append((p, p + t.numel() * t.element_size()))
+    return out
+
+
+def _relativize(recs, bases):
+    """records [n, 6] -> [n, 8] (src base index, src offset, dst base index,
+    dst offset, rows, row_bytes, src_pitch, dst_pitch), or None when a record
+    lies outside every base (a temporary of the generic path: not replayable)."""
+    import numpy as np
+
+    spans = _spans(bases)
+
+    def find(ptr):
+        for i, (lo, hi) in enumerate(spans):
+            if lo <= ptr < hi:
+                return i, ptr - lo
+        return None
+
+    rel = np.empty((len(recs), 8), dtype=np.int64)
+    for i, (sp_, dp_, rows, rb, ps, pd) in enumerate(recs.tolist()):
+        fs, fd = find(sp_), find(dp_)
+        if fs is None or fd is None:
+            return None
+        rel[i] = (fs[0], fs[1], fd[0], fd[1], rows, rb, ps, pd)
+    return rel
+
+
+def _replay(rel, bases) -> None:
+    import numpy as np
+
+    from . import ops
+
+    if len(rel) == 0:
+        return
+    ptr = np.array([0 if t is None else t.data_ptr() for t in bases], dtype=np.int64)
+    recs = np.empty((len(rel), 6), dtype=np.int64)
+    recs[:, 0] = ptr[rel[:, 0]] + rel[:, 1]
+    recs[:, 1] = ptr[rel[:, 2]] + rel[:, 3]
+    recs[:, 2:] = rel[:, 4:]
+    ops.copy_records(recs)
+
+
+def _weights_key(w):
+    ts = tuple(None if t is None else (tuple(t.shape), tuple(t.stride()), str(t.dtype))
+               for t in (w.w13, w.w2, w.ws13, w.ws2))
+    return ts + (w.hw, w.hw_s, w.n_experts_local, w.inter_local, w.shared_inter_local)
+
+
+def _phase_key(cfg, w, lay_src, lay_dst):
+    return (cfg.hidden, cfg.inter, cfg.n_experts, cfg.n_shared, cfg.n_q_heads, cfg.n_kv_heads,
+            lay_src.deg, lay_src.rank, lay_dst.deg, _weights_key(w))
+
+
+def _static_plan(cfg, lay_src, lay_dst):
+    """The host half of a reshard (who sends which (unit, slice) to whom), cached per layout pair."""
     from math import gcd
 
     from .layout import RankLayout
 
+    key = (cfg.hidden, cfg.inter, cfg.n_experts, cfg.n_shared, cfg.n_q_heads, cfg.n_kv_heads,
+           lay_src.deg, lay_src.rank, lay_dst.deg)
+    hit = _STATIC_PLANS.get(key)
+    if hit is not None:
+        return hit
     n = lay_src.n
     tp_i, tp_j = lay_src.deg.e_tp, lay_dst.deg.e_tp
     n_slices = tp_i * tp_j // gcd(tp_i, tp_j)
@@ -194,51 +283,61 @@ def reshard_pack(cfg, w, lay_src, lay_dst):
     dsts = [mk(lay_dst.deg, r) for r in range(n)]
     own_src, own_dst, sends = reshard_plan(srcs, dsts, n_slices)
     me = lay_src.rank
-    e0 = lay_src.experts[0]
-    s0 = lay_src.inter_slice[0] // per
+    piece_elems = 3 * per * h
+    st = dict(n=n, per=per, h=h, own_src=own_src, sends=sends, me=me, e0=lay_src.experts[0],
+              e1=lay_src.experts[1], s0=lay_src.inter_slice[0] // per, piece_elems=piece_elems,
+              order=[(uu, s) for r in range(n) for (uu, s) in sends[me][r]],
+              in_splits=[len(sends[me][r]) * piece_elems for r in range(n)],
+              out_splits=[len(sends[q][me]) * piece_elems for q in range(n)])
+    _STATIC_PLANS[key] = st
+    return st
+
+
+def reshard_pack(cfg, w, lay_src, lay_dst):
+    """Phase 1 of the reshard: the send buffer (pieces this rank ships, grouped by
+    destination) and the all-to-all splits; ctx carries what reshard_unpack needs."""
+    st = _static_plan(cfg, lay_src, lay_dst)
+    per, h, s0, e0, piece_elems, order = st["per"], st["h"], st["s0"], st["e0"], st["piece_elems"], st["order"]
     unpacked = []  # per-unit contiguous (gate, up, down^T), built only if a piece misses the fast path
+
+    def unit_index(unit):
+        return unit - e0 if unit < cfg.n_experts else (st["e1"] - e0) + (unit - cfg.n_experts)
 
     def local_piece(unit, s):
         """(gate [per,h], up [per,h], down [h,per]) views of a piece this rank holds."""
         if not unpacked:
             unpacked.append(_unpack(cfg, w))
-        units = unpacked[0]
-        if unit < cfg.n_experts:
-            u = units[unit - e0]
-        else:
-            u = units[(lay_src.experts[1] - e0) + (unit - cfg.n_experts)]
         k = s - s0
-        g, up, dt = (t[k * per:(k + 1) * per] for t in u)
+        g, up, dt = (t[k * per:(k + 1) * per] for t in unpacked[0][unit_index(unit)])
         return g, up, dt.t()
 
-    piece_elems = 3 * per * h
-    order = [(uu, s) for r in range(n) for (uu, s) in sends[me][r]]
-    in_splits = [len(sends[me][r]) * piece_elems for r in range(n)]
-    out_splits = [len(sends[q][me]) * piece_elems for q in range(n)]
     dev, dt = w.w13.device, w.w13.dtype
     send = torch.empty(len(order) * piece_elems, dtype=dt, device=dev)
     src_views = _unit_views(cfg, w)
-
-    def unit_index(unit):
-        return unit - e0 if unit < cfg.n_experts else (lay_src.experts[1] - e0) + (unit - cfg.n_experts)
-
-    pairs = []
-    for i, (uu, sl) in enumerate(order):
-        # each piece is written once, straight from the packed source layout
-        pg, pu, pd = _piece_views(send[i * piece_elems:(i + 1) * piece_elems], per, h)
-        t13, base, hw_u, t2 = src_views[unit_index(uu)]
-        r0 = base + (sl - s0) * per
-        g, u_ = _gu_rows(t13, hw_u, r0, per, 0), _gu_rows(t13, hw_u, r0, per, 1)
-        if g is None:
-            lg, lu, ld = local_piece(uu, sl)
-            pairs += [(lg, pg), (lu, pu), (ld, pd)]
-        else:
-            pairs += [(g, pg.view(per // hw_u, hw_u, h)), (u_, pu.view(per // hw_u, hw_u, h)),
-                      (t2[:, (sl - s0) * per:(sl - s0 + 1) * per], pd)]
-    _run_copies(pairs)
-    ctx = dict(cfg=cfg, w=w, lay_dst=lay_dst, n=n, me=me, per=per, h=h, own_src=own_src, sends=sends,
-               local_piece=local_piece, piece_elems=piece_elems, src_views=src_views, unit_index=unit_index, s0=s0)
-    return send, in_splits, out_splits, ctx
+    key = ("pack",) + _phase_key(cfg, w, lay_src, lay_dst)
+    bases = [w.w13, w.w2, w.ws13, w.ws2, send]
+    rel = _COPY_PLANS.get(key) if send.is_cuda else None
+    if rel is not None:
+        _replay(rel, bases)
+    else:
+        pairs = []
+        for i, (uu, sl) in enumerate(order):
+            # each piece is written once, straight from the packed source layout
+            pg, pu, pd = _piece_views(send[i * piece_elems:(i + 1) * piece_elems], per, h)
+            t13, base, hw_u, t2 = src_views[unit_index(uu)]
+            r0 = base + (sl - s0) * per
+            g, u_ = _gu_rows(t13, hw_u, r0, per, 0), _gu_rows(t13, hw_u, r0, per, 1)
+            if g is None:
+                lg, lu, ld = local_piece(uu, sl)
+                pairs += [(lg, pg), (lu, pu), (ld, pd)]
+            else:
+                pairs += [(g, pg.view(per // hw_u, hw_u, h)), (u_, pu.view(per // hw_u, hw_u, h)),
+                          (t2[:, (sl - s0) * per:(sl - s0 + 1) * per], pd)]
+        _run_copies(pairs, bases, key if send.is_cuda else None)
+    ctx = dict(cfg=cfg, w=w, lay_src=lay_src, lay_dst=lay_dst, n=st["n"], me=st["me"], per=per, h=h,
+               own_src=st["own_src"], sends=st["sends"], local_piece=local_piece, piece_elems=piece_elems,
+               src_views=src_views, unit_index=unit_index, s0=s0)
+    return send, list(st["in_splits"]), list(st["out_splits"]), ctx
 
 
 def reshard_unpack(ctx, recv):
@@ -251,16 +350,6 @@ def reshard_unpack(ctx, recv):
     cfg, w, n, me, per = ctx["cfg"], ctx["w"], ctx["n"], ctx["me"], ctx["per"]
     own_src, sends, local_piece, piece_elems, h = (ctx["own_src"], ctx["sends"], ctx["local_piece"],
                                                   ctx["piece_elems"], ctx["h"])
-    received = {}
-    off = 0
-    for q in range(n):
-        for key in sends[q][me]:
-            received[key] = _piece_views(recv[off:off + piece_elems], per, h)
-            off += piece_elems
-
-    def piece(key):
-        return local_piece(*key) if key in own_src[me] else received[key]
-
     d = ctx["lay_dst"]
     de0, de1 = d.experts
     ds0, ds1 = d.inter_slice[0] // per, d.inter_slice[1] // per
@@ -278,31 +367,53 @@ def reshard_unpack(ctx, recv):
         w2 = torch.empty(El_d, h, il, dtype=dt, device=dev)
         ws13 = torch.empty(2 * sil, h, dtype=dt, device=dev) if cfg.n_shared else None
         ws2 = torch.empty(h, sil, dtype=dt, device=dev) if cfg.n_shared else None
-        src_views, unit_index, s0 = ctx["src_views"], ctx["unit_index"], ctx["s0"]
-        pairs = []
-        for j, unit in enumerate(units_d):
-            if unit < cfg.n_experts:
-                t13, base, hw_u, t2 = w13[j], 0, hw, w2[j]
-            else:
-                u = unit - cfg.n_experts
-                t13, base, hw_u, t2 = ws13, u * il, hw_s, ws2[:, u * il:(u + 1) * il]
-            for sl in range(ds0, ds1):
-                r0 = base + (sl - ds0) * per
-                gd, ud = _gu_rows(t13, hw_u, r0, per, 0), _gu_rows(t13, hw_u, r0, per, 1)
-                dcols = t2[:, (sl - ds0) * per:(sl - ds0 + 1) * per]
-                key = (unit, sl)
-                if key in own_src[me]:  # straight from this rank's own packed weights
-                    st13, sbase, shw, st2 = src_views[unit_index(unit)]
-                    sr0 = sbase + (sl - s0) * per
-                    sg, su = _gu_rows(st13, shw, sr0, per, 0), _gu_rows(st13, shw, sr0, per, 1)
-                    if sg is not None:
-                        pairs += [(sg, gd), (su, ud), (st2[:, (sl - s0) * per:(sl - s0 + 1) * per], dcols)]
-                        continue
-                pg, pu, pd = piece(key)
-                pairs += [(pg.view(per // hw_u, hw_u, h), gd), (pu.view(per // hw_u, hw_u, h), ud), (pd, dcols)]
-        _run_copies(pairs)
+        key = ("unpack",) + _phase_key(cfg, w, ctx["lay_src"], d)
+        bases = [w.w13, w.w2, w.ws13, w.ws2, recv, w13, w2, ws13, ws2]
+        rel = _COPY_PLANS.get(key) if recv.is_cuda else None
+        if rel is not None:
+            _replay(rel, bases)
+        else:
+            received = {}
+            off = 0
+            for q in range(n):
+                for k_ in sends[q][me]:
+                    received[k_] = _piece_views(recv[off:off + piece_elems], per, h)
+                    off += piece_elems
+            src_views, unit_index, s0 = ctx["src_views"], ctx["unit_index"], ctx["s0"]
+            pairs = []
+            for j, unit in enumerate(units_d):
+                if unit < cfg.n_experts:
+                    t13, base, hw_u, t2 = w13[j], 0, hw, w2[j]
+                else:
+                    u = unit - cfg.n_experts
+                    t13, base, hw_u, t2 = ws13, u * il, hw_s, ws2[:, u * il:(u + 1) * il]
+                for sl in range(ds0, ds1):
+                    r0 = base + (sl - ds0) * per
+                    gd, ud = _gu_rows(t13, hw_u, r0, per, 0), _gu_rows(t13, hw_u, r0, per, 1)
+                    dcols = t2[:, (sl - ds0) * per:(sl - ds0 + 1) * per]
+                    k_ = (unit, sl)
+                    if k_ in own_src[me]:  # straight from this rank's own packed weights
+                        st13, sbase, shw, st2 = src_views[unit_index(unit)]
+                        sr0 = sbase + (sl - s0) * per
+                        sg, su = _gu_rows(st13, shw, sr0, per, 0), _gu_rows(st13, shw, sr0, per, 1)
+                        if sg is not None:
+                            pairs += [(sg, gd), (su, ud), (st2[:, (sl - s0) * per:(sl - s0 + 1) * per], dcols)]
+                            continue
+                    pg, pu, pd = local_piece(*k_) if k_ in own_src[me] else received[k_]
+                    pairs += [(pg.view(per // hw_u, hw_u, h), gd), (pu.view(per // hw_u, hw_u, h), ud), (pd, dcols)]
+            _run_copies(pairs, bases, key if recv.is_cuda else None)
         return dataclasses.replace(w, w13=w13, w2=w2, hw=hw, ws13=ws13, ws2=ws2, hw_s=hw_s,
                                    n_experts_local=El_d, inter_local=il, shared_inter_local=sil)
+
+    received = {}
+    off = 0
+    for q in range(n):
+        for k_ in sends[q][me]:
+            received[k_] = _piece_views(recv[off:off + piece_elems], per, h)
+            off += piece_elems
+
+    def piece(key):
+        return local_piece(*key) if key in own_src[me] else received[key]
 
     def assemble(unit):
         ps = [piece((unit, s)) for s in range(ds0, ds1)]

@@ -58,18 +58,27 @@ def test_reshard_phases_reproduce_destination_layout(cfg_kw, n):
 @pytest.mark.parametrize("cfg_kw", [FAST, SHARED, GENERIC], ids=["fast", "shared", "generic"])
 def test_reshard_phases_on_gpu(cfg_kw):
     """The same phases with the weights on the GPU: pack and unpack run as
-    batched hap_copy2d_batched launches (bit-identical weights)."""
-    from paper_2508_19373_b200 import ops
+    batched hap_copy2d_batched launches (bit-identical weights); the second
+    pass over fresh weight tensors replays the compiled copy records (the
+    per-layer path of a stage switch) and must be bit-identical too."""
+    from paper_2508_19373_b200 import ops, transition
 
     cfg = BlockConfig(**cfg_kw)
+    transition._COPY_PLANS.clear()
     before = ops.LAUNCHES[0]
-    for n in (2, 8):
-        strat = [(t, n // t) for t in (1, 2, 4, 8) if t <= n and n % t == 0 and (cfg.inter // t) % 8 == 0]
-        for src in strat:
-            for dst in strat:
-                if src != dst:
-                    _simulate(cfg, n, src, dst, device="cuda")
+    for rep in range(2):
+        for n in (2, 8):
+            strat = [(t, n // t) for t in (1, 2, 4, 8) if t <= n and n % t == 0 and (cfg.inter // t) % 8 == 0]
+            for src in strat:
+                for dst in strat:
+                    if src != dst:
+                        _simulate(cfg, n, src, dst, device="cuda")
+        if rep == 0:
+            n_plans = len(transition._COPY_PLANS)
     assert ops.LAUNCHES[0] > before
+    assert len(transition._COPY_PLANS) == n_plans  # the second pass compiled nothing new
+    if cfg.name != "rs-generic":
+        assert n_plans > 0
 
 
 def test_rows_split_views():
