@@ -106,6 +106,21 @@ int hap_gemm_qkv_rope(const void* A, int64_t M, int64_t lda, int64_t K, const vo
                       int64_t head_dim, float theta, void* stream);
 
 /*
+ * Attention-module prologue in one call: hn = RMSNorm(x; norm_w, eps) exactly
+ * as hap_rmsnorm, then C = hap_gemm_qkv_rope(hn, ...).  Decode-size launches
+ * (1-2 rows on the GEMV path) normalise the rows while staging them and never
+ * write hn (one launch instead of two); otherwise hn (caller scratch, M x K
+ * bf16, leading dimension ldhn) receives the normalised rows.  The contents
+ * of hn after the call are unspecified; C is bit-identical to the two calls.
+ * Replaces: the attention module's norm + QKV projection whose weights the
+ * reference streams per decode step (arch.py:145-161, costmodel decode rows).
+ */
+int hap_rmsnorm_gemm_qkv_rope(const void* x, int64_t M, int64_t ldx, int64_t K, const void* norm_w, float eps,
+                              void* hn, int64_t ldhn, const void* W, int64_t N, const void* bias, void* C,
+                              int64_t ldc, const int32_t* positions, int64_t n_rope_heads, int64_t head_dim,
+                              float theta, void* workspace, size_t ws_bytes, void* stream);
+
+/*
  * Split-K variants of the two GEMM entry points (same semantics).  With a
  * workspace, shapes whose tiles cannot cover the 148 SMs (small-M weight
  * streaming: decode projections, TP-sharded layers) cut K into slices run by

@@ -142,6 +142,11 @@ SIGNATURES = {
     ),
     "hap_attn_decode_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int64]),
     "hap_copy2d_batched": (ctypes.c_int, [c_void_p, c_int64, c_void_p]),
+    "hap_rmsnorm_gemm_qkv_rope": (
+        ctypes.c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_float, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
+         c_void_p, c_int64, c_void_p, c_int64, c_int64, c_float, c_void_p, c_size_t, c_void_p],
+    ),
     "hap_kv_cache_fill_paged": (
         ctypes.c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int64,

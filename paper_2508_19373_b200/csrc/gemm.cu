@@ -83,6 +83,11 @@ struct Params {
   // being a (possibly peer-mapped) device address; NULL = C
   const int64_t* seg_dst;
   const int32_t* seg_dst_row0;
+  // GEMV only (hap_rmsnorm_gemm_qkv_rope): A rows are RMS-normalised with
+  // these weights while they are staged in shared memory (same arithmetic as
+  // rmsnorm_row_kernel, bit-identical hn); NULL = A is used as is
+  const __nv_bfloat16* norm_w;
+  float norm_eps;
 };
 
 constexpr int kEpiRope = 3;     // internal epilogue id (hap_gemm_qkv_rope)
@@ -918,11 +923,59 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
   pdl_wait();
   extern __shared__ uint4 xs[];  // [a_rows][K/8]
   const int kv = p.K / 8;
-  for (int i = threadIdx.x; i < p.a_rows * kv; i += blockDim.x) {
-    const int r = i / kv, c = i - r * kv;
-    xs[i] = *reinterpret_cast<const uint4*>(A + (int64_t)r * lda + (int64_t)c * 8);
+  if (p.norm_w) {
+    // fused RMSNorm: each 128-thread half of the CTA normalises one row with
+    // exactly rmsnorm_row_kernel's order (thread t: vectors t, t+128, ...;
+    // fma x then y per bf16 pair; xor-shuffle tree; (w0 + w1) + (w2 + w3))
+    __shared__ float red[2][4];
+    const int grp = threadIdx.x >> 7, t = threadIdx.x & 127, lane = threadIdx.x & 31, wq = (threadIdx.x >> 5) & 3;
+    const uint4* nw = reinterpret_cast<const uint4*>(p.norm_w);
+    for (int rr = 0; rr < p.a_rows; rr += 2) {
+      const int r = rr + grp;
+      const uint4* xr = reinterpret_cast<const uint4*>(A + (int64_t)r * lda);
+      float ss = 0.f;
+      if (r < p.a_rows) {
+        for (int c = t; c < kv; c += 128) {
+          const uint4 v = __ldg(xr + c);
+          const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = unpack_bf16x2(u[j]);
+            ss = fmaf(f.x, f.x, ss);
+            ss = fmaf(f.y, f.y, ss);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) red[grp][wq] = ss;
+      __syncthreads();
+      if (r < p.a_rows) {
+        const float tot = (red[grp][0] + red[grp][1]) + (red[grp][2] + red[grp][3]);
+        const float inv = rsqrtf(tot / (float)(kv * 8) + p.norm_eps);
+        for (int c = t; c < kv; c += 128) {
+          const uint4 v = __ldg(xr + c), wv = __ldg(nw + c);
+          const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+          const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+          uint32_t o[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = unpack_bf16x2(u[j]);
+            const float2 g = unpack_bf16x2(ww[j]);
+            o[j] = pack_bf16x2(f.x * inv * g.x, f.y * inv * g.y);
+          }
+          xs[r * kv + c] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int i = threadIdx.x; i < p.a_rows * kv; i += blockDim.x) {
+      const int r = i / kv, c = i - r * kv;
+      xs[i] = *reinterpret_cast<const uint4*>(A + (int64_t)r * lda + (int64_t)c * 8);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pairs = p.epi == HAP_EPI_SWIGLU ? p.N / 2 : p.N / 2;  // column pairs per segment
   const int n_items = p.n_segs * n_pairs;
@@ -1284,6 +1337,48 @@ extern "C" int hap_gemm_qkv_rope_ex(const void* A, int64_t M, int64_t lda, int64
   for (int bn = 256; bn >= head_dim; bn -= (int)head_dim)
     if (N % bn == 0) { p.BN = bn; break; }
   return launch(p, A, M, lda, K, W, 1, N, 1, workspace, ws_bytes, stream);
+}
+
+extern "C" int hap_rmsnorm_gemm_qkv_rope(const void* x, int64_t M, int64_t ldx, int64_t K, const void* norm_w,
+                                         float eps, void* hn, int64_t ldhn, const void* W, int64_t N,
+                                         const void* bias, void* C, int64_t ldc, const int32_t* positions,
+                                         int64_t n_rope_heads, int64_t head_dim, float theta, void* workspace,
+                                         size_t ws_bytes, void* stream) {
+  using namespace hap::gemm;
+  if (!x || !norm_w || !hn || !W || !C || !positions || M < 0 || K <= 0 || N <= 0) return HAP_ERR_INVALID_ARG;
+  if (head_dim != 64 && head_dim != 128) return HAP_ERR_UNSUPPORTED;
+  if (N % head_dim || n_rope_heads < 0 || n_rope_heads * head_dim > N) return HAP_ERR_INVALID_ARG;
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return HAP_ERR_UNSUPPORTED;
+  if (K % 8 || ldx % 8 || ldhn % 8 || ldc % 8 || ldx < K || ldhn < K || ldc < N) return HAP_ERR_MISALIGNED;
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(norm_w) | reinterpret_cast<uintptr_t>(hn) |
+       reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(C)) & 15)
+    return HAP_ERR_MISALIGNED;
+  if (M == 0) return HAP_OK;
+  // the GEMV path (1-2 rows, decode) normalises while staging its rows: one launch
+  if (gemv_mode() > 0 && M <= kGvAutoRows && N % 2 == 0 && M * K * 2 <= 192 * 1024 &&
+      N * K * 2 <= (int64_t)64 << 20) {
+    Params p{};
+    p.a_rows = (int32_t)M;
+    p.K = (int32_t)K;
+    p.N = (int32_t)N;
+    p.n_segs = 1;
+    p.epi = kEpiRope;
+    p.C = reinterpret_cast<__nv_bfloat16*>(C);
+    p.ldc = ldc;
+    p.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+    p.positions = positions;
+    p.head_dim = (int32_t)head_dim;
+    p.rope_cols = (int32_t)(n_rope_heads * head_dim);
+    p.theta = theta;
+    p.out_cols = (int32_t)N;
+    p.norm_w = reinterpret_cast<const __nv_bfloat16*>(norm_w);
+    p.norm_eps = eps;
+    return launch_gemv(p, x, ldx, W, stream);
+  }
+  const int st = hap_rmsnorm(x, M, K, ldx, norm_w, eps, hn, ldhn, stream);
+  if (st != HAP_OK) return st;
+  return hap_gemm_qkv_rope_ex(hn, M, ldhn, K, W, N, bias, C, ldc, positions, n_rope_heads, head_dim, theta, workspace,
+                              ws_bytes, stream);
 }
 
 extern "C" int hap_gemm_qkv_rope(const void* A, int64_t M, int64_t lda, int64_t K, const void* W, int64_t N,

@@ -75,6 +75,13 @@ def _ep_peer_default() -> bool:
     return os.environ.get("HAP_EP_PEER", "0") == "1"
 
 
+# HAP_FUSED_NORM=1: decode runs the attention norm inside the QKV launch
+# (hap_rmsnorm_gemm_qkv_rope).  Off by default: one launch fewer and 1.7-3.6 us
+# faster in isolation, but the graph-replayed decode step measured +15 us
+# (Mixtral-8x7B B=1) / +1 us (Qwen2-57B B=1) with it (profiles/r02_fused_norm_ab.txt)
+_FUSED_NORM = os.environ.get("HAP_FUSED_NORM", "0") == "1"
+
+
 class CudaOps:
     """The product compute backend: every method launches a kernel of
     libhap_kernels.so through the C-ABI (ops.py).  Construction fails loudly
@@ -90,6 +97,7 @@ class CudaOps:
     rmsnorm = staticmethod(K.rmsnorm)
     gemm = staticmethod(K.gemm)
     gemm_qkv_rope = staticmethod(K.gemm_qkv_rope)
+    rmsnorm_qkv_rope = staticmethod(K.rmsnorm_qkv_rope)
     grouped_gemm = staticmethod(K.grouped_gemm)
     rope_qk = staticmethod(K.rope_qk)
     attn_prefill = staticmethod(K.attn_prefill)
@@ -422,8 +430,12 @@ class HapMoEBlock:
             x = x_local.contiguous()
 
         # ---------------- attention module
-        with self._timed("norm"):
-            xn = ops.rmsnorm(x, w.ln1, cfg.rms_eps)
+        # decode, opt-in: the norm rides in the QKV launch (GEMV at 1-2 rows
+        # stages the normalised rows itself; bit-identical to the two launches)
+        fused_norm = decode and _FUSED_NORM and hasattr(ops, "rmsnorm_qkv_rope")
+        if not fused_norm:
+            with self._timed("norm"):
+                xn = ops.rmsnorm(x, w.ln1, cfg.rms_eps)
         nq, nkv = w.n_q_local, w.n_kv_local
         if decode:
             if max_position is not None:  # the caller's host-side length: no device read-back
@@ -443,7 +455,11 @@ class HapMoEBlock:
             pos = self._prefill_positions(bpr, S, rows)
         # QKV projection with RoPE fused into the GEMM epilogue
         with self._timed("qkv"):
-            qkv = ops.gemm_qkv_rope(xn, w.wqkv, pos, nq + nkv, d, cfg.rope_theta, bias=w.bqkv)
+            if fused_norm:
+                qkv = ops.rmsnorm_qkv_rope(x, w.ln1, cfg.rms_eps, w.wqkv, pos, nq + nkv, d, cfg.rope_theta,
+                                           bias=w.bqkv)
+            else:
+                qkv = ops.gemm_qkv_rope(xn, w.wqkv, pos, nq + nkv, d, cfg.rope_theta, bias=w.bqkv)
         attn = torch.zeros(rows, nq * d, device=dev, dtype=BF16) if rows != T_real else \
             torch.empty(rows, nq * d, device=dev, dtype=BF16)
         paged = isinstance(kv_cache, PagedKVCache)

@@ -233,6 +233,46 @@ def gemm_qkv_rope(a: torch.Tensor, w: torch.Tensor, positions: torch.Tensor, n_r
     return out
 
 
+_HN_SCRATCH: dict = {}
+
+
+def rmsnorm_qkv_rope(x: torch.Tensor, norm_w: torch.Tensor, eps: float, w: torch.Tensor, positions: torch.Tensor,
+                     n_rope_heads: int, head_dim: int, theta: float, bias: Optional[torch.Tensor] = None,
+                     out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """gemm_qkv_rope(rmsnorm(x, norm_w, eps), ...) through hap_rmsnorm_gemm_qkv_rope:
+    one launch at decode sizes (the GEMV normalises while staging its rows),
+    bit-identical to the two calls."""
+    lib = _lib.load()
+    _need(x, "x", BF16); _need(norm_w, "norm_w", BF16); _need(w, "w", BF16)
+    _need(positions, "positions", torch.int32)
+    _rowmajor(x, "x")
+    if not w.is_contiguous() or not norm_w.is_contiguous():
+        raise ValueError("w and norm_w must be contiguous")
+    if bias is not None:
+        _need(bias, "bias", BF16)
+    M, K = x.shape
+    N = w.shape[0]
+    if out is None:
+        out = torch.empty(M, N, device=x.device, dtype=BF16)
+    _need(out, "out", BF16); _rowmajor(out, "out")
+    if M <= 2:  # the GEMV path never writes hn: a persistent scratch, no allocation per call
+        key = (x.device, K)
+        hn = _HN_SCRATCH.get(key)
+        if hn is None:
+            hn = _HN_SCRATCH[key] = torch.empty(2, K, device=x.device, dtype=BF16)
+        hn = hn[:M]
+    else:
+        hn = torch.empty(M, K, device=x.device, dtype=BF16)
+    ws, ws_bytes = splitk_workspace(x.device)
+    st = lib.hap_rmsnorm_gemm_qkv_rope(x.data_ptr(), M, x.stride(0), K, norm_w.data_ptr(), float(eps),
+                                       hn.data_ptr(), hn.stride(0), w.data_ptr(), N, _ptr(bias), out.data_ptr(),
+                                       out.stride(0), positions.data_ptr(), n_rope_heads, head_dim, float(theta),
+                                       ws or None, ws_bytes, _stream())
+    check(st, "hap_rmsnorm_gemm_qkv_rope")
+    _count(1 if M <= 2 else 2)
+    return out
+
+
 def router_topk(x: torch.Tensor, w: torch.Tensor, n_experts: int, top_k: int, renormalize: bool,
                 has_shared_gate: bool, topk_idx: torch.Tensor, topk_w: torch.Tensor,
                 shared_gate: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None,

@@ -108,3 +108,56 @@ def test_inner_gemv_swiglu_and_grouped(M):
             continue
         assert rel(H[lo:hi], swiglu(a[lo:hi], e)) < 1e-2
         assert rel(Y[lo:hi], H[lo:hi].float() @ w2[e].float().t()) < 1e-2
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 9])
+@pytest.mark.parametrize("dims", [(3584, 28, 4, True), (4096, 32, 8, False)], ids=["qwen2-57b", "mixtral"])
+def test_fused_norm_qkv_matches_two_launches(M, dims):
+    """hap_rmsnorm_gemm_qkv_rope (default mode: the GEMV stages the normalised
+    rows itself at 1-2 rows, two launches otherwise) is bit-identical to
+    hap_rmsnorm + hap_gemm_qkv_rope, and the rows it normalises equal
+    hap_rmsnorm's output bit for bit (checked through the projection)."""
+    if INNER:
+        pytest.skip("default GEMV mode only")
+    from paper_2508_19373_b200 import ops
+
+    K, nq, nkv, has_bias = dims
+    d = 128
+    N = (nq + 2 * nkv) * d
+    x = r(M, K, seed=M)
+    lnw = (1.0 + 0.05 * r(K, seed=7).float()).to(torch.bfloat16)
+    w = r(N, K, std=0.02, seed=3)
+    bias = r(N, std=0.1, seed=4) if has_bias else None
+    pos = torch.arange(100, 100 + M, device=dev, dtype=torch.int32) * 7
+    want = ops.gemm_qkv_rope(ops.rmsnorm(x, lnw, 1e-6), w, pos, nq + nkv, d, 1e6, bias=bias)
+    got = ops.rmsnorm_qkv_rope(x, lnw, 1e-6, w, pos, nq + nkv, d, 1e6, bias=bias)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want), (M, dims, rel(got, want))
+
+
+def test_fused_norm_decode_block_bit_identical():
+    """The executor's opt-in fused decode prologue (HAP_FUSED_NORM=1) leaves the
+    block's decode output and routing bit-identical."""
+    if INNER:
+        pytest.skip("default GEMV mode only")
+    from paper_2508_19373_b200 import executor as E
+    from paper_2508_19373_b200.config import get_config, scaled
+    from paper_2508_19373_b200.layout import PlanDegrees
+
+    cfg = scaled(get_config("qwen2-57b-a14b"), hidden=1024, n_q_heads=8, n_kv_heads=2, inter=512)
+    blk = E.HapMoEBlock(cfg, PlanDegrees(1, 1, 1, 1), None)
+    prev = E._FUSED_NORM
+    try:
+        for B in (1, 2, 5):
+            torch.manual_seed(B)
+            cache = E.KVCache.empty(B, cfg.n_kv_heads, 256, cfg.head_dim, dev, random=True)
+            pos = torch.full((B,), 200, device=dev, dtype=torch.int32)
+            x = r(B, cfg.hidden, seed=B)
+            res = {}
+            for f in (False, True):
+                E._FUSED_NORM = f
+                res[f] = (blk.forward(x, "decode", B, kv_cache=cache, positions=pos).clone(),
+                          blk.last_routing[0].clone())
+            assert torch.equal(res[False][0], res[True][0]) and torch.equal(res[False][1], res[True][1]), B
+    finally:
+        E._FUSED_NORM = prev
