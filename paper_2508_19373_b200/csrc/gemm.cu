@@ -917,24 +917,24 @@ __device__ __forceinline__ void gv_dot8(const uint4 w, const uint4 x, float& acc
   }
 }
 
-__global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda,
-                                                          const __nv_bfloat16* __restrict__ B, Params p) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ uint4 xs[];  // [a_rows][K/8]
-  const int kv = p.K / 8;
+// Stage the (<= 8) activation rows of a GEMV launch in shared memory, RMS-
+// normalised on the way when p.norm_w is set: each 128-thread group of the
+// first 256 threads normalises one row with exactly rmsnorm_row_kernel's
+// order (thread t: vectors t, t+128, ...; fma x then y per bf16 pair; xor-
+// shuffle tree; (w0 + w1) + (w2 + w3)) — bit-identical to hap_rmsnorm.
+// Called by every thread of the CTA (contains __syncthreads).
+__device__ __forceinline__ void gv_stage_rows(uint4* xs, const __nv_bfloat16* __restrict__ A, int64_t lda,
+                                              const Params& p, int kv) {
   if (p.norm_w) {
-    // fused RMSNorm: each 128-thread half of the CTA normalises one row with
-    // exactly rmsnorm_row_kernel's order (thread t: vectors t, t+128, ...;
-    // fma x then y per bf16 pair; xor-shuffle tree; (w0 + w1) + (w2 + w3))
     __shared__ float red[2][4];
     const int grp = threadIdx.x >> 7, t = threadIdx.x & 127, lane = threadIdx.x & 31, wq = (threadIdx.x >> 5) & 3;
     const uint4* nw = reinterpret_cast<const uint4*>(p.norm_w);
     for (int rr = 0; rr < p.a_rows; rr += 2) {
       const int r = rr + grp;
+      const bool mine = grp < 2 && r < p.a_rows;
       const uint4* xr = reinterpret_cast<const uint4*>(A + (int64_t)r * lda);
       float ss = 0.f;
-      if (r < p.a_rows) {
+      if (mine) {
         for (int c = t; c < kv; c += 128) {
           const uint4 v = __ldg(xr + c);
           const uint32_t u[4] = {v.x, v.y, v.z, v.w};
@@ -948,9 +948,9 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (lane == 0) red[grp][wq] = ss;
+      if (grp < 2 && lane == 0) red[grp][wq] = ss;
       __syncthreads();
-      if (r < p.a_rows) {
+      if (mine) {
         const float tot = (red[grp][0] + red[grp][1]) + (red[grp][2] + red[grp][3]);
         const float inv = rsqrtf(tot / (float)(kv * 8) + p.norm_eps);
         for (int c = t; c < kv; c += 128) {
@@ -976,26 +976,74 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
     }
     __syncthreads();
   }
+}
+
+// The two weight rows of GEMV item (column pair) c2: the two output columns,
+// the gate and up rows of one SwiGLU column, or columns i and i + d/2 of a head.
+__device__ __forceinline__ void gv_rows(const Params& p, int c2, int& na, int& nb) {
+  if (p.epi == HAP_EPI_SWIGLU) {
+    na = (c2 / p.hw) * 2 * p.hw + c2 % p.hw;
+    nb = na + p.hw;
+  } else if (p.epi == kEpiRope) {
+    const int d = p.head_dim, half = d >> 1;
+    na = (c2 / half) * d + c2 % half;
+    nb = na + half;
+  } else {
+    na = 2 * c2;
+    nb = na + 1;
+  }
+}
+
+// Epilogue of one (row, column pair): SwiGLU / bias / RoPE / residual, bf16 out.
+__device__ __forceinline__ void gv_store(const Params& p, int row, int c2, int na, int nb, float x1, float x2) {
+  __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
+  if (p.epi == HAP_EPI_SWIGLU) {
+    crow[c2] = __float2bfloat16_rn(silu(x1) * x2);
+    return;
+  }
+  if (p.bias) {
+    x1 += __bfloat162float(p.bias[na]);
+    x2 += __bfloat162float(p.bias[nb]);
+  }
+  if (p.epi == kEpiRope) {
+    const int d = p.head_dim, half = d >> 1;
+    if (na < p.rope_cols) {
+      const int i = c2 % half;
+      const float inv_freq = 1.0f / powf(p.theta, (float)(2 * i) / (float)d);
+      float sn, cs;
+      rope_sincos((float)p.positions[row] * inv_freq, &sn, &cs);
+      const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
+      x1 = y1;
+      x2 = y2;
+    }
+    crow[na] = __float2bfloat16_rn(x1);
+    crow[nb] = __float2bfloat16_rn(x2);
+    return;
+  }
+  if (p.resid) {
+    x1 += __bfloat162float(p.resid[(int64_t)row * p.ldr + na]);
+    x2 += __bfloat162float(p.resid[(int64_t)row * p.ldr + nb]);
+  }
+  *reinterpret_cast<uint32_t*>(crow + na) = pack_bf16x2(x1, x2);
+}
+
+__global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda,
+                                                          const __nv_bfloat16* __restrict__ B, Params p) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ uint4 xs[];  // [a_rows][K/8]
+  const int kv = p.K / 8;
+  gv_stage_rows(xs, A, lda, p, kv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_pairs = p.epi == HAP_EPI_SWIGLU ? p.N / 2 : p.N / 2;  // column pairs per segment
+  const int n_pairs = p.N / 2;  // column pairs per segment
   const int n_items = p.n_segs * n_pairs;
-  const int d = p.head_dim, half = d >> 1;
   for (int item = blockIdx.x * (kGvThreads / 32) + warp; item < n_items; item += gridDim.x * (kGvThreads / 32)) {
     const int s = item / n_pairs, c2 = item - s * n_pairs;
     const int r0 = p.seg ? p.seg[s] : 0, r1 = p.seg ? p.seg[s + 1] : p.a_rows;
     if (r1 <= r0) continue;
     const int g = p.seg_group ? p.seg_group[s] : s;
     int na, nb;  // the two weight rows of this item
-    if (p.epi == HAP_EPI_SWIGLU) {
-      na = (c2 / p.hw) * 2 * p.hw + c2 % p.hw;
-      nb = na + p.hw;
-    } else if (p.epi == kEpiRope) {
-      na = (c2 / half) * d + c2 % half;
-      nb = na + half;
-    } else {
-      na = 2 * c2;
-      nb = na + 1;
-    }
+    gv_rows(p, c2, na, nb);
     const uint4* wa = reinterpret_cast<const uint4*>(B + ((int64_t)g * p.N + na) * p.K);
     const uint4* wb = reinterpret_cast<const uint4*>(B + ((int64_t)g * p.N + nb) * p.K);
     const int nr = r1 - r0;
@@ -1012,12 +1060,12 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
       vb[u] = c < kv ? __ldg(wb + c) : make_uint4(0, 0, 0, 0);
     }
     for (int c0 = lane; c0 < kv; c0 += 32 * kGvU) {
-      uint4 na[kGvU], nb[kGvU];
+      uint4 na_[kGvU], nb_[kGvU];
 #pragma unroll
       for (int u = 0; u < kGvU; ++u) {
         const int c = c0 + 32 * (kGvU + u);
-        na[u] = c < kv ? __ldg(wa + c) : make_uint4(0, 0, 0, 0);
-        nb[u] = c < kv ? __ldg(wb + c) : make_uint4(0, 0, 0, 0);
+        na_[u] = c < kv ? __ldg(wa + c) : make_uint4(0, 0, 0, 0);
+        nb_[u] = c < kv ? __ldg(wb + c) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < kGvU; ++u) {
@@ -1034,8 +1082,8 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
       }
 #pragma unroll
       for (int u = 0; u < kGvU; ++u) {
-        va[u] = na[u];
-        vb[u] = nb[u];
+        va[u] = na_[u];
+        vb[u] = nb_[u];
       }
     }
 #pragma unroll
@@ -1052,36 +1100,7 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
 #pragma unroll
     for (int m = 0; m < kGvMaxRows; ++m) {
       if (m != lane || m >= nr) continue;
-      const int row = r0 + m;
-      __nv_bfloat16* crow = p.C + (int64_t)row * p.ldc;
-      float x1 = acc_a[m], x2 = acc_b[m];
-      if (p.epi == HAP_EPI_SWIGLU) {
-        crow[c2] = __float2bfloat16_rn(silu(x1) * x2);
-        continue;
-      }
-      if (p.bias) {
-        x1 += __bfloat162float(p.bias[na]);
-        x2 += __bfloat162float(p.bias[nb]);
-      }
-      if (p.epi == kEpiRope) {
-        if (na < p.rope_cols) {
-          const int i = c2 % half;
-          const float inv_freq = 1.0f / powf(p.theta, (float)(2 * i) / (float)d);
-          float sn, cs;
-          rope_sincos((float)p.positions[row] * inv_freq, &sn, &cs);
-          const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
-          x1 = y1;
-          x2 = y2;
-        }
-        crow[na] = __float2bfloat16_rn(x1);
-        crow[nb] = __float2bfloat16_rn(x2);
-        continue;
-      }
-      if (p.resid) {
-        x1 += __bfloat162float(p.resid[(int64_t)row * p.ldr + na]);
-        x2 += __bfloat162float(p.resid[(int64_t)row * p.ldr + nb]);
-      }
-      *reinterpret_cast<uint32_t*>(crow + na) = pack_bf16x2(x1, x2);
+      gv_store(p, r0 + m, c2, na, nb, acc_a[m], acc_b[m]);
     }
   }
 }
