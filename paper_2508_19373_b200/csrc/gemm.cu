@@ -1027,7 +1027,12 @@ __device__ __forceinline__ void gv_store(const Params& p, int row, int c2, int n
   *reinterpret_cast<uint32_t*>(crow + na) = pack_bf16x2(x1, x2);
 }
 
-__global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda,
+// kR: the launch's row bound (2 for the default 1-2-row decode launches: 4
+// accumulators instead of 16 keep the kernel under ~96 registers so 3072
+// warps of a 50 MB QKV stream are resident in one round; same arithmetic per
+// row for every kR, so the results do not depend on it)
+template <int kR>
+__global__ void __launch_bounds__(kGvThreads, kR <= 2 ? 3 : 1) gemv_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda,
                                                           const __nv_bfloat16* __restrict__ B, Params p) {
   pdl_trigger();
   pdl_wait();
@@ -1047,9 +1052,9 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
     const uint4* wa = reinterpret_cast<const uint4*>(B + ((int64_t)g * p.N + na) * p.K);
     const uint4* wb = reinterpret_cast<const uint4*>(B + ((int64_t)g * p.N + nb) * p.K);
     const int nr = r1 - r0;
-    float acc_a[kGvMaxRows], acc_b[kGvMaxRows];
+    float acc_a[kR], acc_b[kR];
 #pragma unroll
-    for (int m = 0; m < kGvMaxRows; ++m) acc_a[m] = acc_b[m] = 0.f;
+    for (int m = 0; m < kR; ++m) acc_a[m] = acc_b[m] = 0.f;
     // software-pipelined: the next group of chunks is in flight while this one
     // is consumed (two groups = 8 KB per warp outstanding)
     uint4 va[kGvU], vb[kGvU];
@@ -1072,7 +1077,7 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
         const int c = c0 + 32 * u;
         if (c >= kv) break;
 #pragma unroll
-        for (int m = 0; m < kGvMaxRows; ++m) {
+        for (int m = 0; m < kR; ++m) {
           if (m < nr) {
             const uint4 x = xs[(r0 + m) * kv + c];
             gv_dot8(va[u], x, acc_a[m]);
@@ -1087,7 +1092,7 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
       }
     }
 #pragma unroll
-    for (int m = 0; m < kGvMaxRows; ++m) {
+    for (int m = 0; m < kR; ++m) {
       if (m < nr) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -1098,7 +1103,7 @@ __global__ void __launch_bounds__(kGvThreads) gemv_kernel(const __nv_bfloat16* _
     }
     // epilogue: lane m writes row r0 + m
 #pragma unroll
-    for (int m = 0; m < kGvMaxRows; ++m) {
+    for (int m = 0; m < kR; ++m) {
       if (m != lane || m >= nr) continue;
       gv_store(p, r0 + m, c2, na, nb, acc_a[m], acc_b[m]);
     }
@@ -1125,15 +1130,17 @@ static int launch_gemv(Params& p, const void* A, int64_t lda, const void* B, voi
   const int smem = p.a_rows * p.K * 2;
   static int configured = 0;
   if (!configured) {
-    if (configure_smem((const void*)gemv_kernel, 200 * 1024)) return HAP_ERR_LAUNCH;
+    if (configure_smem((const void*)gemv_kernel<2>, 200 * 1024)) return HAP_ERR_LAUNCH;
+    if (configure_smem((const void*)gemv_kernel<kGvMaxRows>, 200 * 1024)) return HAP_ERR_LAUNCH;
     configured = 1;
   }
+  auto kern = p.a_rows <= 2 ? gemv_kernel<2> : gemv_kernel<kGvMaxRows>;
   const int64_t items = (int64_t)p.n_segs * (p.N / 2);
   int64_t ctas = (items + (kGvThreads / 32) - 1) / (kGvThreads / 32);
   const int per_sm = smem > 0 ? (int)((220 * 1024) / (smem + 1024)) : 8;
   const int64_t cap = (int64_t)kNumSMs * (per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm));
   if (ctas > cap) ctas = cap;
-  if (hap::launch_kr(p.a_rows, gemv_kernel, dim3((unsigned)ctas), dim3(kGvThreads), smem, reinterpret_cast<cudaStream_t>(stream),
+  if (hap::launch_kr(p.a_rows, kern, dim3((unsigned)ctas), dim3(kGvThreads), smem, reinterpret_cast<cudaStream_t>(stream),
                     reinterpret_cast<const __nv_bfloat16*>(A), lda, reinterpret_cast<const __nv_bfloat16*>(B),
                     p) != cudaSuccess)
     return HAP_ERR_LAUNCH;
