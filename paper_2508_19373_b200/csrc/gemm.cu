@@ -1109,96 +1109,6 @@ __global__ void __launch_bounds__(kGvThreads, kR <= 2 ? 3 : 1) gemv_kernel(const
   }
 }
 
-// Dense 1-2-row GEMV with cp.async weight staging (opt-in HAP_GEMV_ASYNC=1,
-// experiment): a warp owns column pairs gw, gw + G, ...; each lane copies ITS
-// chunks of the next pair's two weight rows into the warp's smem slot with
-// 16-byte cp.async while it computes the current pair from the other slot, so
-// one whole 2 x K x 2-byte pair per warp is in flight without holding
-// registers.  Lane l reduces exactly the chunks it would in gemv_kernel (l,
-// l + 32, ... in order) with the same shuffle tree: bit-identical results.
-constexpr int kGaSmemBytes = 208 * 1024;
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(src) : "memory");
-}
-
-__global__ void __launch_bounds__(256) gemv_async_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda,
-                                                         const __nv_bfloat16* __restrict__ B, Params p) {
-  pdl_trigger();
-  extern __shared__ __align__(128) uint8_t ga_smem[];
-  const int kv = p.K / 8;
-  const int nr = p.a_rows;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  uint4* xs = reinterpret_cast<uint4*>(ga_smem);
-  uint4* slots = xs + nr * kv + (size_t)warp * 4 * kv;  // [2][2 rows][kv]
-  const int n_pairs = p.N / 2;
-  const int G = gridDim.x * nw;
-  const int gw = blockIdx.x * nw + warp;
-  auto issue = [&](int q, int buf) {
-    int na, nb;
-    gv_rows(p, q, na, nb);
-    const uint4* wa = reinterpret_cast<const uint4*>(B + (int64_t)na * p.K);
-    const uint4* wb = reinterpret_cast<const uint4*>(B + (int64_t)nb * p.K);
-    uint4* d = slots + buf * 2 * kv;
-    for (int c = lane; c < kv; c += 32) {
-      cp_async16(d + c, wa + c);
-      cp_async16(d + kv + c, wb + c);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  // the weights depend on no earlier kernel: the first pair streams before pdl_wait
-  if (gw < n_pairs) issue(gw, 0);
-  pdl_wait();
-  gv_stage_rows(xs, A, lda, p, kv);
-  int buf = 0;
-  for (int q = gw; q < n_pairs; q += G, buf ^= 1) {
-    if (q + G < n_pairs) {
-      issue(q + G, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    const uint4* wa = slots + buf * 2 * kv;
-    const uint4* wb = wa + kv;
-    float acc_a[2] = {0.f, 0.f}, acc_b[2] = {0.f, 0.f};
-    for (int c = lane; c < kv; c += 32) {
-      const uint4 va = wa[c], vb = wb[c];
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        if (m < nr) {
-          const uint4 x = xs[m * kv + c];
-          gv_dot8(va, x, acc_a[m]);
-          gv_dot8(vb, x, acc_b[m]);
-        }
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      if (m < nr) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          acc_a[m] += __shfl_xor_sync(0xffffffffu, acc_a[m], o);
-          acc_b[m] += __shfl_xor_sync(0xffffffffu, acc_b[m], o);
-        }
-      }
-    }
-    if (lane < nr) {
-      int na, nb;
-      gv_rows(p, q, na, nb);
-      gv_store(p, lane, q, na, nb, lane == 0 ? acc_a[0] : acc_a[1], lane == 0 ? acc_b[0] : acc_b[1]);
-    }
-  }
-}
-
-// HAP_GEMV_ASYNC=1: dense 1-2-row GEMV launches use gemv_async_kernel (experiment)
-static bool gemv_async_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("HAP_GEMV_ASYNC");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 // HAP_GEMV: 0 = tensor-core tiles for every M; 1 (default) = GEMV for launches
 // of <= 2 activation rows streaming <= 64 MB of weights (decode QKV / O at
 // batch 1-2); 2 = GEMV for every eligible launch of <= 8 rows (experiments).
@@ -1217,28 +1127,6 @@ static int gemv_mode() {
 
 static int launch_gemv(Params& p, const void* A, int64_t lda, const void* B, void* stream) {
   const int smem = p.a_rows * p.K * 2;
-  if (p.seg == nullptr && p.a_rows <= 2 && gemv_async_enabled()) {
-    const int64_t slot = (int64_t)p.K * 8;  // two buffers of two rows per warp
-    int64_t warps = (kGaSmemBytes - smem) / slot;
-    if (warps > 8) warps = 8;
-    if (warps >= 4) {
-      static int ga_configured = 0;
-      if (!ga_configured) {
-        if (configure_smem((const void*)gemv_async_kernel, kGaSmemBytes)) return HAP_ERR_LAUNCH;
-        ga_configured = 1;
-      }
-      const int64_t n_pairs = p.N / 2;
-      int64_t ctas = (n_pairs + warps - 1) / warps;
-      if (ctas > kNumSMs) ctas = kNumSMs;
-      const size_t dsmem = (size_t)smem + (size_t)warps * slot;
-      if (hap::launch_kr(p.a_rows, gemv_async_kernel, dim3((unsigned)ctas), dim3((unsigned)(warps * 32)), dsmem,
-                         reinterpret_cast<cudaStream_t>(stream), reinterpret_cast<const __nv_bfloat16*>(A), lda,
-                         reinterpret_cast<const __nv_bfloat16*>(B), p) != cudaSuccess)
-        return HAP_ERR_LAUNCH;
-      HAP_CHECK_LAUNCH();
-      return HAP_OK;
-    }
-  }
   static int configured = 0;
   if (!configured) {
     if (configure_smem((const void*)gemv_kernel<2>, 200 * 1024)) return HAP_ERR_LAUNCH;

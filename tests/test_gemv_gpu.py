@@ -162,18 +162,3 @@ def test_fused_norm_decode_block_bit_identical():
     finally:
         E._FUSED_NORM = prev
 
-
-def test_gemv_async_variant_bit_identical():
-    """The opt-in cp.async GEMV (HAP_GEMV_ASYNC=1) reproduces the default
-    1-2-row GEMV bit for bit (same per-lane chunk order and shuffle tree)."""
-    if INNER:
-        pytest.skip("default GEMV mode only")
-    worker = str(ROOT / "tests" / "gemv_hash_worker.py")
-    hashes = []
-    for env_async in ("0", "1"):
-        env = dict(os.environ, HAP_GEMV_ASYNC=env_async)
-        env.pop("HAP_GEMV", None)
-        out = subprocess.run([sys.executable, worker], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
-        assert out.returncode == 0, out.stderr[-2000:]
-        hashes.append(out.stdout.strip().splitlines()[-1])
-    assert hashes[0] == hashes[1], hashes
