@@ -255,8 +255,8 @@ def rmsnorm_qkv_rope(x: torch.Tensor, norm_w: torch.Tensor, eps: float, w: torch
     if out is None:
         out = torch.empty(M, N, device=x.device, dtype=BF16)
     _need(out, "out", BF16); _rowmajor(out, "out")
-    if M <= 2:  # the GEMV path never writes hn: a persistent scratch, no allocation per call
-        key = (x.device, K)
+    if M <= 2:  # the GEMV path never writes hn: a persistent scratch per stream, no allocation per call
+        key = (x.device, K, _stream())
         hn = _HN_SCRATCH.get(key)
         if hn is None:
             hn = _HN_SCRATCH[key] = torch.empty(2, K, device=x.device, dtype=BF16)

@@ -259,7 +259,7 @@ def _weights_key(w):
 
 def _phase_key(cfg, w, lay_src, lay_dst):
     return (cfg.hidden, cfg.inter, cfg.n_experts, cfg.n_shared, cfg.n_q_heads, cfg.n_kv_heads,
-            lay_src.deg, lay_src.rank, lay_dst.deg, _weights_key(w))
+            lay_src.deg, lay_src.rank, lay_dst.deg, str(w.w13.device), _weights_key(w))
 
 
 def _static_plan(cfg, lay_src, lay_dst):
